@@ -1,0 +1,192 @@
+/*
+ * klb200.h — C ABI of the B200 Kernel Launcher backend (libklb200.so).
+ *
+ * Plain C types only (no torch, no C++): this is the boundary a binding in any
+ * host language links against.  Python binds it with ctypes in
+ * paper_2303_12374_b200/cuda/_abi.py; INTEGRATION.md shows the stub the
+ * reference package would add.
+ *
+ * Which reference interface each group replaces (reference = the kltune
+ * package, /root/reference/pkg/src/kltune):
+ *   klb_init / klb_device_info     -> DeviceIdent construction     backend.py:47-66
+ *   klb_compile                    -> CompilerInterface.compile    backend.py:274-277
+ *                                     (SubprocessCompiler.compile  backend.py:399-416)
+ *   klb_module_load / _function    -> ExecutableHandle.load        backend.py:265-267
+ *   klb_launch                     -> ExecutableHandle.launch      backend.py:269-271
+ *   klb_time_launches              -> Executor.measure's timed reps backend.py:226-257, 442-468
+ *   klb_synth_field                -> synthetic capture payloads   capture.py:75-98 (BufferArg.data)
+ *   klb_halo_* (NCCL)              -> no reference counterpart (multi-GPU z-slabs)
+ *
+ * Conventions: every function returns 0 on success or a nonzero code
+ * (a CUresult, nvrtcResult + 10000, ncclResult_t + 20000, or KLB_E_* below);
+ * klb_last_error() then returns a thread-local human-readable message.
+ * Device pointers travel as uint64_t.  Streams/events/modules/functions/
+ * communicators are opaque handles (void*).  A NULL stream is the legacy
+ * default stream.
+ */
+#ifndef KLB200_H
+#define KLB200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define KLB_ABI_VERSION 1
+
+#define KLB_E_INVALID 30001   /* bad argument */
+#define KLB_E_NO_NCCL 30002   /* libnccl.so.2 could not be loaded */
+#define KLB_E_COMPILE 30003   /* NVRTC compile failed (log returned) */
+#define KLB_E_NOT_INIT 30004  /* klb_init not called on this process */
+#define KLB_E_NO_DRIVER 30005 /* no usable CUDA driver (libcuda) on this host */
+
+typedef void* klb_stream;
+typedef void* klb_event;
+typedef void* klb_module;
+typedef void* klb_function;
+typedef void* klb_comm;
+
+typedef struct klb_device_info {
+  char name[256];
+  int ordinal;
+  int cc_major;
+  int cc_minor;
+  int sm_count;
+  int l2_bytes;
+  int max_smem_per_block_optin;
+  int max_smem_per_sm;
+  int max_threads_per_sm;
+  int max_threads_per_block;
+  int regs_per_sm;
+  int warp_size;
+  int clock_khz;
+  int mem_clock_khz;
+  int mem_bus_width_bits;
+  int pci_bus_id;
+  int driver_version;
+  size_t total_mem_bytes;
+  unsigned char uuid[16];
+} klb_device_info;
+
+typedef struct klb_func_attrs {
+  int num_regs;
+  int local_bytes;
+  int static_smem_bytes;
+  int max_threads_per_block;
+  int max_dynamic_smem_bytes;
+  int ptx_version;
+  int binary_version;
+} klb_func_attrs;
+
+/* ---- library / device -------------------------------------------------- */
+int klb_abi_version(void);
+const char* klb_last_error(void);
+int klb_device_count(int* count);
+/* cuInit, retain the primary context of `ordinal`, make it current on the
+ * calling thread, fill `info` (may be NULL). */
+int klb_init(int ordinal, klb_device_info* info);
+/* Make `ordinal`'s primary context current on the calling thread. */
+int klb_set_device(int ordinal);
+int klb_device_synchronize(void);
+
+/* ---- NVRTC (replaces the reference CompilerInterface.compile) ---------- */
+int klb_nvrtc_version(int* major, int* minor);
+/* Compile `source` to a CUBIN.  `entry` is the kernel name as it appears in
+ * the reference CompileRequest.entry ("name" or "name<args>"); it is passed to
+ * nvrtcAddNameExpression and the lowered (mangled) name is returned.
+ * options: NVRTC option strings (e.g. "--gpu-architecture=sm_100a",
+ * "-D TILE_X=2", "-std=c++17").  On success *image/*image_size hold the CUBIN
+ * and *lowered_name the symbol; on failure (KLB_E_COMPILE) *log holds the
+ * compiler log.  Free all returned buffers with klb_free. */
+int klb_compile(const char* source, const char* program_name, const char* entry,
+                const char* const* options, int n_options,
+                void** image, size_t* image_size, char** lowered_name, char** log);
+void klb_free(void* p);
+
+/* ---- modules / launch (replaces ExecutableHandle.load / .launch) ------- */
+int klb_module_load(const void* image, klb_module* module);
+int klb_module_unload(klb_module module);
+int klb_module_function(klb_module module, const char* lowered_name, klb_function* fn);
+int klb_function_attributes(klb_function fn, klb_func_attrs* attrs);
+int klb_function_set_max_dynamic_smem(klb_function fn, int bytes);
+int klb_occupancy_blocks_per_sm(klb_function fn, int block_threads, int dynamic_smem, int* blocks);
+/* Asynchronous launch; `params` is the usual cuLaunchKernel array of
+ * pointers to each argument value. */
+int klb_launch(klb_function fn, const unsigned grid[3], const unsigned block[3],
+               unsigned dynamic_smem, klb_stream stream, void** params);
+/* Timed replay: `warmup` untimed launches, then `reps` launches each bracketed
+ * by events on `stream`; when flush_bytes > 0 the buffer at flush_ptr is
+ * overwritten before every launch (outside the timed window) so each launch
+ * starts from a cold L2.  Writes `reps` kernel times in milliseconds. */
+int klb_time_launches(klb_function fn, const unsigned grid[3], const unsigned block[3],
+                      unsigned dynamic_smem, klb_stream stream, void** params,
+                      int warmup, int reps, uint64_t flush_ptr, size_t flush_bytes,
+                      float* ms_out);
+
+/* ---- memory ------------------------------------------------------------ */
+int klb_mem_alloc(size_t bytes, uint64_t* dptr);
+int klb_mem_free(uint64_t dptr);
+int klb_mem_get_info(size_t* free_bytes, size_t* total_bytes);
+int klb_host_alloc(size_t bytes, void** host_ptr);   /* pinned, portable */
+int klb_host_free(void* host_ptr);
+int klb_memcpy_htod(uint64_t dst, const void* src, size_t bytes, klb_stream stream);
+int klb_memcpy_dtoh(void* dst, uint64_t src, size_t bytes, klb_stream stream);
+int klb_memcpy_dtod(uint64_t dst, uint64_t src, size_t bytes, klb_stream stream);
+int klb_memset_d8(uint64_t dst, unsigned char value, size_t bytes, klb_stream stream);
+
+/* ---- streams / events ----------------------------------------------------- */
+int klb_stream_create(klb_stream* stream, int priority);
+int klb_stream_destroy(klb_stream stream);
+int klb_stream_synchronize(klb_stream stream);
+int klb_stream_wait_event(klb_stream stream, klb_event event);
+int klb_event_create(klb_event* event);
+int klb_event_destroy(klb_event event);
+int klb_event_record(klb_event event, klb_stream stream);
+int klb_event_synchronize(klb_event event);
+int klb_event_elapsed_ms(klb_event start, klb_event stop, float* ms);
+
+/* ---- synthetic fields (device twin of oracle/synth.py) --------------------
+ * Fills a ghost-padded field: element (i, j, k) of the local array, stored at
+ * dptr[base_offset + i + j*jj + k*kk] with elem_bytes 4 (fp32) or 8 (fp64),
+ * receives
+ *     lo + (hi - lo) * ((mix64(seed + (n+1)*GOLDEN) >> 11) * 2^-53)
+ * where n = ((k+k_offset)*jcells + j')*icells + i' is the GLOBAL logical index
+ * and (i', j') are (i, j) wrapped periodically into the interior when
+ * periodic_xy != 0.  Only the icells x jcells x kcells_local box is written;
+ * pitch padding is left untouched (callers zero the allocation first). */
+int klb_synth_field(uint64_t dptr, int elem_bytes, long long base_offset,
+                    int icells, int jcells, int kcells_local, int jj, long long kk,
+                    int igc, int jgc, int k_offset, int kcells_global,
+                    uint64_t seed, double lo, double hi, int periodic_xy, klb_stream stream);
+/* max |a - b| and max |b| over the interior of two equally laid-out fields
+ * (device reduction; used by the replay executor's verification step). */
+int klb_compare_fields(uint64_t a, uint64_t b, int elem_bytes, long long base_offset,
+                       int istart, int iend, int jstart, int jend, int kstart, int kend,
+                       int jj, long long kk, double* max_abs_diff, double* max_abs_ref,
+                       klb_stream stream);
+
+/* ---- multi-GPU halo exchange over NCCL (z-slab decomposition) ----------- */
+int klb_nccl_version(int* version);
+int klb_nccl_unique_id(unsigned char id_out[128]);
+int klb_nccl_comm_init(klb_comm* comm, int nranks, const unsigned char id[128], int rank);
+int klb_nccl_comm_destroy(klb_comm comm);
+/* Exchange contiguous z-planes of `nfields` fields with the ranks below/above
+ * (-1 = none).  Every rank passes the same plane counts.  For each field base
+ * pointer (local element (0,0,0), plane stride kk elements):
+ *   send planes [kstart, kstart+n_down) to rank_below   (its top ghost planes),
+ *   recv planes [kstart-n_up, kstart)   from rank_below  (its top interior),
+ *   send planes [kend-n_up, kend)       to rank_above   (its bottom ghost planes),
+ *   recv planes [kend, kend+n_down)     from rank_above  (its bottom interior),
+ * all inside one ncclGroupStart/End on `stream`.  n_down is the stencil's
+ * reach towards +k (planes a rank reads above its slab), n_up its reach
+ * towards -k. */
+int klb_halo_exchange_z(klb_comm comm, klb_stream stream, int nfields, const uint64_t* fields,
+                        int elem_bytes, long long kk, int kstart, int kend,
+                        int n_down, int n_up, int rank_below, int rank_above);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* KLB200_H */

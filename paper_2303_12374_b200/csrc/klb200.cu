@@ -1,0 +1,732 @@
+// libklb200.so — C-ABI backend: CUDA driver + NVRTC + NCCL plumbing and the
+// device-side helpers (synthetic fields, field comparison) for the B200
+// Kernel Launcher.  Declared in include/klb200.h; see that header for which
+// reference (kltune) interface each entry point replaces.
+//
+// Build (see __graft_entry__.build / Makefile):
+//   nvcc -O3 -std=c++17 -shared -Xcompiler -fPIC -lineinfo \
+//        -gencode arch=compute_100a,code=sm_100a -I include \
+//        csrc/klb200.cu -o libklb200.so -lnvrtc -ldl      (no -lcuda: see DriverApi)
+//
+// The stencil kernels themselves are NOT in this library: they are compiled
+// at runtime by NVRTC (klb_compile) from paper_2303_12374_b200/stencils/*.cu
+// with the tunable parameters of the selected configuration as -D defines,
+// exactly the Kernel Launcher model.
+
+#include "klb200.h"
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nvrtc.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "/usr/include/nccl.h"
+
+namespace {
+
+thread_local std::string tl_error;
+std::mutex g_mu;
+CUcontext g_ctx[64] = {};
+int g_default_ordinal = -1;
+
+// ---------------------------------------------------------------------------
+// CUDA driver API, resolved at runtime through cudaGetDriverEntryPoint so the
+// library has no link-time dependency on libcuda.so.1: it loads (and reports
+// a clean error from klb_init) on hosts without an NVIDIA driver.
+#define KLB_DRIVER_API(X) X(cuCtxGetCurrent) X(cuCtxSetCurrent) X(cuCtxSynchronize) X(cuDeviceGet) X(cuDeviceGetAttribute) X(cuDeviceGetCount) X(cuDeviceGetName) X(cuDeviceGetUuid) X(cuDevicePrimaryCtxRetain) X(cuDeviceTotalMem) X(cuDriverGetVersion) X(cuEventCreate) X(cuEventDestroy) X(cuEventElapsedTime) X(cuEventRecord) X(cuEventSynchronize) X(cuFuncGetAttribute) X(cuFuncSetAttribute) X(cuGetErrorName) X(cuGetErrorString) X(cuInit) X(cuLaunchKernel) X(cuMemAlloc) X(cuMemFree) X(cuMemFreeHost) X(cuMemGetInfo) X(cuMemHostAlloc) X(cuMemcpyDtoDAsync) X(cuMemcpyDtoHAsync) X(cuMemcpyHtoDAsync) X(cuMemsetD32Async) X(cuMemsetD8Async) X(cuModuleGetFunction) X(cuModuleLoadData) X(cuModuleUnload) X(cuOccupancyMaxActiveBlocksPerMultiprocessor) X(cuStreamCreateWithPriority) X(cuStreamDestroy) X(cuStreamSynchronize) X(cuStreamWaitEvent)
+
+struct DriverApi {
+#define KLB_DECL(name) decltype(&::name) name = nullptr;
+  KLB_DRIVER_API(KLB_DECL)
+#undef KLB_DECL
+  bool ready = false;
+} drv;
+
+int load_driver_api() {
+  static std::once_flag once;
+  static int status = -1;
+  static std::string why;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+#define KLB_RESOLVE(name)                                                                         \
+  if (status < 0) {                                                                               \
+    void* fp = nullptr;                                                                           \
+    cudaError_t e = cudaGetDriverEntryPoint(#name, &fp, cudaEnableDefault, &q);                   \
+    if (e != cudaSuccess || !fp || q != cudaDriverEntryPointSuccess) {                            \
+      why = std::string("cannot resolve CUDA driver symbol " #name ": ") + cudaGetErrorString(e); \
+      status = 1;                                                                                 \
+    } else {                                                                                      \
+      drv.name = reinterpret_cast<decltype(drv.name)>(fp);                                        \
+    }                                                                                             \
+  }
+    KLB_DRIVER_API(KLB_RESOLVE)
+#undef KLB_RESOLVE
+    if (status < 0) {
+      status = 0;
+      drv.ready = true;
+    }
+  });
+  if (status != 0) {
+    tl_error = why;
+    return KLB_E_NO_DRIVER;
+  }
+  return 0;
+}
+
+int fail(int code, const char* fmt, ...) {
+  char buf[2048];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  tl_error = buf;
+  return code;
+}
+
+int cu_fail(CUresult r, const char* what) {
+  const char* name = nullptr;
+  const char* desc = nullptr;
+  if (drv.ready) {
+    drv.cuGetErrorName(r, &name);
+    drv.cuGetErrorString(r, &desc);
+  }
+  return fail(static_cast<int>(r), "%s failed: %s (%s)", what, name ? name : "?", desc ? desc : "?");
+}
+
+#define CU_TRY(call)                              \
+  do {                                            \
+    CUresult _r = (call);                         \
+    if (_r != CUDA_SUCCESS) return cu_fail(_r, #call); \
+  } while (0)
+
+// Make sure a context is current on the calling thread (ctypes callers may
+// come from any Python thread).
+int ensure_ctx() {
+  if (int e = load_driver_api()) return e;
+  CUcontext cur = nullptr;
+  if (drv.cuCtxGetCurrent(&cur) == CUDA_SUCCESS && cur != nullptr) return 0;
+  if (g_default_ordinal < 0) return fail(KLB_E_NOT_INIT, "klb_init has not been called");
+  CU_TRY(drv.cuCtxSetCurrent(g_ctx[g_default_ordinal]));
+  cudaSetDevice(g_default_ordinal);
+  return 0;
+}
+
+#define CTX_TRY()                  \
+  do {                             \
+    int _e = ensure_ctx();         \
+    if (_e) return _e;             \
+  } while (0)
+
+inline CUstream as_stream(klb_stream s) { return reinterpret_cast<CUstream>(s); }
+
+// ---------------------------------------------------------------------------
+// NCCL, resolved at runtime so the library loads on hosts without it.
+struct NcclApi {
+  bool tried = false;
+  void* handle = nullptr;
+  ncclResult_t (*getVersion)(int*) = nullptr;
+  ncclResult_t (*getUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*groupStart)() = nullptr;
+  ncclResult_t (*groupEnd)() = nullptr;
+  ncclResult_t (*send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  const char* (*errorString)(ncclResult_t) = nullptr;
+} g_nccl;
+
+int nccl_load() {
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (g_nccl.tried) return g_nccl.handle ? 0 : fail(KLB_E_NO_NCCL, "libnccl.so.2 unavailable");
+  g_nccl.tried = true;
+  const char* env = getenv("KLB_NCCL_LIBRARY");
+  const char* names[] = {env, "libnccl.so.2", "libnccl.so"};
+  for (const char* n : names) {
+    if (!n) continue;
+    g_nccl.handle = dlopen(n, RTLD_NOW | RTLD_GLOBAL);
+    if (g_nccl.handle) break;
+  }
+  if (!g_nccl.handle) return fail(KLB_E_NO_NCCL, "dlopen(libnccl.so.2) failed: %s", dlerror());
+#define SYM(field, name)                                                         \
+  g_nccl.field = reinterpret_cast<decltype(g_nccl.field)>(dlsym(g_nccl.handle, name)); \
+  if (!g_nccl.field) { g_nccl.handle = nullptr; return fail(KLB_E_NO_NCCL, "missing NCCL symbol %s", name); }
+  SYM(getVersion, "ncclGetVersion");
+  SYM(getUniqueId, "ncclGetUniqueId");
+  SYM(commInitRank, "ncclCommInitRank");
+  SYM(commDestroy, "ncclCommDestroy");
+  SYM(groupStart, "ncclGroupStart");
+  SYM(groupEnd, "ncclGroupEnd");
+  SYM(send, "ncclSend");
+  SYM(recv, "ncclRecv");
+  SYM(errorString, "ncclGetErrorString");
+#undef SYM
+  return 0;
+}
+
+int nccl_fail(ncclResult_t r, const char* what) {
+  return fail(20000 + static_cast<int>(r), "%s failed: %s", what,
+              g_nccl.errorString ? g_nccl.errorString(r) : "?");
+}
+
+// ---------------------------------------------------------------------------
+// Device helpers
+
+__device__ __forceinline__ unsigned long long mix64(unsigned long long z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+template <typename T>
+__global__ void synth_kernel(T* __restrict__ base, long long total, int icells, int jcells, int jj,
+                             long long kk, int igc, int jgc, int k_offset, unsigned long long seed,
+                             double lo, double span, int periodic) {
+  const int itot = icells - 2 * igc;
+  const int jtot = jcells - 2 * jgc;
+  const long long plane = static_cast<long long>(icells) * jcells;
+  for (long long t = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; t < total;
+       t += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int k = static_cast<int>(t / plane);
+    const long long r = t - static_cast<long long>(k) * plane;
+    const int j = static_cast<int>(r / icells);
+    const int i = static_cast<int>(r - static_cast<long long>(j) * icells);
+    int is = i, js = j;
+    if (periodic) {
+      is = igc + ((i - igc) % itot + itot) % itot;
+      js = jgc + ((j - jgc) % jtot + jtot) % jtot;
+    }
+    const unsigned long long n =
+        (static_cast<unsigned long long>(k + k_offset) * jcells + js) * icells + is;
+    const unsigned long long h = mix64(seed + (n + 1ull) * 0x9E3779B97F4A7C15ull);
+    const double x = static_cast<double>(h >> 11) * 0x1.0p-53;
+    const double v = __dadd_rn(lo, __dmul_rn(span, x));
+    base[i + static_cast<long long>(j) * jj + static_cast<long long>(k) * kk] = static_cast<T>(v);
+  }
+}
+
+__device__ __forceinline__ void atomic_max_nonneg(double* addr, double v) {
+  // IEEE ordering of non-negative doubles equals unsigned ordering of their bits.
+  atomicMax(reinterpret_cast<unsigned long long*>(addr), static_cast<unsigned long long>(__double_as_longlong(v)));
+}
+
+template <typename T>
+__global__ void compare_kernel(const T* __restrict__ a, const T* __restrict__ b, int istart, int iend,
+                               int jstart, int jend, int kstart, int kend, int jj, long long kk,
+                               double* out) {
+  const int ni = iend - istart, nj = jend - jstart;
+  const long long total = static_cast<long long>(ni) * nj * (kend - kstart);
+  double dmax = 0.0, rmax = 0.0;
+  for (long long t = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; t < total;
+       t += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long kq = t / (static_cast<long long>(ni) * nj);
+    const long long r = t - kq * ni * nj;
+    const int j = static_cast<int>(r / ni) + jstart;
+    const int i = static_cast<int>(r % ni) + istart;
+    const long long ijk = i + static_cast<long long>(j) * jj + (kq + kstart) * kk;
+    const double av = static_cast<double>(a[ijk]);
+    const double bv = static_cast<double>(b[ijk]);
+    double d = fabs(av - bv);
+    if (!(d == d)) d = INFINITY;  // NaN counts as an unbounded error
+    double m = fabs(bv);
+    if (!(m == m)) m = INFINITY;
+    dmax = fmax(dmax, d);
+    rmax = fmax(rmax, m);
+  }
+  for (int off = 16; off > 0; off >>= 1) {
+    dmax = fmax(dmax, __shfl_xor_sync(0xffffffffu, dmax, off));
+    rmax = fmax(rmax, __shfl_xor_sync(0xffffffffu, rmax, off));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomic_max_nonneg(out, dmax);
+    atomic_max_nonneg(out + 1, rmax);
+  }
+}
+
+int grid_for(long long work, int threads) {
+  long long blocks = (work + threads - 1) / threads;
+  int sms = 148;
+  int dev = g_default_ordinal < 0 ? 0 : g_default_ordinal;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const long long cap = static_cast<long long>(sms) * 16;
+  if (blocks > cap) blocks = cap;
+  if (blocks < 1) blocks = 1;
+  return static_cast<int>(blocks);
+}
+
+}  // namespace
+
+// ===========================================================================
+extern "C" {
+
+int klb_abi_version(void) { return KLB_ABI_VERSION; }
+
+const char* klb_last_error(void) { return tl_error.c_str(); }
+
+int klb_device_count(int* count) {
+  if (!count) return fail(KLB_E_INVALID, "count is NULL");
+  if (int e = load_driver_api()) return e;
+  CU_TRY(drv.cuInit(0));
+  CU_TRY(drv.cuDeviceGetCount(count));
+  return 0;
+}
+
+int klb_init(int ordinal, klb_device_info* info) {
+  if (ordinal < 0 || ordinal >= 64) return fail(KLB_E_INVALID, "bad device ordinal %d", ordinal);
+  if (int e = load_driver_api()) return e;
+  CU_TRY(drv.cuInit(0));
+  CUdevice dev;
+  CU_TRY(drv.cuDeviceGet(&dev, ordinal));
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (!g_ctx[ordinal]) CU_TRY(drv.cuDevicePrimaryCtxRetain(&g_ctx[ordinal], dev));
+    if (g_default_ordinal < 0) g_default_ordinal = ordinal;
+  }
+  CU_TRY(drv.cuCtxSetCurrent(g_ctx[ordinal]));
+  if (cudaSetDevice(ordinal) != cudaSuccess) return fail(KLB_E_INVALID, "cudaSetDevice(%d) failed", ordinal);
+  if (!info) return 0;
+  std::memset(info, 0, sizeof(*info));
+  CU_TRY(drv.cuDeviceGetName(info->name, sizeof(info->name) - 1, dev));
+  info->ordinal = ordinal;
+  auto attr = [&](CUdevice_attribute a, int* dst) { return drv.cuDeviceGetAttribute(dst, a, dev); };
+  CU_TRY(attr(CU_DEVICE_ATTRIBUTE_COMPUTE_CAPABILITY_MAJOR, &info->cc_major));
+  CU_TRY(attr(CU_DEVICE_ATTRIBUTE_COMPUTE_CAPABILITY_MINOR, &info->cc_minor));
+  CU_TRY(attr(CU_DEVICE_ATTRIBUTE_MULTIPROCESSOR_COUNT, &info->sm_count));
+  CU_TRY(attr(CU_DEVICE_ATTRIBUTE_L2_CACHE_SIZE, &info->l2_bytes));
+  CU_TRY(attr(CU_DEVICE_ATTRIBUTE_MAX_SHARED_MEMORY_PER_BLOCK_OPTIN, &info->max_smem_per_block_optin));
+  CU_TRY(attr(CU_DEVICE_ATTRIBUTE_MAX_SHARED_MEMORY_PER_MULTIPROCESSOR, &info->max_smem_per_sm));
+  CU_TRY(attr(CU_DEVICE_ATTRIBUTE_MAX_THREADS_PER_MULTIPROCESSOR, &info->max_threads_per_sm));
+  CU_TRY(attr(CU_DEVICE_ATTRIBUTE_MAX_THREADS_PER_BLOCK, &info->max_threads_per_block));
+  CU_TRY(attr(CU_DEVICE_ATTRIBUTE_MAX_REGISTERS_PER_MULTIPROCESSOR, &info->regs_per_sm));
+  CU_TRY(attr(CU_DEVICE_ATTRIBUTE_WARP_SIZE, &info->warp_size));
+  CU_TRY(attr(CU_DEVICE_ATTRIBUTE_CLOCK_RATE, &info->clock_khz));
+  CU_TRY(attr(CU_DEVICE_ATTRIBUTE_MEMORY_CLOCK_RATE, &info->mem_clock_khz));
+  CU_TRY(attr(CU_DEVICE_ATTRIBUTE_GLOBAL_MEMORY_BUS_WIDTH, &info->mem_bus_width_bits));
+  CU_TRY(attr(CU_DEVICE_ATTRIBUTE_PCI_BUS_ID, &info->pci_bus_id));
+  CU_TRY(drv.cuDriverGetVersion(&info->driver_version));
+  CU_TRY(drv.cuDeviceTotalMem(&info->total_mem_bytes, dev));
+  CUuuid uuid;
+  CU_TRY(drv.cuDeviceGetUuid(&uuid, dev));
+  std::memcpy(info->uuid, uuid.bytes, 16);
+  return 0;
+}
+
+int klb_set_device(int ordinal) {
+  if (ordinal < 0 || ordinal >= 64 || !g_ctx[ordinal]) return fail(KLB_E_NOT_INIT, "device %d not initialised", ordinal);
+  if (int e = load_driver_api()) return e;
+  CU_TRY(drv.cuCtxSetCurrent(g_ctx[ordinal]));
+  cudaSetDevice(ordinal);
+  return 0;
+}
+
+int klb_device_synchronize(void) {
+  CTX_TRY();
+  CU_TRY(drv.cuCtxSynchronize());
+  return 0;
+}
+
+// ---- NVRTC ----------------------------------------------------------------
+
+int klb_nvrtc_version(int* major, int* minor) {
+  nvrtcResult r = nvrtcVersion(major, minor);
+  if (r != NVRTC_SUCCESS) return fail(10000 + r, "nvrtcVersion: %s", nvrtcGetErrorString(r));
+  return 0;
+}
+
+int klb_compile(const char* source, const char* program_name, const char* entry,
+                const char* const* options, int n_options, void** image, size_t* image_size,
+                char** lowered_name, char** log) {
+  if (!source || !entry || !image || !image_size || !lowered_name)
+    return fail(KLB_E_INVALID, "klb_compile: NULL argument");
+  *image = nullptr;
+  *image_size = 0;
+  *lowered_name = nullptr;
+  if (log) *log = nullptr;
+  nvrtcProgram prog;
+  nvrtcResult r = nvrtcCreateProgram(&prog, source, program_name ? program_name : "kernel.cu", 0, nullptr, nullptr);
+  if (r != NVRTC_SUCCESS) return fail(10000 + r, "nvrtcCreateProgram: %s", nvrtcGetErrorString(r));
+  struct Guard {
+    nvrtcProgram* p;
+    ~Guard() { nvrtcDestroyProgram(p); }
+  } guard{&prog};
+  r = nvrtcAddNameExpression(prog, entry);
+  if (r != NVRTC_SUCCESS) return fail(10000 + r, "nvrtcAddNameExpression(%s): %s", entry, nvrtcGetErrorString(r));
+  const nvrtcResult cr = nvrtcCompileProgram(prog, n_options, options);
+  size_t log_size = 0;
+  nvrtcGetProgramLogSize(prog, &log_size);
+  if (log && log_size > 1) {
+    *log = static_cast<char*>(malloc(log_size));
+    nvrtcGetProgramLog(prog, *log);
+  }
+  if (cr != NVRTC_SUCCESS) return fail(KLB_E_COMPILE, "NVRTC compile of %s failed: %s", entry, nvrtcGetErrorString(cr));
+  const char* lowered = nullptr;
+  r = nvrtcGetLoweredName(prog, entry, &lowered);
+  if (r != NVRTC_SUCCESS || !lowered) return fail(10000 + r, "nvrtcGetLoweredName(%s) failed", entry);
+  *lowered_name = strdup(lowered);
+  size_t n = 0;
+  r = nvrtcGetCUBINSize(prog, &n);
+  if (r != NVRTC_SUCCESS || n == 0)
+    return fail(10000 + r, "nvrtcGetCUBINSize failed (is --gpu-architecture a real sm_ target?)");
+  *image = malloc(n);
+  r = nvrtcGetCUBIN(prog, static_cast<char*>(*image));
+  if (r != NVRTC_SUCCESS) {
+    free(*image);
+    *image = nullptr;
+    return fail(10000 + r, "nvrtcGetCUBIN: %s", nvrtcGetErrorString(r));
+  }
+  *image_size = n;
+  return 0;
+}
+
+void klb_free(void* p) { free(p); }
+
+// ---- modules ---------------------------------------------------------------
+
+int klb_module_load(const void* image, klb_module* module) {
+  if (!image || !module) return fail(KLB_E_INVALID, "klb_module_load: NULL argument");
+  CTX_TRY();
+  CUmodule m;
+  CU_TRY(drv.cuModuleLoadData(&m, image));
+  *module = m;
+  return 0;
+}
+
+int klb_module_unload(klb_module module) {
+  CTX_TRY();
+  CU_TRY(drv.cuModuleUnload(reinterpret_cast<CUmodule>(module)));
+  return 0;
+}
+
+int klb_module_function(klb_module module, const char* lowered_name, klb_function* fn) {
+  CTX_TRY();
+  CUfunction f;
+  CU_TRY(drv.cuModuleGetFunction(&f, reinterpret_cast<CUmodule>(module), lowered_name));
+  *fn = f;
+  return 0;
+}
+
+int klb_function_attributes(klb_function fn, klb_func_attrs* a) {
+  CTX_TRY();
+  CUfunction f = reinterpret_cast<CUfunction>(fn);
+  CU_TRY(drv.cuFuncGetAttribute(&a->num_regs, CU_FUNC_ATTRIBUTE_NUM_REGS, f));
+  CU_TRY(drv.cuFuncGetAttribute(&a->local_bytes, CU_FUNC_ATTRIBUTE_LOCAL_SIZE_BYTES, f));
+  CU_TRY(drv.cuFuncGetAttribute(&a->static_smem_bytes, CU_FUNC_ATTRIBUTE_SHARED_SIZE_BYTES, f));
+  CU_TRY(drv.cuFuncGetAttribute(&a->max_threads_per_block, CU_FUNC_ATTRIBUTE_MAX_THREADS_PER_BLOCK, f));
+  CU_TRY(drv.cuFuncGetAttribute(&a->max_dynamic_smem_bytes, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, f));
+  CU_TRY(drv.cuFuncGetAttribute(&a->ptx_version, CU_FUNC_ATTRIBUTE_PTX_VERSION, f));
+  CU_TRY(drv.cuFuncGetAttribute(&a->binary_version, CU_FUNC_ATTRIBUTE_BINARY_VERSION, f));
+  return 0;
+}
+
+int klb_function_set_max_dynamic_smem(klb_function fn, int bytes) {
+  CTX_TRY();
+  CU_TRY(drv.cuFuncSetAttribute(reinterpret_cast<CUfunction>(fn), CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, bytes));
+  return 0;
+}
+
+int klb_occupancy_blocks_per_sm(klb_function fn, int block_threads, int dynamic_smem, int* blocks) {
+  CTX_TRY();
+  CU_TRY(drv.cuOccupancyMaxActiveBlocksPerMultiprocessor(blocks, reinterpret_cast<CUfunction>(fn), block_threads,
+                                                     static_cast<size_t>(dynamic_smem)));
+  return 0;
+}
+
+int klb_launch(klb_function fn, const unsigned grid[3], const unsigned block[3], unsigned dynamic_smem,
+               klb_stream stream, void** params) {
+  CTX_TRY();
+  CU_TRY(drv.cuLaunchKernel(reinterpret_cast<CUfunction>(fn), grid[0], grid[1], grid[2], block[0], block[1], block[2],
+                        dynamic_smem, as_stream(stream), params, nullptr));
+  return 0;
+}
+
+int klb_time_launches(klb_function fn, const unsigned grid[3], const unsigned block[3], unsigned dynamic_smem,
+                      klb_stream stream, void** params, int warmup, int reps, uint64_t flush_ptr,
+                      size_t flush_bytes, float* ms_out) {
+  if (reps < 1 || !ms_out) return fail(KLB_E_INVALID, "reps must be >= 1");
+  CTX_TRY();
+  CUfunction f = reinterpret_cast<CUfunction>(fn);
+  CUstream s = as_stream(stream);
+  for (int w = 0; w < warmup; ++w)
+    CU_TRY(drv.cuLaunchKernel(f, grid[0], grid[1], grid[2], block[0], block[1], block[2], dynamic_smem, s, params, nullptr));
+  std::vector<CUevent> ev(2 * static_cast<size_t>(reps), nullptr);
+  int rc = 0;
+  for (auto& e : ev) {
+    CUresult r = drv.cuEventCreate(&e, CU_EVENT_DEFAULT);
+    if (r != CUDA_SUCCESS) { rc = cu_fail(r, "cuEventCreate"); break; }
+  }
+  for (int i = 0; rc == 0 && i < reps; ++i) {
+    CUresult r = CUDA_SUCCESS;
+    if (flush_bytes >= 4)
+      r = drv.cuMemsetD32Async(static_cast<CUdeviceptr>(flush_ptr), 0x9E3779B9u + i, flush_bytes / 4, s);
+    if (r == CUDA_SUCCESS) r = drv.cuEventRecord(ev[2 * i], s);
+    if (r == CUDA_SUCCESS)
+      r = drv.cuLaunchKernel(f, grid[0], grid[1], grid[2], block[0], block[1], block[2], dynamic_smem, s, params, nullptr);
+    if (r == CUDA_SUCCESS) r = drv.cuEventRecord(ev[2 * i + 1], s);
+    if (r != CUDA_SUCCESS) rc = cu_fail(r, "timed launch");
+  }
+  if (rc == 0) {
+    CUresult r = drv.cuStreamSynchronize(s);
+    if (r != CUDA_SUCCESS) rc = cu_fail(r, "cuStreamSynchronize");
+  }
+  for (int i = 0; rc == 0 && i < reps; ++i) {
+    CUresult r = drv.cuEventElapsedTime(&ms_out[i], ev[2 * i], ev[2 * i + 1]);
+    if (r != CUDA_SUCCESS) rc = cu_fail(r, "cuEventElapsedTime");
+  }
+  for (auto& e : ev)
+    if (e) drv.cuEventDestroy(e);
+  return rc;
+}
+
+// ---- memory ----------------------------------------------------------------
+
+int klb_mem_alloc(size_t bytes, uint64_t* dptr) {
+  CTX_TRY();
+  CUdeviceptr p;
+  CU_TRY(drv.cuMemAlloc(&p, bytes ? bytes : 1));
+  *dptr = static_cast<uint64_t>(p);
+  return 0;
+}
+
+int klb_mem_free(uint64_t dptr) {
+  CTX_TRY();
+  CU_TRY(drv.cuMemFree(static_cast<CUdeviceptr>(dptr)));
+  return 0;
+}
+
+int klb_mem_get_info(size_t* free_bytes, size_t* total_bytes) {
+  CTX_TRY();
+  CU_TRY(drv.cuMemGetInfo(free_bytes, total_bytes));
+  return 0;
+}
+
+int klb_host_alloc(size_t bytes, void** host_ptr) {
+  CTX_TRY();
+  CU_TRY(drv.cuMemHostAlloc(host_ptr, bytes ? bytes : 1, CU_MEMHOSTALLOC_PORTABLE));
+  return 0;
+}
+
+int klb_host_free(void* host_ptr) {
+  CTX_TRY();
+  CU_TRY(drv.cuMemFreeHost(host_ptr));
+  return 0;
+}
+
+int klb_memcpy_htod(uint64_t dst, const void* src, size_t bytes, klb_stream stream) {
+  CTX_TRY();
+  CU_TRY(drv.cuMemcpyHtoDAsync(static_cast<CUdeviceptr>(dst), src, bytes, as_stream(stream)));
+  return 0;
+}
+
+int klb_memcpy_dtoh(void* dst, uint64_t src, size_t bytes, klb_stream stream) {
+  CTX_TRY();
+  CU_TRY(drv.cuMemcpyDtoHAsync(dst, static_cast<CUdeviceptr>(src), bytes, as_stream(stream)));
+  return 0;
+}
+
+int klb_memcpy_dtod(uint64_t dst, uint64_t src, size_t bytes, klb_stream stream) {
+  CTX_TRY();
+  CU_TRY(drv.cuMemcpyDtoDAsync(static_cast<CUdeviceptr>(dst), static_cast<CUdeviceptr>(src), bytes, as_stream(stream)));
+  return 0;
+}
+
+int klb_memset_d8(uint64_t dst, unsigned char value, size_t bytes, klb_stream stream) {
+  CTX_TRY();
+  CU_TRY(drv.cuMemsetD8Async(static_cast<CUdeviceptr>(dst), value, bytes, as_stream(stream)));
+  return 0;
+}
+
+// ---- streams / events ---------------------------------------------------------
+
+int klb_stream_create(klb_stream* stream, int priority) {
+  CTX_TRY();
+  CUstream s;
+  CU_TRY(drv.cuStreamCreateWithPriority(&s, CU_STREAM_NON_BLOCKING, priority));
+  *stream = s;
+  return 0;
+}
+
+int klb_stream_destroy(klb_stream stream) {
+  CTX_TRY();
+  CU_TRY(drv.cuStreamDestroy(as_stream(stream)));
+  return 0;
+}
+
+int klb_stream_synchronize(klb_stream stream) {
+  CTX_TRY();
+  CU_TRY(drv.cuStreamSynchronize(as_stream(stream)));
+  return 0;
+}
+
+int klb_stream_wait_event(klb_stream stream, klb_event event) {
+  CTX_TRY();
+  CU_TRY(drv.cuStreamWaitEvent(as_stream(stream), reinterpret_cast<CUevent>(event), 0));
+  return 0;
+}
+
+int klb_event_create(klb_event* event) {
+  CTX_TRY();
+  CUevent e;
+  CU_TRY(drv.cuEventCreate(&e, CU_EVENT_DEFAULT));
+  *event = e;
+  return 0;
+}
+
+int klb_event_destroy(klb_event event) {
+  CTX_TRY();
+  CU_TRY(drv.cuEventDestroy(reinterpret_cast<CUevent>(event)));
+  return 0;
+}
+
+int klb_event_record(klb_event event, klb_stream stream) {
+  CTX_TRY();
+  CU_TRY(drv.cuEventRecord(reinterpret_cast<CUevent>(event), as_stream(stream)));
+  return 0;
+}
+
+int klb_event_synchronize(klb_event event) {
+  CTX_TRY();
+  CU_TRY(drv.cuEventSynchronize(reinterpret_cast<CUevent>(event)));
+  return 0;
+}
+
+int klb_event_elapsed_ms(klb_event start, klb_event stop, float* ms) {
+  CTX_TRY();
+  CU_TRY(drv.cuEventElapsedTime(ms, reinterpret_cast<CUevent>(start), reinterpret_cast<CUevent>(stop)));
+  return 0;
+}
+
+// ---- synthetic fields / comparison ----------------------------------------------
+
+int klb_synth_field(uint64_t dptr, int elem_bytes, long long base_offset, int icells, int jcells, int kcells_local,
+                    int jj, long long kk, int igc, int jgc, int k_offset, int kcells_global, uint64_t seed,
+                    double lo, double hi, int periodic_xy, klb_stream stream) {
+  if (elem_bytes != 4 && elem_bytes != 8) return fail(KLB_E_INVALID, "elem_bytes must be 4 or 8");
+  if (icells <= 2 * igc || jcells <= 2 * jgc || kcells_local < 1 || k_offset < 0 ||
+      k_offset + kcells_local > kcells_global || jj < icells || kk < static_cast<long long>(jj) * jcells)
+    return fail(KLB_E_INVALID, "inconsistent field layout");
+  CTX_TRY();
+  const long long total = static_cast<long long>(icells) * jcells * kcells_local;
+  const int threads = 256;
+  const int blocks = grid_for(total, threads);
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const double span = hi - lo;
+  if (elem_bytes == 4)
+    synth_kernel<float><<<blocks, threads, 0, s>>>(reinterpret_cast<float*>(dptr) + base_offset, total, icells, jcells,
+                                                   jj, kk, igc, jgc, k_offset, seed, lo, span, periodic_xy);
+  else
+    synth_kernel<double><<<blocks, threads, 0, s>>>(reinterpret_cast<double*>(dptr) + base_offset, total, icells,
+                                                    jcells, jj, kk, igc, jgc, k_offset, seed, lo, span, periodic_xy);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(static_cast<int>(e), "synth_kernel launch: %s", cudaGetErrorString(e));
+  return 0;
+}
+
+int klb_compare_fields(uint64_t a, uint64_t b, int elem_bytes, long long base_offset, int istart, int iend, int jstart,
+                       int jend, int kstart, int kend, int jj, long long kk, double* max_abs_diff,
+                       double* max_abs_ref, klb_stream stream) {
+  if (elem_bytes != 4 && elem_bytes != 8) return fail(KLB_E_INVALID, "elem_bytes must be 4 or 8");
+  CTX_TRY();
+  double* d_out = nullptr;
+  if (cudaMalloc(&d_out, 2 * sizeof(double)) != cudaSuccess) return fail(KLB_E_INVALID, "cudaMalloc failed");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  cudaMemsetAsync(d_out, 0, 2 * sizeof(double), s);
+  const long long total = static_cast<long long>(iend - istart) * (jend - jstart) * (kend - kstart);
+  const int threads = 256;
+  const int blocks = grid_for(total, threads);
+  if (elem_bytes == 4)
+    compare_kernel<float><<<blocks, threads, 0, s>>>(reinterpret_cast<const float*>(a) + base_offset,
+                                                     reinterpret_cast<const float*>(b) + base_offset, istart, iend,
+                                                     jstart, jend, kstart, kend, jj, kk, d_out);
+  else
+    compare_kernel<double><<<blocks, threads, 0, s>>>(reinterpret_cast<const double*>(a) + base_offset,
+                                                      reinterpret_cast<const double*>(b) + base_offset, istart, iend,
+                                                      jstart, jend, kstart, kend, jj, kk, d_out);
+  double host[2] = {0, 0};
+  cudaError_t e = cudaMemcpyAsync(host, d_out, sizeof(host), cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  cudaFree(d_out);
+  if (e != cudaSuccess) return fail(static_cast<int>(e), "compare_fields: %s", cudaGetErrorString(e));
+  *max_abs_diff = host[0];
+  *max_abs_ref = host[1];
+  return 0;
+}
+
+// ---- NCCL halo exchange -----------------------------------------------------------
+
+int klb_nccl_version(int* version) {
+  int e = nccl_load();
+  if (e) return e;
+  ncclResult_t r = g_nccl.getVersion(version);
+  return r == ncclSuccess ? 0 : nccl_fail(r, "ncclGetVersion");
+}
+
+int klb_nccl_unique_id(unsigned char id_out[128]) {
+  int e = nccl_load();
+  if (e) return e;
+  ncclUniqueId id;
+  ncclResult_t r = g_nccl.getUniqueId(&id);
+  if (r != ncclSuccess) return nccl_fail(r, "ncclGetUniqueId");
+  std::memcpy(id_out, id.internal, NCCL_UNIQUE_ID_BYTES);
+  return 0;
+}
+
+int klb_nccl_comm_init(klb_comm* comm, int nranks, const unsigned char id[128], int rank) {
+  int e = nccl_load();
+  if (e) return e;
+  CTX_TRY();
+  ncclUniqueId uid;
+  std::memcpy(uid.internal, id, NCCL_UNIQUE_ID_BYTES);
+  ncclComm_t c;
+  ncclResult_t r = g_nccl.commInitRank(&c, nranks, uid, rank);
+  if (r != ncclSuccess) return nccl_fail(r, "ncclCommInitRank");
+  *comm = c;
+  return 0;
+}
+
+int klb_nccl_comm_destroy(klb_comm comm) {
+  int e = nccl_load();
+  if (e) return e;
+  ncclResult_t r = g_nccl.commDestroy(reinterpret_cast<ncclComm_t>(comm));
+  return r == ncclSuccess ? 0 : nccl_fail(r, "ncclCommDestroy");
+}
+
+int klb_halo_exchange_z(klb_comm comm, klb_stream stream, int nfields, const uint64_t* fields, int elem_bytes,
+                        long long kk, int kstart, int kend, int n_down, int n_up, int rank_below,
+                        int rank_above) {
+  if (n_down < 0 || n_up < 0 || nfields < 0) return fail(KLB_E_INVALID, "negative halo extent");
+  int e = nccl_load();
+  if (e) return e;
+  CTX_TRY();
+  ncclComm_t c = reinterpret_cast<ncclComm_t>(comm);
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const size_t plane_bytes = static_cast<size_t>(kk) * elem_bytes;
+  auto at = [&](int f, int k) { return reinterpret_cast<char*>(fields[f]) + static_cast<long long>(k) * plane_bytes; };
+  ncclResult_t r = g_nccl.groupStart();
+  if (r != ncclSuccess) return nccl_fail(r, "ncclGroupStart");
+  for (int f = 0; f < nfields && r == ncclSuccess; ++f) {
+    if (rank_below >= 0) {
+      if (n_down > 0) r = g_nccl.send(at(f, kstart), n_down * plane_bytes, ncclUint8, rank_below, c, s);
+      if (r == ncclSuccess && n_up > 0)
+        r = g_nccl.recv(at(f, kstart - n_up), n_up * plane_bytes, ncclUint8, rank_below, c, s);
+    }
+    if (r == ncclSuccess && rank_above >= 0) {
+      if (n_up > 0) r = g_nccl.send(at(f, kend - n_up), n_up * plane_bytes, ncclUint8, rank_above, c, s);
+      if (r == ncclSuccess && n_down > 0)
+        r = g_nccl.recv(at(f, kend), n_down * plane_bytes, ncclUint8, rank_above, c, s);
+    }
+  }
+  ncclResult_t r2 = g_nccl.groupEnd();
+  if (r != ncclSuccess) return nccl_fail(r, "ncclSend/ncclRecv");
+  if (r2 != ncclSuccess) return nccl_fail(r2, "ncclGroupEnd");
+  return 0;
+}
+
+}  // extern "C"

@@ -1,0 +1,284 @@
+"""NVRTC compiler and CUDA executable — the B200 implementations of the
+reference ``CompilerInterface`` / ``ExecutableHandle`` (backend.py:264-277).
+
+``NvrtcCompiler.compile(request, device)``
+    CompileRequest -> NVRTC (``--gpu-architecture=sm_100a``, the request's
+    flags and its ``"-D name=value"`` defines passed verbatim, name
+    expression = ``request.entry`` so templated entries lower correctly)
+    -> CUBIN -> ``CudaExecutable``.  NVRTC failures raise
+    ``CompileError(log)``.  Identical requests hit an in-process CUBIN cache;
+    ``compile_many`` compiles a batch on a thread pool (NVRTC is reentrant),
+    which the tuner uses to overlap compilation with GPU measurement.
+
+``CudaExecutable.load()``   cuModuleLoadData + cuModuleGetFunction.
+``CudaExecutable.launch(geometry, args)``
+    packs arguments by ``position`` (ScalarArg by dtype, DeviceBuffer as a
+    device pointer, host BufferArg uploaded to a scratch allocation) and
+    enqueues cuLaunchKernel.  Asynchronous by default (returns the host
+    enqueue seconds, which is all the dispatcher measures,
+    dispatch.py:185-187); ``timed=True`` brackets the launch with events and
+    returns kernel seconds.  Failures raise ``LaunchError``.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import hashlib
+import os
+import threading
+import time
+from concurrent.futures import ThreadPoolExecutor
+from dataclasses import dataclass
+from typing import Sequence
+
+from ..backend import CompileError, CompilerInterface, DeviceIdent, ExecutableHandle, LaunchError
+from ..capture import BufferArg, ScalarArg
+from ..kerneldef import CompileRequest, LaunchGeometry
+from ._abi import FuncAttrs, KlbError, check, lib
+from .device import DeviceArray, DeviceBuffer, DeviceContext, Event, Stream
+
+__all__ = ["CompiledImage", "NvrtcCompiler", "CudaExecutable", "pack_args"]
+
+_SCALAR_CTYPES = {
+    "f32": C.c_float, "f64": C.c_double, "i8": C.c_int8, "i16": C.c_int16, "i32": C.c_int32, "i64": C.c_int64,
+    "u8": C.c_uint8, "u16": C.c_uint16, "u32": C.c_uint32, "u64": C.c_uint64,
+}
+_KLB_E_COMPILE = 30003
+
+
+@dataclass(frozen=True)
+class CompiledImage:
+    cubin: bytes
+    lowered_name: str
+    log: str
+    compile_seconds: float
+    options: tuple[str, ...]
+
+
+def _arch_for(device: DeviceIdent | None, ctx: DeviceContext | None) -> str:
+    if ctx is not None:
+        return ctx.arch_flag
+    cc = (device.attributes or {}).get("compute_capability") if device is not None else None
+    if cc:
+        major, minor = (int(x) for x in str(cc).split("."))
+        return f"sm_{major}{minor}{'a' if major >= 9 else ''}"
+    return "sm_100a"
+
+
+class NvrtcCompiler(CompilerInterface):
+    """Runtime compiler for sm_100a through ``klb_compile``."""
+
+    def __init__(self, ctx: DeviceContext | None = None, extra_options: Sequence[str] = (), lineinfo: bool = True,
+                 max_workers: int | None = None) -> None:
+        self.ctx = ctx
+        self.extra_options = tuple(extra_options)
+        self.lineinfo = lineinfo
+        self.invocations = 0
+        self.cache_hits = 0
+        self._cache: dict[str, CompiledImage] = {}
+        self._lock = threading.Lock()
+        self._pool = ThreadPoolExecutor(max_workers=max_workers or min(8, os.cpu_count() or 4))
+
+    def options_for(self, request: CompileRequest, device: DeviceIdent | None) -> tuple[str, ...]:
+        opts = [f"--gpu-architecture={_arch_for(device, self.ctx)}"]
+        if not any(f.startswith("-std") for f in request.flags):
+            opts.append("-std=c++17")
+        if self.lineinfo:
+            opts.append("-lineinfo")
+        opts += list(request.flags)
+        opts += list(request.defines)
+        opts += list(self.extra_options)
+        return tuple(opts)
+
+    def compile_image(self, request: CompileRequest, device: DeviceIdent | None = None) -> CompiledImage:
+        options = self.options_for(request, device)
+        key = hashlib.sha256("\0".join((request.source, request.entry, *options)).encode()).hexdigest()
+        with self._lock:
+            self.invocations += 1
+            hit = self._cache.get(key)
+            if hit is not None:
+                self.cache_hits += 1
+                return hit
+        opt_arr = (C.c_char_p * len(options))(*(o.encode() for o in options))
+        image, size = C.c_void_p(), C.c_size_t()
+        lowered, log = C.c_void_p(), C.c_void_p()
+        t0 = time.perf_counter()
+        rc = lib().klb_compile(request.source.encode(), b"kltune_kernel.cu", request.entry.encode(), opt_arr,
+                               len(options), C.byref(image), C.byref(size), C.byref(lowered), C.byref(log))
+        elapsed = time.perf_counter() - t0
+        log_text = C.string_at(log.value).decode("utf-8", "replace") if log.value else ""
+        try:
+            if rc != 0:
+                msg = lib().klb_last_error().decode("utf-8", "replace")
+                if rc == _KLB_E_COMPILE:
+                    raise CompileError(f"{msg}\n{log_text}")
+                raise CompileError(f"[klb {rc}] {msg}")
+            img = CompiledImage(C.string_at(image.value, size.value), C.string_at(lowered.value).decode(), log_text,
+                                elapsed, options)
+        finally:
+            for p in (image, lowered, log):
+                if p.value:
+                    lib().klb_free(p)
+        with self._lock:
+            self._cache[key] = img
+        return img
+
+    def compile(self, request: CompileRequest, device: DeviceIdent) -> "CudaExecutable":
+        img = self.compile_image(request, device)
+        return CudaExecutable(request, img, self.ctx)
+
+    def compile_many(self, requests: Sequence[CompileRequest], device: DeviceIdent | None = None):
+        """Futures of ``CompiledImage`` compiled concurrently."""
+        return [self._pool.submit(self.compile_image, r, device) for r in requests]
+
+    def submit(self, request: CompileRequest, device: DeviceIdent | None = None):
+        return self._pool.submit(self.compile_image, request, device)
+
+
+def pack_args(args: Sequence[object], keep: list, ctx_stream: Stream | None = None):
+    """cuLaunchKernel parameter array from position-ordered launch args.
+
+    Returns ``(params, staged)``: ``staged`` lists (BufferArg, DeviceArray)
+    pairs uploaded for host buffers.
+    """
+    ordered = sorted(args, key=lambda a: a.position)
+    if [a.position for a in ordered] != list(range(len(ordered))):
+        raise LaunchError(f"argument positions must be 0..{len(ordered) - 1}, got {[a.position for a in ordered]}")
+    params = (C.c_void_p * len(ordered))()
+    staged = []
+    for slot, arg in enumerate(ordered):
+        if isinstance(arg, ScalarArg):
+            ctype = _SCALAR_CTYPES[arg.dtype]
+            value = ctype(float(arg.value) if arg.dtype in ("f32", "f64") else int(arg.value))
+        elif isinstance(arg, DeviceBuffer):
+            value = C.c_uint64(arg.ptr)
+        elif isinstance(arg, BufferArg):
+            scratch = DeviceArray(len(arg.data))
+            if arg.data:
+                scratch.upload(arg.data, stream=ctx_stream)
+            staged.append((arg, scratch))
+            value = C.c_uint64(scratch.ptr)
+        else:
+            raise LaunchError(f"unsupported launch argument {type(arg).__name__}")
+        keep.append(value)
+        params[slot] = C.cast(C.pointer(value), C.c_void_p)
+    return params, staged
+
+
+class CudaExecutable(ExecutableHandle):
+    """A loaded CUBIN function plus a cache of packed parameter blocks."""
+
+    def __init__(self, request: CompileRequest, image: CompiledImage, ctx: DeviceContext | None) -> None:
+        self.request = request
+        self.image = image
+        self.ctx = ctx
+        self.module = None
+        self.function = None
+        self.attrs: FuncAttrs | None = None
+        self._smem_opt_in = 48 * 1024
+        self._packed: dict = {}
+        self.launch_count = 0
+
+    # -- ExecutableHandle ---------------------------------------------------------
+    def load(self) -> None:
+        if self.function is not None:
+            return
+        try:
+            mod, fn = C.c_void_p(), C.c_void_p()
+            blob = C.create_string_buffer(self.image.cubin, len(self.image.cubin))
+            check(lib().klb_module_load(blob, C.byref(mod)))
+            check(lib().klb_module_function(mod, self.image.lowered_name.encode(), C.byref(fn)))
+            attrs = FuncAttrs()
+            check(lib().klb_function_attributes(fn, C.byref(attrs)))
+        except KlbError as err:
+            raise LaunchError(str(err)) from err
+        self.module, self.function, self.attrs = mod.value, fn.value, attrs
+
+    def _prepare(self, geometry: LaunchGeometry):
+        if self.function is None:
+            self.load()
+        smem = geometry.shared_mem_bytes
+        if smem > self._smem_opt_in:
+            try:
+                check(lib().klb_function_set_max_dynamic_smem(self.function, smem))
+            except KlbError as err:
+                raise LaunchError(str(err)) from err
+            self._smem_opt_in = smem
+        grid = (C.c_uint * 3)(*geometry.grid)
+        block = (C.c_uint * 3)(*geometry.block)
+        return grid, block, smem
+
+    def _params(self, args: Sequence[object], stream: Stream | None):
+        if all(isinstance(a, (ScalarArg, DeviceBuffer)) for a in args):
+            key = tuple(args)
+            hit = self._packed.get(key)
+            if hit is None:
+                keep: list = []
+                params, _ = pack_args(args, keep)
+                hit = (params, keep)
+                if len(self._packed) > 256:
+                    self._packed.clear()
+                self._packed[key] = hit
+            return hit[0], hit[1], []
+        keep = []
+        params, staged = pack_args(args, keep, stream)
+        return params, keep, staged
+
+    def launch(self, geometry: LaunchGeometry, args: Sequence[object], stream: Stream | None = None,
+               timed: bool = False, outputs: dict | None = None) -> float:
+        grid, block, smem = self._prepare(geometry)
+        params, _keep, staged = self._params(args, stream)
+        handle = stream.handle if stream is not None else (self.ctx.stream.handle if self.ctx else None)
+        sync = timed or bool(staged)
+        try:
+            if sync:
+                start, stop = Event(), Event()
+                start.record(Stream(handle))
+                check(lib().klb_launch(self.function, grid, block, smem, handle, params))
+                stop.record(Stream(handle))
+                stop.synchronize()
+                seconds = start.elapsed_ms(stop) * 1e-3
+            else:
+                t0 = time.perf_counter()
+                check(lib().klb_launch(self.function, grid, block, smem, handle, params))
+                seconds = time.perf_counter() - t0
+        except KlbError as err:
+            raise LaunchError(str(err)) from err
+        self.launch_count += 1
+        for arg, scratch in staged:
+            if outputs is not None and arg.role == "output":
+                outputs[arg.position] = scratch.download()
+            scratch.free()
+        return max(seconds, 1e-9)
+
+    def time_launches(self, geometry: LaunchGeometry, args: Sequence[object], warmup: int, reps: int,
+                      flush: DeviceArray | None = None, stream: Stream | None = None) -> list[float]:
+        """Kernel seconds of ``reps`` launches after ``warmup`` (klb_time_launches)."""
+        grid, block, smem = self._prepare(geometry)
+        params, _keep, staged = self._params(args, stream)
+        if staged:
+            raise LaunchError("time_launches needs device-resident arguments")
+        handle = stream.handle if stream is not None else (self.ctx.stream.handle if self.ctx else None)
+        out = (C.c_float * reps)()
+        try:
+            check(lib().klb_time_launches(self.function, grid, block, smem, handle, params, warmup, reps,
+                                          flush.ptr if flush else 0, flush.nbytes if flush else 0, out))
+        except KlbError as err:
+            raise LaunchError(str(err)) from err
+        self.launch_count += warmup + reps
+        return [ms * 1e-3 for ms in out]
+
+    def occupancy(self, geometry: LaunchGeometry) -> int:
+        if self.function is None:
+            self.load()
+        n = C.c_int()
+        check(lib().klb_occupancy_blocks_per_sm(self.function, geometry.threads_per_block,
+                                                geometry.shared_mem_bytes, C.byref(n)))
+        return n.value
+
+    def close(self) -> None:
+        if self.module is not None:
+            try:
+                lib().klb_module_unload(self.module)
+            finally:
+                self.module = self.function = None

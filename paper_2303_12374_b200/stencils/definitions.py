@@ -1,0 +1,184 @@
+"""KernelDefinitions of the MicroHH stencils on the reference API.
+
+Each kernel is defined once per precision so the precision reaches the
+wisdom key (the reference ``kernel_key`` hashes only the space,
+so the name must carry it): ``advec_u_fp32``, ``advec_u_fp64``,
+``diff_uvw_fp32``, ``diff_uvw_fp64``.
+
+Space = the paper's Table 2 (presets.table2_params, 7,776,000 raw points) plus
+two B200 knobs:
+
+``staging``  "DIRECT" (the paper's kernel) | "ZMARCH" (register/shared-memory
+             z-marching column);
+``zchunk``   planes marched per block for ZMARCH (8..128); 1 under DIRECT,
+             so ``block_z * tile_z * zchunk`` is the z extent of a block in
+             both variants and one grid formula serves the whole space.
+
+Restrictions: ``block_x*block_y*block_z <= 1024`` (Table 2 limit) and, so the
+tuner never measures two names for one binary, the z-knobs are pinned to
+their defaults where they have no meaning (``zchunk`` under DIRECT;
+``block_z``/``tile_z``/``unroll_z``/``contiguous_z`` under ZMARCH).
+
+Launch geometry: a 1-D list of blocks (the paper's "thread blocks are launched
+as a one-dimensional list ... each thread unravels its 1D block identifier",
+PAPER.md:425-431) of ``nbx*nby*nbz`` blocks; shared memory is derived per
+configuration for ZMARCH.  ``KL_JJ``/``KL_KK`` specialise the row/plane pitch
+from the launch's scalar arguments.
+"""
+
+from __future__ import annotations
+
+import re
+from functools import lru_cache
+from pathlib import Path
+
+from ..kerneldef import KernelDefinition
+from ..presets import BLOCK_LIMIT_RESTRICTION, table2_params
+from ..space import ConfigSpace, TunableParam
+
+__all__ = [
+    "KERNELS", "PRECISIONS", "stencil_space", "advec_u_definition", "diff_uvw_definition", "definition_for",
+    "assemble_source", "ARG_LAYOUT",
+]
+
+_HERE = Path(__file__).resolve().parent
+PRECISIONS = {"fp32": "float", "fp64": "double"}
+KERNELS = ("advec_u", "diff_uvw")
+
+STAGING_VALUES = ("DIRECT", "ZMARCH")
+ZCHUNK_VALUES = (1, 8, 16, 32, 64, 128)
+
+#: argument positions of each kernel's MicroHH-style signature
+ARG_LAYOUT = {
+    "advec_u": {
+        "buffers": [("ut", "output"), ("u", "input"), ("v", "input"), ("w", "input"),
+                    ("rhoref", "input"), ("rhorefh", "input"), ("dzi", "input")],
+        "scalars": ["dxi", "dyi", "jj", "kk", "istart", "jstart", "kstart", "iend", "jend", "kend"],
+    },
+    "diff_uvw": {
+        "buffers": [("ut", "output"), ("vt", "output"), ("wt", "output"), ("evisc", "input"), ("u", "input"),
+                    ("v", "input"), ("w", "input"), ("dzi", "input"), ("dzhi", "input"), ("rhoref", "input"),
+                    ("rhorefh", "input")],
+        "scalars": ["dxi", "dyi", "jj", "kk", "istart", "jstart", "kstart", "iend", "jend", "kend"],
+    },
+}
+
+
+def _pos(kernel: str, name: str) -> int:
+    layout = ARG_LAYOUT[kernel]
+    names = [b for b, _ in layout["buffers"]] + layout["scalars"]
+    return names.index(name)
+
+
+_INCLUDE = re.compile(r'^\s*#\s*include\s+"([^"]+)"\s*$', re.M)
+
+
+def _inline(path: Path, seen: set[str]) -> str:
+    text = path.read_text(encoding="utf-8")
+
+    def repl(m: re.Match) -> str:
+        name = m.group(1)
+        if name in seen:
+            return f"// (already included: {name})"
+        seen.add(name)
+        return f"// ---- begin {name} ----\n{_inline(_HERE / name, seen)}\n// ---- end {name} ----"
+
+    return _INCLUDE.sub(repl, text).replace("#pragma once", "")
+
+
+@lru_cache(maxsize=None)
+def assemble_source(kernel: str, precision: str) -> str:
+    """Self-contained NVRTC source: precision/entry prelude + inlined headers."""
+    if kernel not in KERNELS or precision not in PRECISIONS:
+        raise ValueError(f"unknown kernel/precision {kernel}/{precision}")
+    prelude = (
+        f"// {kernel} ({precision}) — B200 Kernel Launcher stencil, runtime-compiled by NVRTC\n"
+        f"#define KL_REAL {PRECISIONS[precision]}\n"
+        f"#define KL_ENTRY {kernel}_{precision}\n"
+        "#define DIRECT 0\n#define ZMARCH 1\n"
+    )
+    return prelude + _inline(_HERE / f"{kernel}.cu", set())
+
+
+#: ZMARCH shared-memory plane budget per kernel, in halo'd cells per plane
+#: (keeps fp64 staging <= ~96 KB so at least two blocks fit per SM).
+_ZMARCH_PLANE_LIMIT = {
+    "advec_u": "(block_x * tile_x + 6) * (block_y * tile_y + 6) <= 6144",
+    "diff_uvw": "(block_x * tile_x + 2) * (block_y * tile_y + 2) <= 768",
+}
+
+
+@lru_cache(maxsize=None)
+def stencil_space(kernel: str = "advec_u") -> ConfigSpace:
+    params = table2_params() + [
+        TunableParam("staging", STAGING_VALUES, "DIRECT"),
+        TunableParam("zchunk", ZCHUNK_VALUES, 1),
+    ]
+    restrictions = [
+        BLOCK_LIMIT_RESTRICTION,
+        'staging == "ZMARCH" || zchunk == 1',
+        'staging == "DIRECT" || (zchunk > 1 && block_z == 1 && tile_z == 1 && !unroll_z && !contiguous_z)',
+        # a ZMARCH block must hold at least one warp of columns
+        'staging == "DIRECT" || block_x * block_y >= 32',
+        # register-resident tiles: the tile loops are always unrolled under ZMARCH
+        'staging == "DIRECT" || (!unroll_x && !unroll_y)',
+        f'staging == "DIRECT" || ({_ZMARCH_PLANE_LIMIT[kernel]})',
+    ]
+    return ConfigSpace(params, restrictions)
+
+
+_SMEM = {
+    # ZMARCH shared-memory bytes (see *_zmarch.cuh): advec_u double-buffers one
+    # 3-halo plane of u; diff_uvw keeps a 4-slot ring of 1-halo planes of 4 fields.
+    "advec_u": "(2 * (block_x * tile_x + 6) * (block_y * tile_y + 6)) * {S}",
+    "diff_uvw": "(16 * (block_x * tile_x + 2) * (block_y * tile_y + 2)) * {S}",
+}
+
+
+def _definition(kernel: str, precision: str) -> KernelDefinition:
+    space = stencil_space(kernel)
+    p = lambda n: f"arg{_pos(kernel, n)}"  # noqa: E731
+    size = 4 if precision == "fp32" else 8
+    # z extent of one block: block_z*tile_z under DIRECT (zchunk pinned to 1),
+    # zchunk under ZMARCH (block_z = tile_z = 1 pinned) -> one formula for both.
+    grid_x = (
+        "ceil_div(problem_x, block_x * tile_x) * ceil_div(problem_y, block_y * tile_y) * "
+        "ceil_div(problem_z, block_z * tile_z * zchunk)"
+    )
+    defines = [
+        ("BLOCK_X", "block_x"), ("BLOCK_Y", "block_y"), ("BLOCK_Z", "block_z"),
+        ("TILE_X", "tile_x"), ("TILE_Y", "tile_y"), ("TILE_Z", "tile_z"),
+        ("UNROLL_X", "unroll_x"), ("UNROLL_Y", "unroll_y"), ("UNROLL_Z", "unroll_z"),
+        ("CONTIG_X", "contiguous_x"), ("CONTIG_Y", "contiguous_y"), ("CONTIG_Z", "contiguous_z"),
+        ("UNRAVEL", "unravel"), ("MIN_BLOCKS", "min_blocks"),
+        ("STAGING", "staging"), ("ZCHUNK", "zchunk"),
+        ("KL_JJ", p("jj")), ("KL_KK", p("kk")),
+    ]
+    return KernelDefinition(
+        f"{kernel}_{precision}",
+        space,
+        source_text=assemble_source(kernel, precision),
+        problem_size=(f"{p('iend')} - {p('istart')}", f"{p('jend')} - {p('jstart')}", f"{p('kend')} - {p('kstart')}"),
+        block=("block_x", "block_y", "block_z"),
+        grid=(grid_x, 1, 1),
+        shared_mem="min(zchunk - 1, 1) * " + _SMEM[kernel].format(S=size),
+        defines=defines,
+        flags=("-std=c++17",),
+    )
+
+
+def definition_for(kernel: str, precision: str) -> KernelDefinition:
+    return _cached_definition(kernel, precision)
+
+
+@lru_cache(maxsize=None)
+def _cached_definition(kernel: str, precision: str) -> KernelDefinition:
+    return _definition(kernel, precision)
+
+
+def advec_u_definition(precision: str = "fp32") -> KernelDefinition:
+    return definition_for("advec_u", precision)
+
+
+def diff_uvw_definition(precision: str = "fp32") -> KernelDefinition:
+    return definition_for("diff_uvw", precision)

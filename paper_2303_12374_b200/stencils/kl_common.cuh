@@ -1,0 +1,108 @@
+// kl_common.cuh — shared prelude of the runtime-compiled MicroHH stencils.
+//
+// Every tunable parameter of the selected configuration arrives as a -D
+// define rendered by KernelDefinition.render_compile_request (reference
+// kerneldef.py:188-211): ints verbatim, bools as true/false, strings bare
+// (so UNRAVEL=ZYX names one of the macros below).  The Table-2 knobs
+// map to code as follows:
+//   BLOCK_{X,Y,Z}     blockDim
+//   TILE_{X,Y,Z}      cells per thread along each axis
+//   UNROLL_{X,Y,Z}    #pragma unroll (full) vs #pragma unroll 1 on the tile loop
+//   CONTIG_{X,Y,Z}    true: a thread's cells are consecutive (x, x+1, ...);
+//                     false: block-strided (x, x+BLOCK_X, ...)
+//   UNRAVEL           order in which the 1-D block id is unravelled into
+//                     (bx, by, bz); first letter varies fastest
+//   MIN_BLOCKS        second argument of __launch_bounds__
+// Problem-shape constants (KL_JJ, KL_KK: row / plane pitch in elements) are
+// specialised at compile time from the launch's scalar arguments, so every
+// neighbour offset becomes an immediate in the SASS addressing mode.
+
+#pragma once
+
+#ifndef KL_REAL
+#error "KL_REAL (float|double) must be defined"
+#endif
+typedef KL_REAL real;
+
+#define XYZ 0
+#define XZY 1
+#define YXZ 2
+#define YZX 3
+#define ZXY 4
+#define ZYX 5
+
+#define KL_STR(x) #x
+#define KL_PRAGMA(x) _Pragma(KL_STR(x))
+
+#if UNROLL_X
+#define KL_UNROLL_X KL_PRAGMA(unroll)
+#else
+#define KL_UNROLL_X KL_PRAGMA(unroll 1)
+#endif
+#if UNROLL_Y
+#define KL_UNROLL_Y KL_PRAGMA(unroll)
+#else
+#define KL_UNROLL_Y KL_PRAGMA(unroll 1)
+#endif
+#if UNROLL_Z
+#define KL_UNROLL_Z KL_PRAGMA(unroll)
+#else
+#define KL_UNROLL_Z KL_PRAGMA(unroll 1)
+#endif
+
+#define KL_THREADS (BLOCK_X * BLOCK_Y * BLOCK_Z)
+
+namespace kl {
+
+// 1-D block id -> 3-D block coordinates; the first letter of UNRAVEL is the
+// fastest-varying axis (PAPER.md: "for (Z,X,Y) ... first along Z, then X, then Y").
+__device__ __forceinline__ void unravel(unsigned b, unsigned nbx, unsigned nby, unsigned nbz,
+                                        int& bx, int& by, int& bz) {
+#if UNRAVEL == XYZ
+  bx = b % nbx; b /= nbx; by = b % nby; bz = b / nby;
+#elif UNRAVEL == XZY
+  bx = b % nbx; b /= nbx; bz = b % nbz; by = b / nbz;
+#elif UNRAVEL == YXZ
+  by = b % nby; b /= nby; bx = b % nbx; bz = b / nbx;
+#elif UNRAVEL == YZX
+  by = b % nby; b /= nby; bz = b % nbz; bx = b / nbz;
+#elif UNRAVEL == ZXY
+  bz = b % nbz; b /= nbz; bx = b % nbx; by = b / nbx;
+#elif UNRAVEL == ZYX
+  bz = b % nbz; b /= nbz; by = b % nby; bx = b / nby;
+#else
+#error "UNRAVEL must be one of XYZ XZY YXZ YZX ZXY ZYX"
+#endif
+}
+
+// Global index of tile item t of thread `tid` in block `b` along one axis.
+template <int BLOCK, int TILE, bool CONTIG>
+__device__ __forceinline__ int tile_index(int b, int tid, int t) {
+  return CONTIG ? (b * BLOCK + tid) * TILE + t : b * BLOCK * TILE + t * BLOCK + tid;
+}
+
+__device__ __forceinline__ unsigned ceil_div(unsigned a, unsigned b) { return (a + b - 1) / b; }
+
+// MicroHH finite-difference helpers (restated in oracle/stencil_oracle.py).
+template <typename T>
+__device__ __forceinline__ T interp2(T a, T b) { return T(0.5) * (a + b); }
+
+// 60 * interp6_ws(a..f): 6th-order centred face value, unscaled.
+template <typename T>
+__device__ __forceinline__ T i6x60(T a, T b, T c, T d, T e, T f) {
+  return T(37) * (c + d) - T(8) * (b + e) + (a + f);
+}
+
+// 60 * interp5_ws(a..f): the odd (upwind-correction) part, unscaled.
+template <typename T>
+__device__ __forceinline__ T i5x60(T a, T b, T c, T d, T e, T f) {
+  return T(10) * (d - c) - T(5) * (e - b) + (f - a);
+}
+
+// 60 * (vel * interp6_ws - |vel| * interp5_ws): 5th-order upwind flux.
+template <typename T>
+__device__ __forceinline__ T flux5x60(T vel, T a, T b, T c, T d, T e, T f) {
+  return vel * i6x60(a, b, c, d, e, f) - fabs(vel) * i5x60(a, b, c, d, e, f);
+}
+
+}  // namespace kl

@@ -1,0 +1,145 @@
+"""Device-resident stencil problems: fields in HBM + the launch argument list.
+
+``StencilProblem(kernel, layout, ctx)`` allocates every field the kernel
+touches in the ghost-padded pitched layout (``layout.GridLayout``), fills them
+on the device with the deterministic generator (``klb_synth_field``; the
+oracle twin is ``oracle/synth.py``), uploads the 1-D profiles, and builds the
+MicroHH-ordered argument list of ``DeviceBuffer`` / ``ScalarArg`` the
+``WisdomKernel`` / ``CudaExecutable`` launch API takes (positions from
+``definitions.ARG_LAYOUT``).
+
+For z-slab decomposition (``k_offset``/``kcells_global``) a rank's local
+fields hold global planes ``[k_offset, k_offset + layout.kcells)``; the
+generator indexes by global plane, so a slab's ghost planes initially equal
+its neighbours' interior planes, and the halo exchange keeps them so.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from ..capture import ScalarArg
+from ..cuda._abi import check, lib
+from ..cuda.device import DeviceArray, DeviceBuffer, DeviceContext, Stream
+from .definitions import ARG_LAYOUT, definition_for
+from .layout import GridLayout
+from .profiles import FIELD_SEED_BASE, FIELD_SPECS, Profiles, make_profiles
+
+__all__ = ["StencilProblem", "KERNEL_FIELDS", "BYTES_PER_CELL_WORDS"]
+
+KERNEL_FIELDS = {
+    "advec_u": ("ut", "u", "v", "w"),
+    "diff_uvw": ("ut", "vt", "wt", "evisc", "u", "v", "w"),
+}
+#: algorithmic HBM words per interior cell: advec_u reads u,v,w,ut
+#: and writes ut; diff_uvw reads evisc,u,v,w,ut,vt,wt and writes ut,vt,wt.
+BYTES_PER_CELL_WORDS = {"advec_u": 5, "diff_uvw": 10}
+_PROFILE_FIELDS = ("rhoref", "rhorefh", "dzi", "dzhi")
+
+
+class StencilProblem:
+    def __init__(self, kernel: str, layout: GridLayout, ctx: DeviceContext, *, k_offset: int = 0,
+                 kcells_global: int | None = None, profiles: Profiles | None = None,
+                 dxi: float = 1.0, dyi: float = 1.0, stream: Stream | None = None) -> None:
+        if kernel not in ARG_LAYOUT:
+            raise ValueError(f"unknown kernel {kernel!r}")
+        self.kernel = kernel
+        self.layout = layout
+        self.ctx = ctx
+        self.k_offset = k_offset
+        self.kcells_global = kcells_global if kcells_global is not None else layout.kcells
+        self.definition = definition_for(kernel, layout.precision)
+        self.dxi, self.dyi = dxi, dyi
+        self.stream = stream or ctx.stream
+        glob = profiles if profiles is not None else make_profiles(self.kcells_global, layout.kgc)
+        self.profiles = glob.window(k_offset, layout.kcells).as_dtype(layout.dtype)
+        self.fields: dict[str, DeviceArray] = {}
+        for name in KERNEL_FIELDS[kernel]:
+            arr = DeviceArray(layout.alloc_bytes)
+            arr.zero(self.stream)
+            self.fields[name] = arr
+        self.regenerate()
+        self.profile_arrays: dict[str, DeviceArray] = {}
+        for name in _PROFILE_FIELDS:
+            data = np.ascontiguousarray(getattr(self.profiles, name))
+            arr = DeviceArray(data.nbytes)
+            arr.upload(data, stream=self.stream)
+            self.profile_arrays[name] = arr
+        self._args = self._build_args()
+
+    # -- data ----------------------------------------------------------------------
+    def regenerate(self, names=None) -> None:
+        """(Re)fill fields with the deterministic synthetic values."""
+        lay = self.layout
+        for name in names or self.fields:
+            seed_off, lo, hi = FIELD_SPECS[name]
+            check(lib().klb_synth_field(
+                self.fields[name].ptr, lay.elem_bytes, lay.lead, lay.icells, lay.jcells, lay.kcells, lay.jj, lay.kk,
+                lay.igc, lay.jgc, self.k_offset, self.kcells_global, FIELD_SEED_BASE + seed_off, lo, hi, 1,
+                self.stream.handle))
+        self.stream.synchronize()
+
+    def field_ptr(self, name: str) -> int:
+        """Device pointer of element (0, 0, 0) — what kernels receive."""
+        return self.fields[name].ptr + self.layout.lead * self.layout.elem_bytes
+
+    def download(self, name: str) -> np.ndarray:
+        """(kcells, jcells, icells) host view of a field."""
+        flat = self.fields[name].download_array(self.layout.dtype)
+        return self.layout.host_view(flat)
+
+    def outputs(self) -> tuple[str, ...]:
+        return tuple(n for n, role in ARG_LAYOUT[self.kernel]["buffers"] if role == "output")
+
+    # -- launch arguments --------------------------------------------------------------
+    def _build_args(self) -> list:
+        lay = self.layout
+        elem = lay.element_type
+        args: list = []
+        pos = 0
+        for name, role in ARG_LAYOUT[self.kernel]["buffers"]:
+            if name in self.fields:
+                args.append(DeviceBuffer(pos, role, elem, self.field_ptr(name), lay.span_elems, owner=self.fields[name]))
+            else:
+                arr = self.profile_arrays[name]
+                args.append(DeviceBuffer(pos, role, elem, arr.ptr, arr.nbytes // lay.elem_bytes, owner=arr))
+            pos += 1
+        scalars = {
+            "dxi": (elem, self.dxi), "dyi": (elem, self.dyi), "jj": ("i32", lay.jj), "kk": ("i32", lay.kk),
+            "istart": ("i32", lay.istart), "jstart": ("i32", lay.jstart), "kstart": ("i32", lay.kstart),
+            "iend": ("i32", lay.iend), "jend": ("i32", lay.jend), "kend": ("i32", lay.kend),
+        }
+        for name in ARG_LAYOUT[self.kernel]["scalars"]:
+            dtype, value = scalars[name]
+            args.append(ScalarArg(pos, dtype, value))
+            pos += 1
+        return args
+
+    def args(self, k_range: tuple[int, int] | None = None) -> list:
+        """Launch args, optionally restricted to local planes ``[kb, ke)``."""
+        if k_range is None:
+            return list(self._args)
+        kb, ke = k_range
+        pos_ks = len(ARG_LAYOUT[self.kernel]["buffers"]) + ARG_LAYOUT[self.kernel]["scalars"].index("kstart")
+        pos_ke = len(ARG_LAYOUT[self.kernel]["buffers"]) + ARG_LAYOUT[self.kernel]["scalars"].index("kend")
+        out = list(self._args)
+        out[pos_ks] = ScalarArg(pos_ks, "i32", kb)
+        out[pos_ke] = ScalarArg(pos_ke, "i32", ke)
+        return out
+
+    def scalar_env(self) -> dict[str, int]:
+        from ..capture import scalar_env_from_args
+
+        return scalar_env_from_args(self._args)
+
+    @property
+    def algorithmic_bytes(self) -> int:
+        return BYTES_PER_CELL_WORDS[self.kernel] * self.layout.elem_bytes * self.layout.cells
+
+    def close(self) -> None:
+        for arr in list(self.fields.values()) + list(self.profile_arrays.values()):
+            arr.free()
+        self.fields.clear()
+        self.profile_arrays.clear()

@@ -1,0 +1,67 @@
+"""Shared GPU-test helpers: run a stencil configuration and compare with the oracle."""
+
+from __future__ import annotations
+
+import numpy as np
+
+from oracle import stencil_oracle
+from oracle.synth import synth_field
+from paper_2303_12374_b200.stencils.layout import GridLayout
+from paper_2303_12374_b200.stencils.problem import KERNEL_FIELDS, StencilProblem
+from paper_2303_12374_b200.stencils.profiles import FIELD_SEED_BASE, FIELD_SPECS, make_profiles
+
+TOL = {"fp32": 1e-5, "fp64": 1e-12}
+
+
+def host_fields(layout: GridLayout, names, k_offset=0):
+    out = {}
+    for n in names:
+        off, lo, hi = FIELD_SPECS[n]
+        out[n] = synth_field(FIELD_SEED_BASE + off, lo, hi, layout.icells, layout.jcells, layout.kcells, layout.igc,
+                             layout.jgc, k_offset=k_offset, dtype=layout.dtype)
+    return out
+
+
+def oracle_outputs(kernel: str, layout: GridLayout, dxi=1.0, dyi=1.0, k_range=None):
+    """Oracle result for the full interior (or local planes ``k_range``)."""
+    f = host_fields(layout, KERNEL_FIELDS[kernel])
+    prof = make_profiles(layout.kcells, layout.kgc).as_dtype(layout.dtype)
+    g = (layout.igc, layout.jgc, layout.kgc)
+    if kernel == "advec_u":
+        res = {"ut": stencil_oracle.advec_u(f["ut"], f["u"], f["v"], f["w"], prof.rhoref, prof.rhorefh, prof.dzi, dxi,
+                                             dyi, ghost=g)}
+    else:
+        ut, vt, wt = stencil_oracle.diff_uvw(f["ut"], f["vt"], f["wt"], f["evisc"], f["u"], f["v"], f["w"], prof.dzi,
+                                             prof.dzhi, prof.rhoref, prof.rhorefh, dxi, dyi, ghost=g)
+        res = {"ut": ut, "vt": vt, "wt": wt}
+    if k_range is not None:
+        kb, ke = k_range
+        for name, arr in res.items():
+            orig = f[name].astype(np.float64)
+            arr[:kb] = orig[:kb]
+            arr[ke:] = orig[ke:]
+    return res, f
+
+
+def rel_error(got: np.ndarray, ref: np.ndarray, layout: GridLayout) -> float:
+    gi = layout.interior(got).astype(np.float64)
+    ri = layout.interior(ref)
+    scale = np.max(np.abs(ri))
+    return float(np.max(np.abs(gi - ri)) / scale)
+
+
+def run_config(ctx, compiler, kernel, layout, config, k_range=None):
+    prob = StencilProblem(kernel, layout, ctx)
+    try:
+        d = prob.definition
+        args = prob.args(k_range)
+        from paper_2303_12374_b200.capture import scalar_env_from_args
+
+        env = scalar_env_from_args(args)
+        problem = d.derive_problem_size(env)
+        exe = compiler.compile(d.render_compile_request(config, problem, env), ctx.ident)
+        exe.load()
+        exe.launch(d.derive_geometry(config, problem, env), args, timed=True)
+        return {n: prob.download(n).copy() for n in prob.outputs()}
+    finally:
+        prob.close()

@@ -1,0 +1,93 @@
+"""GPU parity: NVRTC-compiled stencils vs the NumPy oracle (tests/stencil_helpers.py).
+
+Bar (BASELINE.json north_star): max|gpu - ref| / max|ref| <= 1e-5 (fp32),
+<= 1e-12 (fp64) per output array, ref computed in float64 from the same inputs.
+"""
+
+import numpy as np
+import pytest
+
+from stencil_helpers import TOL, host_fields, oracle_outputs, rel_error, run_config
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def compiler(gpu_ctx):
+    from paper_2303_12374_b200.cuda import NvrtcCompiler
+
+    return NvrtcCompiler(gpu_ctx)
+
+
+def _default(kernel, precision):
+    from paper_2303_12374_b200.stencils.definitions import definition_for
+
+    return definition_for(kernel, precision).space.default_config()[0]
+
+
+def test_device_synth_is_bit_exact(gpu_ctx):
+    from paper_2303_12374_b200.stencils.layout import GridLayout
+    from paper_2303_12374_b200.stencils.problem import StencilProblem
+
+    for precision in ("fp32", "fp64"):
+        lay = GridLayout(37, 29, 11, precision)
+        prob = StencilProblem("diff_uvw", lay, gpu_ctx)
+        try:
+            want = host_fields(lay, prob.fields)
+            for name in prob.fields:
+                got = prob.download(name)
+                assert np.array_equal(got, want[name]), (precision, name)
+        finally:
+            prob.close()
+
+
+@pytest.mark.parametrize("kernel", ["advec_u", "diff_uvw"])
+@pytest.mark.parametrize("precision", ["fp32", "fp64"])
+def test_default_config_matches_oracle(gpu_ctx, compiler, kernel, precision):
+    from paper_2303_12374_b200.stencils.layout import GridLayout
+
+    lay = GridLayout(64, 64, 64, precision) if kernel == "diff_uvw" else GridLayout(48, 40, 24, precision)
+    got = run_config(gpu_ctx, compiler, kernel, lay, _default(kernel, precision))
+    ref, _ = oracle_outputs(kernel, lay)
+    for name in ref:
+        err = rel_error(got[name], ref[name], lay)
+        assert err <= TOL[precision], (name, err)
+
+
+def _sample_configs(kernel, precision, n, seed):
+    from paper_2303_12374_b200.stencils.definitions import definition_for
+
+    space = definition_for(kernel, precision).space
+    cfgs = space.sample_random(seed, n)
+    zm = [c for c in space.sample_random(seed + 1, 400) if c["staging"] == "ZMARCH"][: max(2, n // 2)]
+    return cfgs + zm
+
+
+@pytest.mark.parametrize("kernel", ["advec_u", "diff_uvw"])
+@pytest.mark.parametrize("precision", ["fp32", "fp64"])
+def test_sampled_configs_match_oracle(gpu_ctx, compiler, kernel, precision):
+    """Random Table-2 + B200 configurations on a ragged grid (extents not multiples of any tile)."""
+    from paper_2303_12374_b200.stencils.layout import GridLayout
+
+    lay = GridLayout(45, 23, 19, precision)
+    ref, _ = oracle_outputs(kernel, lay)
+    for cfg in _sample_configs(kernel, precision, 6, seed=7 if precision == "fp32" else 11):
+        got = run_config(gpu_ctx, compiler, kernel, lay, cfg)
+        for name in ref:
+            err = rel_error(got[name], ref[name], lay)
+            assert err <= TOL[precision], (cfg, name, err)
+
+
+@pytest.mark.parametrize("kernel", ["advec_u", "diff_uvw"])
+def test_k_subrange_launch(gpu_ctx, compiler, kernel):
+    """Launching a k sub-range (the multi-GPU interior/boundary split) only touches those planes."""
+    from paper_2303_12374_b200.stencils.layout import GridLayout
+
+    lay = GridLayout(32, 24, 20, "fp64")
+    kr = (lay.kstart + 4, lay.kstart + 13)
+    ref, _ = oracle_outputs(kernel, lay, k_range=kr)
+    for cfg in (_default(kernel, "fp64"), dict(_default(kernel, "fp64"), staging="ZMARCH", zchunk=8, block_x=32, block_y=4)):
+        got = run_config(gpu_ctx, compiler, kernel, lay, cfg, k_range=kr)
+        for name in ref:
+            diff = np.max(np.abs(got[name].astype(np.float64) - ref[name]))
+            assert diff <= 1e-12 * np.max(np.abs(ref[name])), (cfg["staging"], name, diff)
