@@ -1,0 +1,118 @@
+"""``SlabDriver`` — one rank's share of a z-slab decomposed stencil application.
+
+Wires the pieces of ``halo.py`` to the runtime launch path:
+
+* fields of the rank's slab live in HBM (``StencilProblem`` with the global
+  plane offset, so the synthetic data are those of the undecomposed grid);
+* every sub-range (interior / lower / upper, ``SlabRank.subranges``) is
+  launched through ``WisdomKernel.launch`` — the application-facing API —
+  so each gets its own wisdom selection and compiled instance;
+* ``step()`` issues: halo exchange on the comm stream (NCCL, or D2D copies
+  for virtual ranks), the interior launch on the compute stream concurrently,
+  then the boundary launches after the exchange event.
+
+All launches are asynchronous; callers time steps with CUDA events on
+``compute`` (the comm stream is joined back into it every step).
+"""
+
+from __future__ import annotations
+
+from pathlib import Path
+
+from .capture import CapturePolicy
+from .cuda.device import DeviceContext, Event, Stream
+from .dispatch import WisdomKernel
+from .halo import HALO_REACH, SlabDecomposition, SlabRank
+from .stencils.layout import GridLayout
+from .stencils.problem import StencilProblem
+from .stencils.profiles import make_profiles
+
+__all__ = ["SlabDriver"]
+
+
+class SlabDriver:
+    def __init__(self, kernel: str, precision: str, grid: tuple[int, int, int], ctx: DeviceContext, *,
+                 rank: int = 0, nranks: int = 1, exchanger=None, compiler=None,
+                 wisdom_dir: str | Path | None = None, ghost: int = 3) -> None:
+        from .cuda.compiler import NvrtcCompiler
+
+        self.kernel, self.precision, self.grid = kernel, precision, tuple(grid)
+        self.ctx = ctx
+        self.rank, self.nranks = rank, nranks
+        self.exchanger = exchanger
+        self.global_layout = GridLayout(*grid, precision, ghost, ghost, ghost)
+        self.decomposition = SlabDecomposition(grid[2], nranks)
+        self.slab = SlabRank(self.decomposition, rank, ghost, kernel)
+        self.layout = GridLayout(grid[0], grid[1], self.slab.count, precision, ghost, ghost, ghost)
+        profiles = make_profiles(self.global_layout.kcells, ghost)
+        self.compute = ctx.stream
+        self.comm = Stream.create() if exchanger is not None else None
+        self.problem = StencilProblem(kernel, self.layout, ctx, k_offset=self.slab.offset,
+                                      kcells_global=self.global_layout.kcells, profiles=profiles, stream=self.compute)
+        self.compiler = compiler or NvrtcCompiler(ctx)
+        self.wisdom = WisdomKernel(self.problem.definition, self.compiler, wisdom_dir=wisdom_dir or ".",
+                                   capture_policy=CapturePolicy())
+        self.ranges = self.slab.subranges()
+        self.args = {name: self.problem.args(rng) for name, rng in self.ranges.items()}
+        self.below, self.above = self.decomposition.neighbours(rank)
+        self._ev_start = Event()
+        self._ev_halo = Event()
+        self.kernel_events: list[tuple[Event, Event]] = []
+        self.reports = {}
+
+    # -- setup -------------------------------------------------------------------------
+    def resolve(self) -> dict:
+        """Select + compile every sub-range before timing; returns name -> (config, match_kind)."""
+        out = {}
+        for name, args in self.args.items():
+            report = self.wisdom.launch(self.ctx.ident, args, stream=self.compute)
+            self.reports[name] = report
+            out[name] = (report.configuration, report.match_kind)
+        self.compute.synchronize()
+        self.problem.regenerate(self.problem.outputs())
+        return out
+
+    @property
+    def local_cells(self) -> int:
+        return self.layout.cells
+
+    def cells_in(self, name: str) -> int:
+        kb, ke = self.ranges[name]
+        return self.layout.itot * self.layout.jtot * (ke - kb)
+
+    # -- one application step -------------------------------------------------------------
+    def exchange(self) -> None:
+        if self.exchanger is None:
+            return
+        self._ev_start.record(self.compute)
+        self.comm.wait(self._ev_start)
+        lay = self.layout
+        for field, (down, up) in HALO_REACH[self.kernel].items():
+            self.exchanger.exchange(self.comm, [self.problem.field_ptr(field)], lay.elem_bytes, lay.kk, lay.kstart,
+                                    lay.kend, down, up, self.below, self.above)
+        self._ev_halo.record(self.comm)
+
+    def step(self, time_kernel: tuple[Event, Event] | None = None) -> int:
+        """Enqueue one step; returns the number of kernels launched."""
+        ident = self.ctx.ident
+        self.exchange()
+        launched = 0
+        if "interior" in self.args:
+            if time_kernel is not None:
+                time_kernel[0].record(self.compute)
+            self.wisdom.launch(ident, self.args["interior"], stream=self.compute)
+            if time_kernel is not None:
+                time_kernel[1].record(self.compute)
+            launched += 1
+        if self.exchanger is not None:
+            self.compute.wait(self._ev_halo)
+        for name in ("lower", "upper"):
+            if name in self.args:
+                self.wisdom.launch(ident, self.args[name], stream=self.compute)
+                launched += 1
+        return launched
+
+    def close(self) -> None:
+        self.problem.close()
+        if self.comm is not None:
+            self.comm.close()
