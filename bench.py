@@ -190,51 +190,82 @@ class ClockSampler:
 # CPU reference (the NumPy oracle on the host cores)
 
 
-def cpu_oracle_rate(kernel, precision, grid, threads, budget_s=8.0, min_reps=1):
-    """Gcells/s of the NumPy oracle over a bounded z-sample of the workload."""
-    import numpy as np
+class CpuOracle:
+    """The CPU restatement of the path on a bounded z-sample of the workload.
 
-    from oracle import stencil_oracle
-    from oracle.synth import synth_field
-    from paper_2303_12374_b200.stencils.problem import KERNEL_FIELDS
-    from paper_2303_12374_b200.stencils.profiles import FIELD_SEED_BASE, FIELD_SPECS, make_profiles
+    Prefers the C restatement (oracle/stencil_ref.c via oracle/cref.py, in the
+    workload's precision, one z-chunk per host thread); falls back to the NumPy
+    oracle (float64, threads over z-chunks) when the C library is not built.
+    Input generation happens once, outside every timed region.
+    """
 
-    itot, jtot, ktot = grid
-    g = 3
-    per_thread = 2 if itot * jtot >= 512 * 512 else 8
-    nk = min(ktot, per_thread * threads)
-    kcells = nk + 2 * g
-    dtype = np.float32 if precision == "fp32" else np.float64
-    fields = {}
-    for name in KERNEL_FIELDS[kernel]:
-        off, lo, hi = FIELD_SPECS[name]
-        fields[name] = synth_field(FIELD_SEED_BASE + off, lo, hi, itot + 2 * g, jtot + 2 * g, kcells, g, g, dtype=dtype)
-    prof = make_profiles(ktot + 2 * g, g).window(0, kcells).as_dtype(dtype)
-    chunks = [(k0, min(per_thread, nk - k0)) for k0 in range(0, nk, per_thread)]
+    def __init__(self, kernel, precision, grid, threads, planes_per_thread=None):
+        import numpy as np
 
-    def work(chunk):
-        k0, n = chunk
-        sl = slice(k0, k0 + n + 2 * g)
-        f = {k: v[sl] for k, v in fields.items()}
-        p = {k: getattr(prof, k)[sl] for k in ("rhoref", "rhorefh", "dzi", "dzhi")}
-        inter = (itot, jtot, n)
-        if kernel == "advec_u":
-            stencil_oracle.advec_u(f["ut"], f["u"], f["v"], f["w"], p["rhoref"], p["rhorefh"], p["dzi"], 1.0, 1.0,
-                                   interior=inter)
-        else:
-            stencil_oracle.diff_uvw(f["ut"], f["vt"], f["wt"], f["evisc"], f["u"], f["v"], f["w"], p["dzi"], p["dzhi"],
-                                    p["rhoref"], p["rhorefh"], 1.0, 1.0, interior=inter)
+        from oracle import cref
+        from oracle.synth import synth_field
+        from paper_2303_12374_b200.stencils.problem import KERNEL_FIELDS
+        from paper_2303_12374_b200.stencils.profiles import FIELD_SEED_BASE, FIELD_SPECS, make_profiles
 
-    times = []
-    with ThreadPoolExecutor(max_workers=threads) as pool:
-        t_end = time.perf_counter() + budget_s
-        while len(times) < min_reps or (time.perf_counter() < t_end and len(times) < 5):
+        self.kernel, self.threads = kernel, threads
+        itot, jtot, ktot = grid
+        g = 3
+        per = planes_per_thread or (4 if itot * jtot >= 512 * 512 else 16)
+        self.nk = min(ktot, per * threads)
+        self.cells = itot * jtot * self.nk
+        dtype = np.float32 if precision == "fp32" else np.float64
+        self.use_c = cref.available()
+        self.kind = "C restatement (oracle/stencil_ref.c)" if self.use_c else "NumPy oracle (float64)"
+        kc = self.nk + 2 * g
+        self.f = {}
+        for name in KERNEL_FIELDS[kernel]:
+            off, lo, hi = FIELD_SPECS[name]
+            self.f[name] = synth_field(FIELD_SEED_BASE + off, lo, hi, itot + 2 * g, jtot + 2 * g, kc, g, g,
+                                       dtype=dtype)
+        self.prof = make_profiles(ktot + 2 * g, g).window(0, kc).as_dtype(dtype)
+        self.interior = (itot, jtot, self.nk)
+        self.pool = ThreadPoolExecutor(max_workers=threads)
+
+    def step(self):
+        from oracle import cref, stencil_oracle
+
+        f, p = self.f, self.prof
+        if self.use_c:
+            if self.kernel == "advec_u":
+                cref.advec_u(f["ut"], f["u"], f["v"], f["w"], p.rhoref, p.rhorefh, p.dzi, 1.0, 1.0,
+                             threads=self.threads, pool=self.pool)
+            else:
+                cref.diff_uvw(f["ut"], f["vt"], f["wt"], f["evisc"], f["u"], f["v"], f["w"], p.dzi, p.dzhi, p.rhoref,
+                              p.rhorefh, 1.0, 1.0, threads=self.threads, pool=self.pool)
+            return
+        g = 3
+        per = max(1, -(-self.nk // self.threads))
+
+        def work(k0):
+            n = min(per, self.nk - k0)
+            sl = slice(k0, k0 + n + 2 * g)
+            ff = {k: v[sl] for k, v in f.items()}
+            pp = {k: getattr(p, k)[sl] for k in ("rhoref", "rhorefh", "dzi", "dzhi")}
+            inter = (self.interior[0], self.interior[1], n)
+            if self.kernel == "advec_u":
+                stencil_oracle.advec_u(ff["ut"], ff["u"], ff["v"], ff["w"], pp["rhoref"], pp["rhorefh"], pp["dzi"],
+                                       1.0, 1.0, interior=inter)
+            else:
+                stencil_oracle.diff_uvw(ff["ut"], ff["vt"], ff["wt"], ff["evisc"], ff["u"], ff["v"], ff["w"],
+                                        pp["dzi"], pp["dzhi"], pp["rhoref"], pp["rhorefh"], 1.0, 1.0, interior=inter)
+
+        list(self.pool.map(work, range(0, self.nk, per)))
+
+    def rate(self, reps=3):
+        times = []
+        for _ in range(reps):
             t0 = time.perf_counter()
-            list(pool.map(work, chunks))
+            self.step()
             times.append(time.perf_counter() - t0)
-    cells = itot * jtot * nk
-    t = statistics.median(times)
-    return cells / t / 1e9, {"cells": cells, "planes": nk, "reps": len(times), "seconds_per_rep": t}
+        return self.cells / statistics.median(times) / 1e9, statistics.median(times)
+
+    def close(self):
+        self.pool.shutdown()
 
 
 def host_threads():
@@ -249,19 +280,21 @@ def run_reference(args, dist):
     if dist.rank != 0:
         return 0
     threads = host_threads()
+    cpu = CpuOracle(kernel, precision, grid, threads)
+    for _ in range(args.warmup):
+        cpu.step()
     rates = []
-    for _ in range(max(args.warmup, 0)):
-        cpu_oracle_rate(kernel, precision, grid, threads, budget_s=0.0)
-    detail = None
     t_start = time.perf_counter()
     for _ in range(args.steps):
-        rate, detail = cpu_oracle_rate(kernel, precision, grid, threads, budget_s=0.0)
-        rates.append(rate)
-        if time.perf_counter() - t_start > 240:
+        t0 = time.perf_counter()
+        cpu.step()
+        rates.append(cpu.cells / (time.perf_counter() - t0) / 1e9)
+        if time.perf_counter() - t_start > 180:
             break
+    cpu.close()
     value = statistics.median(rates)
-    sample = (f"{detail['planes']} of {grid[2]} z-planes ({detail['cells']} cells) of {label}, NumPy oracle "
-              f"(oracle/stencil_oracle.py), {threads} threads over z-chunks, median of {len(rates)} steps")
+    sample = (f"{cpu.nk} of {grid[2]} z-planes ({cpu.cells} cells) of {label}; {cpu.kind}, {threads} host "
+              f"threads over z-chunks; median of {len(rates)} steps")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "Gcells/s", "n_gpus": args.gpus,
         "steps": len(rates), "warmup": args.warmup, "higher_is_better": True, "scaling": "strong",
@@ -472,11 +505,14 @@ def run_ours(args, dist):
     }
     if dist.rank == 0 and dist.world == 1 and not args.no_cpu_baseline:
         threads = host_threads()
-        rate, detail = cpu_oracle_rate(kernel, precision, grid, threads, budget_s=6.0)
+        cpu = CpuOracle(kernel, precision, grid, threads)
+        cpu.step()
+        rate, secs = cpu.rate(reps=3)
+        cpu.close()
         line["cpu_baseline"] = {
             "value": round(rate, 5), "unit": "Gcells/s", "cores": threads, "kind": "port",
-            "sample": f"{detail['planes']} z-planes ({detail['cells']} cells) of the same grid, NumPy oracle, "
-                      f"{threads} threads, median of {detail['reps']}"}
+            "sample": f"{cpu.nk} z-planes ({cpu.cells} cells) of the same grid; {cpu.kind}; {threads} host "
+                      f"threads; median of 3 ({secs:.3f} s each)"}
     if dist.rank == 0 and dist.world == 1 and args.suite:
         try:
             line["suite"] = suite_measure(ctx, compiler, wisdom_dir, peak)

@@ -14,6 +14,7 @@
  *   klb_module_load / _function    -> ExecutableHandle.load        backend.py:265-267
  *   klb_launch                     -> ExecutableHandle.launch      backend.py:269-271
  *   klb_time_launches              -> Executor.measure's timed reps backend.py:226-257, 442-468
+ *   klb_module_global / klb_tensor_map_encode_3d -> part of ExecutableHandle.launch (TMA staging)
  *   klb_synth_field                -> synthetic capture payloads   capture.py:75-98 (BufferArg.data)
  *   klb_halo_* (NCCL)              -> no reference counterpart (multi-GPU z-slabs)
  *
@@ -146,6 +147,19 @@ int klb_event_destroy(klb_event event);
 int klb_event_record(klb_event event, klb_stream stream);
 int klb_event_synchronize(klb_event event);
 int klb_event_elapsed_ms(klb_event start, klb_event stop, float* ms);
+
+/* ---- module globals / TMA descriptors ------------------------------------
+ * A runtime-compiled kernel may request TMA tensor maps for some of its
+ * pointer arguments by exporting `kl_tma_spec` (see paper_2303_12374_b200/
+ * cuda/compiler.py); the host builds them with klb_tensor_map_encode_3d and
+ * writes them into the module's `kl_tma_maps` global before launching. */
+int klb_module_global(klb_module module, const char* name, uint64_t* dptr, size_t* bytes);
+/* cuTensorMapEncodeTiled for a 3-D fp32/fp64 tensor (no swizzle, no
+ * interleave, zero OOB fill): dims = elements per dimension (innermost
+ * first), strides_bytes = byte strides of dims 1 and 2, box = box extents.
+ * Writes the 128-byte CUtensorMap to `out`. */
+int klb_tensor_map_encode_3d(void* out, int elem_bytes, uint64_t global_address, const uint64_t dims[3],
+                             const uint64_t strides_bytes[2], const unsigned box[3]);
 
 /* ---- synthetic fields (device twin of oracle/synth.py) --------------------
  * Fills a ghost-padded field: element (i, j, k) of the local array, stored at

@@ -30,7 +30,8 @@ __all__ = ["tune_problem", "main"]
 def tune_problem(kernel: str, precision: str, grid: tuple[int, int, int], ctx, *, strategy: str = "random",
                  budget: Budget | None = None, seed: int = 0, wisdom_dir: str | Path | None = "wisdom",
                  session_dir: str | Path | None = None, k_range: tuple[int, int] | None = None,
-                 repetitions: int = 7, warmup: int = 3, log=print):
+                 repetitions: int = 7, warmup: int = 3, restrict: str | None = None, family: str | None = None,
+                 log=print):
     from .cuda.executor import CudaReplayExecutor
     from .stencils.layout import GridLayout
     from .stencils.problem import StencilProblem
@@ -51,7 +52,18 @@ def tune_problem(kernel: str, precision: str, grid: tuple[int, int, int], ctx, *
 
     default_cfg = prob.definition.space.default_config()[0]
     default_m = executor.measure(default_cfg)
-    session = tune(prob.definition.space, executor, strategy=strategy, budget=budget or Budget(max_evaluations=50),
+    space = prob.definition.space
+    if family:
+        from .stencils.definitions import family_space
+
+        space = family_space(kernel, family)
+    if restrict:
+        # explore a sub-space (e.g. 'staging == "ZMARCH"'); every point is valid in the
+        # full space, so the session still feeds the kernel's real wisdom file
+        from .space import ConfigSpace
+
+        space = ConfigSpace(space.params, list(space.restrictions) + [restrict])
+    session = tune(space, executor, strategy=strategy, budget=budget or Budget(max_evaluations=50),
                    seed=seed, device=ctx.ident, kernel_key=prob.definition.kernel_key(),
                    problem=executor.problem, on_evaluation=progress)
     cells = executor.problem[0] * executor.problem[1] * executor.problem[2]
@@ -63,6 +75,8 @@ def tune_problem(kernel: str, precision: str, grid: tuple[int, int, int], ctx, *
         "default_us": default_m.objective * 1e6 if default_m.status == STATUS_OK else None,
         "best_us": session.best_objective * 1e6 if session.best_objective else None,
         "best_config": session.best_config,
+        "restrict": restrict,
+        "family": family,
     }
     for tag in ("default", "best"):
         us = summary[f"{tag}_us"]
@@ -71,7 +85,8 @@ def tune_problem(kernel: str, precision: str, grid: tuple[int, int, int], ctx, *
             summary[f"{tag}_gbs"] = cells * words * layout.elem_bytes / (us * 1e-6) / 1e9
     if session_dir is not None:
         Path(session_dir).mkdir(parents=True, exist_ok=True)
-        stem = f"{kernel}_{precision}_{'x'.join(map(str, executor.problem))}.{strategy}.seed{seed}"
+        tag = (f".{family.lower()}" if family else "") + (".restricted" if restrict else "")
+        stem = f"{kernel}_{precision}_{'x'.join(map(str, executor.problem))}.{strategy}{tag}.seed{seed}"
         save_session(session, Path(session_dir) / f"{stem}.klsession")
     if wisdom_dir is not None and session.best is not None:
         wfile = load_or_create(wisdom_dir, session.kernel_key)
@@ -100,6 +115,9 @@ def main(argv=None) -> int:
     ap.add_argument("--sessions", default=None)
     ap.add_argument("--device", type=int, default=0)
     ap.add_argument("--json-out", default=None)
+    ap.add_argument("--restrict", default=None, help="extra restriction expression to explore a sub-space")
+    ap.add_argument("--family", choices=("DIRECT", "ZMARCH", "TMA"), default=None,
+                    help="tune one staging family (its fixed knobs narrowed; see definitions.family_space)")
     a = ap.parse_args(argv)
     from .cuda import open_device
 
@@ -107,7 +125,7 @@ def main(argv=None) -> int:
     grid = tuple(int(x) for x in a.grid.split(","))
     _, summary = tune_problem(a.kernel, a.precision, grid, ctx, strategy=a.strategy,
                               budget=Budget(a.budget_evals, a.budget_seconds), seed=a.seed, wisdom_dir=a.wisdom,
-                              session_dir=a.sessions)
+                              session_dir=a.sessions, restrict=a.restrict, family=a.family)
     line = json.dumps(summary, sort_keys=True)
     print(line)
     if a.json_out:

@@ -42,7 +42,7 @@ int g_default_ordinal = -1;
 // CUDA driver API, resolved at runtime through cudaGetDriverEntryPoint so the
 // library has no link-time dependency on libcuda.so.1: it loads (and reports
 // a clean error from klb_init) on hosts without an NVIDIA driver.
-#define KLB_DRIVER_API(X) X(cuCtxGetCurrent) X(cuCtxSetCurrent) X(cuCtxSynchronize) X(cuDeviceGet) X(cuDeviceGetAttribute) X(cuDeviceGetCount) X(cuDeviceGetName) X(cuDeviceGetUuid) X(cuDevicePrimaryCtxRetain) X(cuDeviceTotalMem) X(cuDriverGetVersion) X(cuEventCreate) X(cuEventDestroy) X(cuEventElapsedTime) X(cuEventRecord) X(cuEventSynchronize) X(cuFuncGetAttribute) X(cuFuncSetAttribute) X(cuGetErrorName) X(cuGetErrorString) X(cuInit) X(cuLaunchKernel) X(cuMemAlloc) X(cuMemFree) X(cuMemFreeHost) X(cuMemGetInfo) X(cuMemHostAlloc) X(cuMemcpyDtoDAsync) X(cuMemcpyDtoHAsync) X(cuMemcpyHtoDAsync) X(cuMemsetD32Async) X(cuMemsetD8Async) X(cuModuleGetFunction) X(cuModuleLoadData) X(cuModuleUnload) X(cuOccupancyMaxActiveBlocksPerMultiprocessor) X(cuStreamCreateWithPriority) X(cuStreamDestroy) X(cuStreamSynchronize) X(cuStreamWaitEvent)
+#define KLB_DRIVER_API(X) X(cuCtxGetCurrent) X(cuCtxSetCurrent) X(cuCtxSynchronize) X(cuDeviceGet) X(cuDeviceGetAttribute) X(cuDeviceGetCount) X(cuDeviceGetName) X(cuDeviceGetUuid) X(cuDevicePrimaryCtxRetain) X(cuDeviceTotalMem) X(cuDriverGetVersion) X(cuEventCreate) X(cuEventDestroy) X(cuEventElapsedTime) X(cuEventRecord) X(cuEventSynchronize) X(cuFuncGetAttribute) X(cuFuncSetAttribute) X(cuGetErrorName) X(cuGetErrorString) X(cuInit) X(cuLaunchKernel) X(cuMemAlloc) X(cuMemFree) X(cuMemFreeHost) X(cuMemGetInfo) X(cuMemHostAlloc) X(cuMemcpyDtoDAsync) X(cuMemcpyDtoHAsync) X(cuMemcpyHtoDAsync) X(cuMemsetD32Async) X(cuMemsetD8Async) X(cuModuleGetFunction) X(cuModuleLoadData) X(cuModuleUnload) X(cuOccupancyMaxActiveBlocksPerMultiprocessor) X(cuStreamCreateWithPriority) X(cuStreamDestroy) X(cuStreamSynchronize) X(cuStreamWaitEvent) X(cuModuleGetGlobal) X(cuTensorMapEncodeTiled)
 
 struct DriverApi {
 #define KLB_DECL(name) decltype(&::name) name = nullptr;
@@ -600,6 +600,35 @@ int klb_event_synchronize(klb_event event) {
 int klb_event_elapsed_ms(klb_event start, klb_event stop, float* ms) {
   CTX_TRY();
   CU_TRY(drv.cuEventElapsedTime(ms, reinterpret_cast<CUevent>(start), reinterpret_cast<CUevent>(stop)));
+  return 0;
+}
+
+// ---- module globals / TMA descriptors --------------------------------------------
+
+int klb_module_global(klb_module module, const char* name, uint64_t* dptr, size_t* bytes) {
+  CTX_TRY();
+  CUdeviceptr p = 0;
+  size_t n = 0;
+  CU_TRY(drv.cuModuleGetGlobal(&p, &n, reinterpret_cast<CUmodule>(module), name));
+  if (dptr) *dptr = static_cast<uint64_t>(p);
+  if (bytes) *bytes = n;
+  return 0;
+}
+
+int klb_tensor_map_encode_3d(void* out, int elem_bytes, uint64_t global_address, const uint64_t dims[3],
+                             const uint64_t strides_bytes[2], const unsigned box[3]) {
+  if (!out || (elem_bytes != 4 && elem_bytes != 8)) return fail(KLB_E_INVALID, "bad tensor map request");
+  if (int e = load_driver_api()) return e;
+  CUtensorMap map;
+  const cuuint64_t gdim[3] = {dims[0], dims[1], dims[2]};
+  const cuuint64_t gstride[2] = {strides_bytes[0], strides_bytes[1]};
+  const cuuint32_t bdim[3] = {box[0], box[1], box[2]};
+  const cuuint32_t estride[3] = {1, 1, 1};
+  CU_TRY(drv.cuTensorMapEncodeTiled(&map, elem_bytes == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64,
+                                    3, reinterpret_cast<void*>(global_address), gdim, gstride, bdim, estride,
+                                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE));
+  std::memcpy(out, &map, sizeof(map));
   return 0;
 }
 

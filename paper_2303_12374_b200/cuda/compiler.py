@@ -178,6 +178,7 @@ class CudaExecutable(ExecutableHandle):
         self._smem_opt_in = 48 * 1024
         self._packed: dict = {}
         self.launch_count = 0
+        self.tma_spec: list[tuple[int, int, int, int, int]] = []
 
     # -- ExecutableHandle ---------------------------------------------------------
     def load(self) -> None:
@@ -193,6 +194,38 @@ class CudaExecutable(ExecutableHandle):
         except KlbError as err:
             raise LaunchError(str(err)) from err
         self.module, self.function, self.attrs = mod.value, fn.value, attrs
+        self._read_tma_spec()
+
+    # -- TMA descriptors (kernels exporting kl_tma_spec, see stencils/kl_tma.cuh) ----
+    def _read_tma_spec(self) -> None:
+        ptr, size = C.c_uint64(), C.c_size_t()
+        if lib().klb_module_global(self.module, b"kl_tma_spec", C.byref(ptr), C.byref(size)) != 0:
+            return  # the kernel does not use TMA
+        raw = (C.c_int * (size.value // 4))()
+        check(lib().klb_memcpy_dtoh(raw, ptr.value, size.value, None))
+        check(lib().klb_device_synchronize())
+        self.tma_spec = [tuple(raw[1 + 5 * m: 6 + 5 * m]) for m in range(raw[0])]
+
+    def _tma_blob(self, args: Sequence[object]):
+        """The kernel's trailing ``__grid_constant__`` tensor-map parameter (N x 128 B)."""
+        by_pos = {a.position: a for a in args}
+        blob = (C.c_ubyte * (128 * len(self.tma_spec)))()
+        for m, (pos, jpos, kpos, bw, bh) in enumerate(self.tma_spec):
+            buf = by_pos[pos]
+            if not isinstance(buf, DeviceBuffer):
+                raise LaunchError("TMA staging needs device-resident buffers")
+            width = 4 if buf.element_type == "f32" else 8
+            jj, kk = int(by_pos[jpos].value), int(by_pos[kpos].value)
+            xoff = (buf.ptr & 15) // width
+            dims = (C.c_uint64 * 3)(jj, kk // jj, buf.element_count // kk)
+            strides = (C.c_uint64 * 2)(jj * width, kk * width)
+            box = (C.c_uint * 3)(bw, bh, 1)
+            try:
+                check(lib().klb_tensor_map_encode_3d(C.byref(blob, 128 * m), width, buf.ptr - xoff * width, dims,
+                                                     strides, box))
+            except KlbError as err:
+                raise LaunchError(str(err)) from err
+        return blob
 
     def _prepare(self, geometry: LaunchGeometry):
         if self.function is None:
@@ -215,6 +248,8 @@ class CudaExecutable(ExecutableHandle):
             if hit is None:
                 keep: list = []
                 params, _ = pack_args(args, keep)
+                if self.tma_spec:
+                    params = self._with_tma(params, args, keep)
                 hit = (params, keep)
                 if len(self._packed) > 256:
                     self._packed.clear()
@@ -222,7 +257,16 @@ class CudaExecutable(ExecutableHandle):
             return hit[0], hit[1], []
         keep = []
         params, staged = pack_args(args, keep, stream)
+        if self.tma_spec:
+            raise LaunchError("TMA staging needs device-resident buffers")
         return params, keep, staged
+
+    def _with_tma(self, params, args, keep):
+        blob = self._tma_blob(args)
+        keep.append(blob)
+        full = (C.c_void_p * (len(params) + 1))(*params)
+        full[len(params)] = C.cast(blob, C.c_void_p)
+        return full
 
     def launch(self, geometry: LaunchGeometry, args: Sequence[object], stream: Stream | None = None,
                timed: bool = False, outputs: dict | None = None) -> float:

@@ -14,11 +14,11 @@
 // Variant selected by STAGING (a B200 knob added to the Table-2 space):
 //   0  direct: every thread covers a TILE_X*TILE_Y*TILE_Z tile with global
 //      loads (the paper's kernel; neighbours come from L1/L2);
-//   1  zmarch: a BLOCK_X x (BLOCK_Y*TILE_Y) column marches along k through
-//      ZCHUNK planes; the u stencil's 7 z-neighbours and the w plane stay in
-//      registers, x/y neighbours come from a halo'd shared-memory plane
-//      refilled each step, and the x/z face fluxes are computed once per face
-//      (reused by the neighbouring cell) — see docs in DESIGN.md.
+//   1  ZMARCH: flux-form z-march; every face flux evaluated once (z carried,
+//      y reused along a TILE_Y strip, x via warp shuffles); u planes staged
+//      through registers into shared memory (advec_u_zmarch.cuh);
+//   2  TMA: the same compute with u planes staged by the Tensor Memory
+//      Accelerator DEPTH planes ahead (advec_u_tma.cuh).
 
 #include "kl_common.cuh"
 
@@ -102,6 +102,8 @@ KL_ENTRY(real* __restrict__ ut, const real* __restrict__ u, const real* __restri
   }
 }
 
-#else
+#elif STAGING == 1
 #include "advec_u_zmarch.cuh"
+#else
+#include "advec_u_tma.cuh"
 #endif

@@ -38,14 +38,15 @@ from ..space import ConfigSpace, TunableParam
 
 __all__ = [
     "KERNELS", "PRECISIONS", "stencil_space", "advec_u_definition", "diff_uvw_definition", "definition_for",
-    "assemble_source", "ARG_LAYOUT",
+    "assemble_source", "ARG_LAYOUT", "family_space", "FAMILY_PINS",
 ]
 
 _HERE = Path(__file__).resolve().parent
 PRECISIONS = {"fp32": "float", "fp64": "double"}
 KERNELS = ("advec_u", "diff_uvw")
 
-STAGING_VALUES = ("DIRECT", "ZMARCH")
+STAGING_VALUES = ("DIRECT", "ZMARCH", "TMA")
+DEPTH_VALUES = (0, 1, 2, 3)
 ZCHUNK_VALUES = (1, 8, 16, 32, 64, 128)
 
 #: argument positions of each kernel's MicroHH-style signature
@@ -73,17 +74,18 @@ def _pos(kernel: str, name: str) -> int:
 _INCLUDE = re.compile(r'^\s*#\s*include\s+"([^"]+)"\s*$', re.M)
 
 
-def _inline(path: Path, seen: set[str]) -> str:
+def _inline(path: Path, depth: int = 0) -> str:
+    """Textually inline local ``#include "x"`` (headers carry include guards, so
+    every occurrence is inlined and the preprocessor picks the live ones)."""
+    if depth > 8:
+        raise RecursionError(f"include nesting too deep at {path.name}")
     text = path.read_text(encoding="utf-8")
 
     def repl(m: re.Match) -> str:
         name = m.group(1)
-        if name in seen:
-            return f"// (already included: {name})"
-        seen.add(name)
-        return f"// ---- begin {name} ----\n{_inline(_HERE / name, seen)}\n// ---- end {name} ----"
+        return f"// ---- begin {name} ----\n{_inline(_HERE / name, depth + 1)}\n// ---- end {name} ----"
 
-    return _INCLUDE.sub(repl, text).replace("#pragma once", "")
+    return _INCLUDE.sub(repl, text)
 
 
 @lru_cache(maxsize=None)
@@ -95,16 +97,28 @@ def assemble_source(kernel: str, precision: str) -> str:
         f"// {kernel} ({precision}) — B200 Kernel Launcher stencil, runtime-compiled by NVRTC\n"
         f"#define KL_REAL {PRECISIONS[precision]}\n"
         f"#define KL_ENTRY {kernel}_{precision}\n"
-        "#define DIRECT 0\n#define ZMARCH 1\n"
+        "#define DIRECT 0\n#define ZMARCH 1\n#define TMA 2\n"
     )
-    return prelude + _inline(_HERE / f"{kernel}.cu", set())
+    return prelude + _inline(_HERE / f"{kernel}.cu")
 
 
 #: ZMARCH shared-memory plane budget per kernel, in halo'd cells per plane
 #: (keeps fp64 staging <= ~96 KB so at least two blocks fit per SM).
 _ZMARCH_PLANE_LIMIT = {
-    "advec_u": "(block_x * tile_x + 6) * (block_y * tile_y + 6) <= 6144",
-    "diff_uvw": "(block_x * tile_x + 2) * (block_y * tile_y + 2) <= 768",
+    "advec_u": "(block_x + 6) * (block_y * tile_y + 6) <= 6144",
+    "diff_uvw": "(block_x + 2) * (block_y * tile_y + 2) <= 1024",
+}
+#: TMA box extents are <= 256 elements; the smem ring must fit the opt-in limit
+_TMA_LIMIT = {
+    "diff_uvw": ['staging != "TMA" || (block_x + 6) * (block_y * tile_y + 2) * (depth + 2) <= 3072'],
+    "advec_u": ['staging != "TMA" || (block_x + 12) * (block_y * tile_y + 6) * (depth + 4) <= 12288'],
+}
+#: knobs the ZMARCH variant of each kernel fixes (pinned to their defaults)
+_ZMARCH_PINNED = {
+    # warps along x (block_x % 32 == 0), one column per thread, contiguous y strip
+    "advec_u": "block_x >= 32 && tile_x == 1 && !unroll_x && !unroll_y && !contiguous_x && !contiguous_y",
+    # one column per thread, a contiguous strip of tile_y rows (flux reuse along y)
+    "diff_uvw": "tile_x == 1 && !unroll_x && !unroll_y && !contiguous_x && !contiguous_y",
 }
 
 
@@ -113,25 +127,70 @@ def stencil_space(kernel: str = "advec_u") -> ConfigSpace:
     params = table2_params() + [
         TunableParam("staging", STAGING_VALUES, "DIRECT"),
         TunableParam("zchunk", ZCHUNK_VALUES, 1),
+        TunableParam("depth", DEPTH_VALUES, 0),
     ]
     restrictions = [
         BLOCK_LIMIT_RESTRICTION,
-        'staging == "ZMARCH" || zchunk == 1',
+        'staging != "DIRECT" || zchunk == 1',
         'staging == "DIRECT" || (zchunk > 1 && block_z == 1 && tile_z == 1 && !unroll_z && !contiguous_z)',
-        # a ZMARCH block must hold at least one warp of columns
+        # TMA prefetch depth only exists for TMA staging
+        '(staging == "TMA" && depth > 0) || (staging != "TMA" && depth == 0)',
+        # a marching block must hold at least one warp of columns
         'staging == "DIRECT" || block_x * block_y >= 32',
-        # register-resident tiles: the tile loops are always unrolled under ZMARCH
-        'staging == "DIRECT" || (!unroll_x && !unroll_y)',
+        # register-resident tiles: the tile loops are always unrolled when marching
+        f'staging == "DIRECT" || ({_ZMARCH_PINNED[kernel]})',
         f'staging == "DIRECT" || ({_ZMARCH_PLANE_LIMIT[kernel]})',
-    ]
+    ] + _TMA_LIMIT.get(kernel, [])
     return ConfigSpace(params, restrictions)
+
+
+#: per staging family, the knobs it fixes (value lists narrowed to one value)
+_MARCH_PINS = {"block_z": 1, "tile_z": 1, "unroll_x": False, "unroll_y": False, "unroll_z": False,
+               "contiguous_z": False}
+FAMILY_PINS = {
+    "DIRECT": {"staging": "DIRECT", "zchunk": 1, "depth": 0},
+    "ZMARCH": dict(_MARCH_PINS, staging="ZMARCH", depth=0),
+    "TMA": dict(_MARCH_PINS, staging="TMA"),
+}
+_FAMILY_EXTRA = {
+    (kernel, fam): {"tile_x": 1, "contiguous_x": False, "contiguous_y": False}
+    for kernel in ("diff_uvw", "advec_u") for fam in ("ZMARCH", "TMA")
+}
+
+
+def family_space(kernel: str, family: str) -> ConfigSpace:
+    """The kernel's space with the family's fixed knobs narrowed to one value.
+
+    Every point is valid in (and measured as) the full ``stencil_space`` — the
+    narrowing only makes rejection sampling efficient: ZMARCH points are ~1e-4
+    of the full product, so unrestricted random search would almost never
+    reach them.  Tuning runs one session per family and keeps the best in the
+    kernel's wisdom file (keep-best append, wisdom.py:151-178).
+    """
+    full = stencil_space(kernel)
+    pins = dict(FAMILY_PINS[family], **_FAMILY_EXTRA.get((kernel, family), {}))
+    params = [TunableParam(p.name, (pins[p.name],), pins[p.name]) if p.name in pins else p for p in full.params]
+    return ConfigSpace(params, full.restrictions)
 
 
 _SMEM = {
     # ZMARCH shared-memory bytes (see *_zmarch.cuh): advec_u double-buffers one
-    # 3-halo plane of u; diff_uvw keeps a 4-slot ring of 1-halo planes of 4 fields.
-    "advec_u": "(2 * (block_x * tile_x + 6) * (block_y * tile_y + 6)) * {S}",
-    "diff_uvw": "(16 * (block_x * tile_x + 2) * (block_y * tile_y + 2)) * {S}",
+    # 3-halo plane of u; diff_uvw keeps a 3-slot ring of 1-halo planes of 4 fields.
+    "advec_u": "(2 * (block_x + 6) * (block_y * tile_y + 6)) * {S}",
+    "diff_uvw": "(12 * (block_x + 2) * (block_y * tile_y + 2)) * {S}",
+}
+
+
+# TMA ring: 128 B alignment slack + 128 B of mbarriers + ring slots of 128-B
+# aligned field-planes (diff_uvw: depth+2 slots x 4 fields; advec_u: depth+4
+# slots of u, since plane k+3 feeds the z-window); box width = block_x + halo
+# plus up to one 16-byte chunk of alignment slack, rounded to 16 B.
+_BW = "(ceil_div((block_x + {H}) * {S} + 16 - {S}, 16) * 16 / {S})"
+_SMEM_TMA = {
+    "diff_uvw": "(256 + (depth + 2) * 4 * ceil_div(" + _BW.format(H=2, S="{S}") +
+                " * (block_y * tile_y + 2) * {S}, 128) * 128)",
+    "advec_u": "(256 + (depth + 4) * ceil_div(" + _BW.format(H=6, S="{S}") +
+               " * (block_y * tile_y + 6) * {S}, 128) * 128)",
 }
 
 
@@ -151,7 +210,7 @@ def _definition(kernel: str, precision: str) -> KernelDefinition:
         ("UNROLL_X", "unroll_x"), ("UNROLL_Y", "unroll_y"), ("UNROLL_Z", "unroll_z"),
         ("CONTIG_X", "contiguous_x"), ("CONTIG_Y", "contiguous_y"), ("CONTIG_Z", "contiguous_z"),
         ("UNRAVEL", "unravel"), ("MIN_BLOCKS", "min_blocks"),
-        ("STAGING", "staging"), ("ZCHUNK", "zchunk"),
+        ("STAGING", "staging"), ("ZCHUNK", "zchunk"), ("DEPTH", "depth"),
         ("KL_JJ", p("jj")), ("KL_KK", p("kk")),
     ]
     return KernelDefinition(
@@ -161,7 +220,8 @@ def _definition(kernel: str, precision: str) -> KernelDefinition:
         problem_size=(f"{p('iend')} - {p('istart')}", f"{p('jend')} - {p('jstart')}", f"{p('kend')} - {p('kstart')}"),
         block=("block_x", "block_y", "block_z"),
         grid=(grid_x, 1, 1),
-        shared_mem="min(zchunk - 1, 1) * " + _SMEM[kernel].format(S=size),
+        shared_mem=(f"min(zchunk - 1, 1) * ((1 - min(depth, 1)) * {_SMEM[kernel].format(S=size)}"
+                    f" + min(depth, 1) * {_SMEM_TMA[kernel].format(S=size)})"),
         defines=defines,
         flags=("-std=c++17",),
     )

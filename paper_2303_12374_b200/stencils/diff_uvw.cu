@@ -9,8 +9,10 @@
 // write ut, vt, wt = 10 words per cell.
 //
 // STAGING 0: direct global loads (paper kernel, Table-2 knobs);
-// STAGING 1: z-marching column with a 3-plane register window per field and
-//            halo'd shared-memory planes for the x/y neighbours.
+// STAGING 1 (ZMARCH): flux-form z-march, planes staged through registers into
+//            a shared-memory ring (diff_uvw_zmarch.cuh);
+// STAGING 2 (TMA): same compute, planes staged by the Tensor Memory
+//            Accelerator DEPTH planes ahead (diff_uvw_tma.cuh).
 
 #include "kl_common.cuh"
 
@@ -147,6 +149,8 @@ KL_ENTRY(real* __restrict__ ut, real* __restrict__ vt, real* __restrict__ wt, co
   }
 }
 
-#else
+#elif STAGING == 1
 #include "diff_uvw_zmarch.cuh"
+#else
+#include "diff_uvw_tma.cuh"
 #endif

@@ -1,0 +1,149 @@
+// diff_uvw_tma.cuh — STAGING == TMA variant of diff_uvw (included by
+// diff_uvw.cu).  Same flux-form plane step as ZMARCH (diff_uvw_flux.cuh), but
+// the halo'd planes of evisc, u, v and w are fetched by the Tensor Memory
+// Accelerator: one elected thread issues cp.async.bulk.tensor.3d copies DEPTH
+// planes ahead of the compute into a (DEPTH+2)-slot shared-memory ring, each
+// slot completing on its own mbarrier (expect_tx bytes).  Staging costs no
+// registers and no load instructions in the compute warps, and DEPTH planes x
+// 4 fields of each block are in flight — the memory-level parallelism the
+// register-prefetch ZMARCH variant lacks (ncu: long_scoreboard-bound at 25%
+// occupancy).  Out-of-box rows/columns are zero-filled by the TMA unit (they
+// only feed cells outside the grid, which are never stored).
+
+#if BLOCK_Z != 1 || TILE_Z != 1 || TILE_X != 1
+#error "diff_uvw TMA requires BLOCK_Z == TILE_Z == TILE_X == 1"
+#endif
+#ifndef DEPTH
+#define DEPTH 2
+#endif
+
+#include "diff_uvw_flux.cuh"
+#include "kl_tma.cuh"
+
+namespace {
+constexpr int kS = static_cast<int>(sizeof(real));
+constexpr int kTYT = BLOCK_Y * TILE_Y;
+// Box width: BLOCK_X + 2 halo columns, started at a 16-byte aligned x (TMA
+// faults on an unaligned innermost box start) -> up to 16/kS - 1 extra
+// columns on the left, total rounded to a 16-byte multiple.
+constexpr int kBW = (((BLOCK_X + 2) * kS + 16 - kS + 15) / 16) * 16 / kS;
+constexpr int kBH = kTYT + 2;
+constexpr int kFSB = ((kBW * kBH * kS + 127) / 128) * 128;  // bytes per field-plane (128-B aligned)
+constexpr int kFS = kFSB / kS;
+constexpr int kSlot = 4 * kFS;
+constexpr int kNS = DEPTH + 2;
+constexpr unsigned kTxBytes = 4u * kBW * kBH * kS;
+static_assert(kBW <= 256 && kBH <= 256, "TMA box extents are limited to 256");
+}  // namespace
+
+// positions: evisc=3 u=4 v=5 w=6, jj=13 kk=14 (definitions.ARG_LAYOUT["diff_uvw"])
+extern "C" __device__ const int kl_tma_spec[1 + 5 * 4] = {4, 3, 13, 14, kBW, kBH, 4, 13, 14, kBW, kBH,
+                                                          5, 13, 14, kBW, kBH, 6, 13, 14, kBW, kBH};
+struct __align__(64) KlTmaParams {
+  TmaDesc map[4];
+};
+
+extern "C" __global__ void __launch_bounds__(KL_THREADS, MIN_BLOCKS)
+KL_ENTRY(real* __restrict__ ut, real* __restrict__ vt, real* __restrict__ wt, const real* __restrict__ evisc,
+         const real* __restrict__ u, const real* __restrict__ v, const real* __restrict__ w,
+         const real* __restrict__ dzi, const real* __restrict__ dzhi, const real* __restrict__ rhoref,
+         const real* __restrict__ rhorefh, const real dxi, const real dyi, const int jj, const int kk,
+         const int istart, const int jstart, const int kstart, const int iend, const int jend, const int kend, const __grid_constant__ KlTmaParams tma) {
+  if (jj != KL_JJ || kk != KL_KK) __trap();
+  // param-space address of the descriptors (__grid_constant__: no local copy)
+  const TmaDesc* const maps = &tma.map[0];
+  extern __shared__ __align__(128) unsigned char kl_smem_raw[];
+  unsigned char* base = kl_smem_raw + ((128u - (kl::smem_u32(kl_smem_raw) & 127u)) & 127u);
+  unsigned long long* full = reinterpret_cast<unsigned long long*>(base);  // kNS mbarriers
+  real* const ring = reinterpret_cast<real*>(base + 128);                  // [kNS][4][kFS]
+
+  const unsigned nbx = kl::ceil_div(iend - istart, BLOCK_X);
+  const unsigned nby = kl::ceil_div(jend - jstart, kTYT);
+  const unsigned nbz = kl::ceil_div(kend - kstart, ZCHUNK);
+  int bx, by, bz;
+  kl::unravel(blockIdx.x, nbx, nby, nbz, bx, by, bz);
+  const int i0 = istart + bx * BLOCK_X;
+  const int j0 = jstart + by * kTYT;
+  const int k0 = kstart + bz * ZCHUNK;
+  const int k1 = min(k0 + ZCHUNK, kend);
+  const int tid = threadIdx.x + threadIdx.y * BLOCK_X;
+  const int xfirst = i0 - 1 + kl::tma_xoff(evisc);  // tensor x of column i0-1 (all fields share the layout)
+  const int x0 = xfirst & ~(16 / kS - 1);          // 16-byte aligned box start
+  const int cshift = xfirst - x0;                  // extra leading columns in the tile
+  const int kfirst = k0 - 1;                     // first staged plane
+
+  // plane p lives in slot (p - kfirst) % kNS; its mbarrier phase is ((p - kfirst) / kNS) & 1
+  auto issue = [&](int p) {
+    const int rel = p - kfirst;
+    unsigned long long* bar = full + rel % kNS;
+    real* dst = ring + (rel % kNS) * kSlot;
+    kl::mbar_expect_tx(bar, kTxBytes);
+#pragma unroll
+    for (int f = 0; f < 4; ++f) kl::tma_load_3d(dst + f * kFS, maps + f, bar, x0, j0 - 1, p);
+  };
+  auto wait = [&](int p) {
+    const int rel = p - kfirst;
+    kl::mbar_wait(full + rel % kNS, (rel / kNS) & 1);
+  };
+  auto plane = [&](int p) { return ring + ((p - kfirst) % kNS) * kSlot; };
+
+  if (tid == 0) {
+    for (int s = 0; s < kNS; ++s) kl::mbar_init(full + s, 1);
+    kl::mbar_init_fence();
+  }
+  __syncthreads();
+  if (tid == 0) {
+    for (int p = kfirst; p <= min(kfirst + kNS - 1, k1); ++p) issue(p);
+  }
+
+  const real c2x = real(2) * dxi * dxi;
+  const real c2y = real(2) * dyi * dyi;
+  const int lj0 = threadIdx.y * TILE_Y;
+  const int off = lj0 * kBW + threadIdx.x + 1 + cshift;  // (strip row -1, this column) inside a field-plane
+  const int i = i0 + threadIdx.x;
+  DiffCarry carry;
+  real dut[TILE_Y], dvt[TILE_Y], dwt[TILE_Y];
+
+  wait(kfirst);
+  wait(kfirst + 1);
+  diff_step<false, kBW>(plane(kfirst) + off, plane(kfirst + 1) + off, kFS, carry, dxi, dyi, c2x, c2y,
+                        rhorefh[k0], dzhi[k0], rhoref[kfirst] * dzi[kfirst], real(0), real(0), dut, dvt, dwt);
+
+  for (int k = k0; k < k1; ++k) {
+    __syncthreads();  // everyone is done with plane k-1's slot
+    if (tid == 0) {
+      const int p = k - 1 + kNS;  // refill the slot plane k-1 vacated
+      if (p <= k1) {
+        kl::fence_proxy_async_smem();
+        issue(p);
+      }
+    }
+    // RMW operands of this plane: issue the loads before waiting on the staged plane
+    real ot[TILE_Y], ov[TILE_Y], ow[TILE_Y];
+    const bool col_ok = i < iend;
+#pragma unroll
+    for (int t = 0; t < TILE_Y; ++t) {
+      const int j = j0 + lj0 + t;
+      const long long ijk = i + static_cast<long long>(j) * KL_JJ + static_cast<long long>(k) * KL_KK;
+      const bool ok = col_ok && j < jend;
+      ot[t] = ok ? ut[ijk] : real(0);
+      ov[t] = ok ? vt[ijk] : real(0);
+      ow[t] = ok ? wt[ijk] : real(0);
+    }
+    wait(k + 1);
+    const real fac_uv = dzi[k] / rhoref[k];
+    const real fac_w = real(2) * dzhi[k] / rhorefh[k];
+    diff_step<true, kBW>(plane(k) + off, plane(k + 1) + off, kFS, carry, dxi, dyi, c2x, c2y, rhorefh[k + 1],
+                         dzhi[k + 1], rhoref[k] * dzi[k], fac_uv, fac_w, dut, dvt, dwt);
+#pragma unroll
+    for (int t = 0; t < TILE_Y; ++t) {
+      const int j = j0 + lj0 + t;
+      if (col_ok && j < jend) {
+        const long long ijk = i + static_cast<long long>(j) * KL_JJ + static_cast<long long>(k) * KL_KK;
+        ut[ijk] = ot[t] + dut[t];
+        vt[ijk] = ov[t] + dvt[t];
+        wt[ijk] = ow[t] + dwt[t];
+      }
+    }
+  }
+}

@@ -17,7 +17,8 @@
 // specialised at compile time from the launch's scalar arguments, so every
 // neighbour offset becomes an immediate in the SASS addressing mode.
 
-#pragma once
+#ifndef KL_COMMON_CUH
+#define KL_COMMON_CUH
 
 #ifndef KL_REAL
 #error "KL_REAL (float|double) must be defined"
@@ -106,3 +107,5 @@ __device__ __forceinline__ T flux5x60(T vel, T a, T b, T c, T d, T e, T f) {
 }
 
 }  // namespace kl
+
+#endif  // KL_COMMON_CUH

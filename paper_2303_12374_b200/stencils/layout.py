@@ -78,7 +78,9 @@ class GridLayout:
 
     @property
     def jj(self) -> int:
-        return -(-self.icells // self.align) * self.align
+        # +1: the TMA tensor map is built over the 16-byte-aligned base just below
+        # element (0,0,0) (one element lower), so a row must hold icells + 1.
+        return -(-(self.icells + 1) // self.align) * self.align
 
     @property
     def lead(self) -> int:

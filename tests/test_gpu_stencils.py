@@ -55,12 +55,16 @@ def test_default_config_matches_oracle(gpu_ctx, compiler, kernel, precision):
 
 
 def _sample_configs(kernel, precision, n, seed):
-    from paper_2303_12374_b200.stencils.definitions import definition_for
+    """n configurations per staging family (DIRECT / ZMARCH / TMA)."""
+    from paper_2303_12374_b200.stencils.definitions import FAMILY_PINS, definition_for, family_space
 
     space = definition_for(kernel, precision).space
-    cfgs = space.sample_random(seed, n)
-    zm = [c for c in space.sample_random(seed + 1, 400) if c["staging"] == "ZMARCH"][: max(2, n // 2)]
-    return cfgs + zm
+    cfgs = []
+    for fam in FAMILY_PINS:
+        for c in family_space(kernel, fam).sample_random(seed, n):
+            assert space.is_valid(c)
+            cfgs.append(c)
+    return cfgs
 
 
 @pytest.mark.parametrize("kernel", ["advec_u", "diff_uvw"])
@@ -71,7 +75,7 @@ def test_sampled_configs_match_oracle(gpu_ctx, compiler, kernel, precision):
 
     lay = GridLayout(45, 23, 19, precision)
     ref, _ = oracle_outputs(kernel, lay)
-    for cfg in _sample_configs(kernel, precision, 6, seed=7 if precision == "fp32" else 11):
+    for cfg in _sample_configs(kernel, precision, 3, seed=7 if precision == "fp32" else 11):
         got = run_config(gpu_ctx, compiler, kernel, lay, cfg)
         for name in ref:
             err = rel_error(got[name], ref[name], lay)
@@ -86,7 +90,8 @@ def test_k_subrange_launch(gpu_ctx, compiler, kernel):
     lay = GridLayout(32, 24, 20, "fp64")
     kr = (lay.kstart + 4, lay.kstart + 13)
     ref, _ = oracle_outputs(kernel, lay, k_range=kr)
-    for cfg in (_default(kernel, "fp64"), dict(_default(kernel, "fp64"), staging="ZMARCH", zchunk=8, block_x=32, block_y=4)):
+    for cfg in (_default(kernel, "fp64"), dict(_default(kernel, "fp64"), staging="ZMARCH", zchunk=8, block_x=32, block_y=4),
+                dict(_default(kernel, "fp64"), staging="TMA", zchunk=8, block_x=32, block_y=4, depth=2)):
         got = run_config(gpu_ctx, compiler, kernel, lay, cfg, k_range=kr)
         for name in ref:
             diff = np.max(np.abs(got[name].astype(np.float64) - ref[name]))

@@ -1,0 +1,66 @@
+"""Stencil definitions on the reference API; NVRTC compiles sampled
+configurations of every kernel/precision for sm_100a (no GPU needed)."""
+
+import pytest
+
+from paper_2303_12374_b200.backend import DeviceIdent
+from paper_2303_12374_b200.capture import scalar_env_from_args, ScalarArg
+from paper_2303_12374_b200.stencils.definitions import ARG_LAYOUT, KERNELS, PRECISIONS, definition_for
+from paper_2303_12374_b200.stencils.layout import GridLayout
+
+B200 = DeviceIdent("NVIDIA B200", "Blackwell", {"compute_capability": "10.0"})
+
+
+def scalars(kernel, lay):
+    nb = len(ARG_LAYOUT[kernel]["buffers"])
+    vals = dict(dxi=1.0, dyi=1.0, jj=lay.jj, kk=lay.kk, istart=lay.istart, jstart=lay.jstart, kstart=lay.kstart,
+                iend=lay.iend, jend=lay.jend, kend=lay.kend)
+    out = []
+    for i, n in enumerate(ARG_LAYOUT[kernel]["scalars"]):
+        out.append(ScalarArg(nb + i, "f32" if n in ("dxi", "dyi") else "i32", vals[n]))
+    return out
+
+
+def test_layout_alignment():
+    for prec, align in (("fp32", 32), ("fp64", 16)):
+        lay = GridLayout(1024, 1024, 128, prec)
+        assert lay.jj % align == 0 and (lay.lead + lay.istart) % align == 0
+        assert lay.jj >= lay.icells and lay.kk == lay.jj * lay.jcells
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_default_config_is_the_paper_default(kernel):
+    d = definition_for(kernel, "fp32")
+    cfg, ok = d.space.default_config()
+    assert ok and cfg["block_x"] == 256 and cfg["staging"] == "DIRECT" and cfg["zchunk"] == 1
+    lay = GridLayout(256, 256, 256, "fp32")
+    env = scalar_env_from_args(scalars(kernel, lay))
+    problem = d.derive_problem_size(env)
+    assert problem == (256, 256, 256)
+    geom = d.derive_geometry(cfg, problem, env)
+    assert geom.block == (256, 1, 1) and geom.grid == (256 * 256, 1, 1) and geom.shared_mem_bytes == 0
+
+
+def test_precision_is_in_the_kernel_key():
+    keys = {definition_for(k, p).kernel_key() for k in KERNELS for p in PRECISIONS}
+    assert len(keys) == 4
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+@pytest.mark.parametrize("precision", list(PRECISIONS))
+def test_nvrtc_compiles_sampled_configs(kernel, precision):
+    from paper_2303_12374_b200.cuda._abi import library_path
+    from paper_2303_12374_b200.cuda.compiler import NvrtcCompiler
+
+    if not library_path().exists():
+        pytest.skip("libklb200.so not built")
+    d = definition_for(kernel, precision)
+    lay = GridLayout(40, 24, 16, precision)
+    env = scalar_env_from_args(scalars(kernel, lay))
+    problem = d.derive_problem_size(env)
+    comp = NvrtcCompiler()
+    cfgs = d.space.sample_random(3, 3) + [c for c in d.space.sample_random(4, 300) if c["staging"] == "ZMARCH"][:2]
+    futures = comp.compile_many([d.render_compile_request(c, problem, env) for c in cfgs], B200)
+    for fut in futures:
+        img = fut.result()
+        assert img.lowered_name == f"{kernel}_{precision}" and len(img.cubin) > 1000
