@@ -110,8 +110,8 @@ _ZMARCH_PLANE_LIMIT = {
 }
 #: TMA box extents are <= 256 elements; the smem ring must fit the opt-in limit
 _TMA_LIMIT = {
-    "diff_uvw": ['staging != "TMA" || (block_x + 6) * (block_y * tile_y + 2) * (depth + 2) <= 3072'],
-    "advec_u": ['staging != "TMA" || (block_x + 12) * (block_y * tile_y + 6) * (depth + 4) <= 12288'],
+    "diff_uvw": ['staging != "TMA" || (block_x <= 128 && (block_x + 6) * (block_y * tile_y + 2) * (depth + 2) <= 3072)'],
+    "advec_u": ['staging != "TMA" || (block_x <= 128 && (block_x + 12) * (block_y * tile_y + 6) * (depth + 4) <= 12288)'],
 }
 #: knobs the ZMARCH variant of each kernel fixes (pinned to their defaults)
 _ZMARCH_PINNED = {
