@@ -77,3 +77,24 @@ def test_virtual_ranks_match_single_grid(gpu_ctx, tmp_path, kernel, staging):
             assert err <= 1e-13, (drv.rank, name, err)
         assert drv.wisdom.reports and all(r.configuration == cfg for r in drv.wisdom.reports)
         drv.close()
+
+
+def test_nccl_single_rank_exchange_is_a_noop(gpu_ctx):
+    """The NCCL path end to end on one GPU: unique id, comm init, grouped
+    send/recv call with no neighbours (the only topology one GPU allows)."""
+    from paper_2303_12374_b200.cuda._abi import lib
+    from paper_2303_12374_b200.halo import NcclExchanger
+    from paper_2303_12374_b200.slab import SlabDriver
+
+    import ctypes
+
+    ver = ctypes.c_int()
+    if lib().klb_nccl_version(ctypes.byref(ver)) != 0:
+        pytest.skip("libnccl.so.2 not loadable on this host")
+    ex = NcclExchanger(0, 1, NcclExchanger.unique_id())
+    drv = SlabDriver("diff_uvw", "fp32", (64, 32, 16), gpu_ctx, rank=0, nranks=1, exchanger=ex)
+    drv.step()
+    gpu_ctx.synchronize()
+    drv.close()
+    ex.close()
+    assert ver.value >= 22700
