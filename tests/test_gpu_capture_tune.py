@@ -1,0 +1,61 @@
+"""Capture -> replay -> wisdom -> runtime selection on the GPU.
+
+1. An application launch through WisdomKernel with KERNEL_LAUNCHER_CAPTURE
+   set writes a .klcap holding the PRE-launch device buffers.
+2. ``kltune tune cap.klcap --backend cuda`` replays the captured buffers
+   across configurations (verify + timed reps) and appends the best to the
+   kernel's wisdom file.
+3. A fresh WisdomKernel selects that record (match_kind "exact") and its
+   launch reproduces the oracle.
+"""
+
+import json
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def test_capture_tune_select_round_trip(gpu_ctx, tmp_path, monkeypatch):
+    from paper_2303_12374_b200 import cli
+    from paper_2303_12374_b200.capture import CapturePolicy, read_capture
+    from paper_2303_12374_b200.cuda import NvrtcCompiler
+    from paper_2303_12374_b200.dispatch import WisdomKernel
+    from paper_2303_12374_b200.stencils.layout import GridLayout
+    from paper_2303_12374_b200.stencils.problem import StencilProblem
+    from paper_2303_12374_b200.wisdom import WisdomFile, wisdom_path
+    from stencil_helpers import TOL, oracle_outputs, rel_error
+
+    lay = GridLayout(40, 24, 12, "fp64")
+    prob = StencilProblem("advec_u", lay, gpu_ctx)
+    comp = NvrtcCompiler(gpu_ctx)
+    policy = CapturePolicy(names=frozenset({"advec_u_fp64"}), directory=str(tmp_path))
+    wk = WisdomKernel(prob.definition, comp, wisdom_dir=tmp_path, capture_policy=policy)
+    wk.launch(gpu_ctx.ident, prob.args())
+    gpu_ctx.synchronize()
+    cap_path = tmp_path / "advec_u_fp64_40x24x12.klcap"
+    cap = read_capture(cap_path)
+    assert cap.problem == (40, 24, 12) and len(cap.buffers) == 7
+    # the capture holds the pre-launch ut (the launch has since updated it)
+    ut_cap = np.frombuffer(cap.buffers[0].data, dtype=np.float64)
+    ut_now = prob.fields["ut"].download_array(np.float64)[lay.lead:]
+    assert not np.array_equal(ut_cap[: ut_now.size], ut_now)
+
+    (tmp_path / "klconfig.json").write_text(json.dumps({"backend": "cuda", "repetitions": 3, "warmup": 1}))
+    monkeypatch.chdir(tmp_path)
+    rc = cli.main(["tune", str(cap_path), "--strategy", "random", "--budget-evals", "6", "--seed", "3",
+                   "--wisdom", str(tmp_path)])
+    assert rc == 0
+    wfile = WisdomFile.load(wisdom_path(tmp_path, prob.definition.kernel_key()))
+    rec = wfile.records[0]
+    assert rec.device.name == gpu_ctx.ident.name and rec.problem == (40, 24, 12)
+
+    prob.regenerate()
+    fresh = WisdomKernel(prob.definition, comp, wisdom_dir=tmp_path, capture_policy=CapturePolicy())
+    report = fresh.launch(gpu_ctx.ident, prob.args())
+    gpu_ctx.synchronize()
+    assert report.match_kind == "exact" and report.configuration == rec.config
+    ref, _ = oracle_outputs("advec_u", lay)
+    assert rel_error(prob.download("ut"), ref["ut"], lay) <= TOL["fp64"]
+    prob.close()
