@@ -1,14 +1,16 @@
 // advec_u_tma.cuh — STAGING == TMA variant of advec_u (included by
 // advec_u.cu).  Same flux-form z-march as ZMARCH (advec_u_zmarch.cuh), with
-// the halo'd u planes fetched by the Tensor Memory Accelerator into a
-// shared-memory ring of DEPTH+4 slots (one mbarrier each):
-//   * plane k feeds the x/y stencil of step k, plane k+3 feeds the z-window
-//     (the u[k+3] of every cell comes from the ring instead of a global load);
-//   * one elected thread refills the slot vacated by plane k-1 at the start of
-//     step k, so DEPTH planes beyond the ones being read are in flight;
-//   * v, w and ut of the next plane are prefetched into registers one step
-//     ahead, so their latency overlaps the current plane's compute.
-// Requires BLOCK_X % 32 == 0 (warps along x; west fluxes via __shfl_up_sync).
+// every operand fetched by the Tensor Memory Accelerator into a shared-memory
+// ring of DEPTH+4 slots (one mbarrier each).  Slot p holds plane p of
+//   * u with a 3-cell x/y halo — plane k feeds the x/y stencil of step k and
+//     plane k+3 the z-window (so u[k+3] of every cell comes from the ring);
+//   * v (columns i-1..i, rows j..j+1), w (columns i-1..i) and ut (no halo):
+//     step k reads v and ut of plane k and w of plane k+1;
+// so the compute warps issue no global loads, only the final ut stores.  One
+// elected thread refills the slot vacated by plane k-1 at the start of step
+// k, keeping DEPTH planes beyond the ones being read in flight.  Box starts
+// are rounded down to 16-byte aligned x (TMA requires it).  Requires
+// BLOCK_X % 32 == 0 (warps along x; west fluxes via __shfl_up_sync).
 
 #if BLOCK_Z != 1 || TILE_Z != 1 || TILE_X != 1
 #error "advec_u TMA requires BLOCK_Z == TILE_Z == TILE_X == 1"
@@ -24,22 +26,30 @@
 
 namespace {
 constexpr int kS = static_cast<int>(sizeof(real));
+constexpr int kE = 16 / kS;
 constexpr int kTYT = BLOCK_Y * TILE_Y;
-// Box width: BLOCK_X + 6 halo columns from a 16-byte aligned x start (TMA
-// requires it), rounded to a 16-byte multiple.
-constexpr int kBW = (((BLOCK_X + 6) * kS + 16 - kS + 15) / 16) * 16 / kS;
+constexpr int kBW = (((BLOCK_X + 6) * kS + 16 - kS + 15) / 16) * 16 / kS;  // u: 3-halo + alignment slack
 constexpr int kBH = kTYT + 6;
-constexpr int kPB = ((kBW * kBH * kS + 127) / 128) * 128;  // bytes per plane slot
+constexpr int kVW = (((BLOCK_X + 1) * kS + 16 - kS + 15) / 16) * 16 / kS;  // v, w: column i-1 + slack
+constexpr int kTW = ((BLOCK_X * kS + 16 - kS + 15) / 16) * 16 / kS;        // ut: no halo
+constexpr int kUB = ((kBW * kBH * kS + 127) / 128) * 128;
+constexpr int kVB = ((kVW * (kTYT + 1) * kS + 127) / 128) * 128;
+constexpr int kWB = ((kVW * kTYT * kS + 127) / 128) * 128;
+constexpr int kTB = ((kTW * kTYT * kS + 127) / 128) * 128;
+constexpr int kPB = kUB + kVB + kWB + kTB;  // bytes per plane slot
 constexpr int kPS = kPB / kS;
+constexpr int kVO = kUB / kS, kWO = (kUB + kVB) / kS, kTO = (kUB + kVB + kWB) / kS;  // field offsets in a slot
 constexpr int kNS = DEPTH + 4;
-constexpr unsigned kTxBytes = static_cast<unsigned>(kBW * kBH * kS);
+constexpr unsigned kTxBytes =
+    static_cast<unsigned>((kBW * kBH + kVW * (kTYT + 1) + kVW * kTYT + kTW * kTYT) * kS);
 static_assert(kBW <= 256 && kBH <= 256, "TMA box extents are limited to 256");
 }  // namespace
 
-// position of u = 1, jj = 9, kk = 10 (definitions.ARG_LAYOUT["advec_u"])
-extern "C" __device__ const int kl_tma_spec[1 + 5] = {1, 1, 9, 10, kBW, kBH};
+// positions: ut=0 u=1 v=2 w=3, jj=9 kk=10 (definitions.ARG_LAYOUT["advec_u"])
+extern "C" __device__ const int kl_tma_spec[1 + 5 * 4] = {4, 1, 9, 10, kBW, kBH, 2, 9, 10, kVW, kTYT + 1,
+                                                          3, 9, 10, kVW, kTYT, 0, 9, 10, kTW, kTYT};
 struct __align__(64) KlTmaParams {
-  TmaDesc map[1];
+  TmaDesc map[4];
 };
 
 extern "C" __global__ void __launch_bounds__(KL_THREADS, MIN_BLOCKS)
@@ -68,19 +78,24 @@ KL_ENTRY(real* __restrict__ ut, const real* __restrict__ u, const real* __restri
   const int kmax = k1 + 2;  // last plane the z-window reads
   const int tid = threadIdx.x + threadIdx.y * BLOCK_X;
   const int lane = threadIdx.x & 31;
-  const int xfirst = i0 - 3 + kl::tma_xoff(u);  // tensor x of column i0-3
-  const int x0 = xfirst & ~(16 / kS - 1);       // 16-byte aligned box start
-  const int cshift = xfirst - x0;
+  const int xu = i0 - 3 + kl::tma_xoff(u);  // tensor x of column i0-3
+  const int xu0 = xu & ~(kE - 1);            // 16-byte aligned box starts
+  const int xv0 = (xu + 2) & ~(kE - 1);      // column i0-1
+  const int xt0 = (xu + 3) & ~(kE - 1);      // column i0
+  const int ushift = xu - xu0, vshift = xu + 2 - xv0, tshift = xu + 3 - xt0;
   const real dxi60 = dxi * real(1.0 / 60.0);
   const real dyi60 = dyi * real(1.0 / 60.0);
   constexpr long long K1 = KL_KK;
-  constexpr long long J1 = KL_JJ;
 
   auto slot = [&](int p) { return (p - k0) % kNS; };
   auto issue = [&](int p) {
     unsigned long long* bar = full + slot(p);
+    real* dst = ring + slot(p) * kPS;
     kl::mbar_expect_tx(bar, kTxBytes);
-    kl::tma_load_3d(ring + slot(p) * kPS, maps, bar, x0, j0 - 3, p);
+    kl::tma_load_3d(dst, maps + 0, bar, xu0, j0 - 3, p);
+    kl::tma_load_3d(dst + kVO, maps + 1, bar, xv0, j0, p);
+    kl::tma_load_3d(dst + kWO, maps + 2, bar, xv0, j0, p);
+    kl::tma_load_3d(dst + kTO, maps + 3, bar, xt0, j0, p);
   };
   auto wait = [&](int p) { kl::mbar_wait(full + slot(p), ((p - k0) / kNS) & 1); };
 
@@ -96,30 +111,28 @@ KL_ENTRY(real* __restrict__ ut, const real* __restrict__ u, const real* __restri
   const int i = min(i0 + static_cast<int>(threadIdx.x), iend - 1);
   const bool col_ok = i0 + static_cast<int>(threadIdx.x) < iend;
   const int lj0 = threadIdx.y * TILE_Y;
-  const int colofs = (lj0 + 3) * kBW + threadIdx.x + 3 + cshift;  // (i, j0+lj0) inside a plane slot
-  long long base[TILE_Y];
+  const int colofs = (lj0 + 3) * kBW + threadIdx.x + 3 + ushift;  // (i, j0+lj0) in the u box
+  const int vofs = lj0 * kVW + threadIdx.x + vshift;             // (i-1, j0+lj0) in the v / w boxes
+  const int tofs = lj0 * kTW + threadIdx.x + tshift;             // (i, j0+lj0) in the ut box
   real uq[TILE_Y][7];
   real fz_bot[TILE_Y];
-  // next-plane operands (prefetched one step ahead)
-  real nv_n0[TILE_Y], nv_n1[TILE_Y], nw_t0[TILE_Y], nw_t1[TILE_Y], nut[TILE_Y];
-  real nv_s0, nv_s1;
-  const real rh0 = rhorefh[k0];
+  wait(k0);
+  {
+    const real* ring0 = ring + slot(k0) * kPS;
+    const real rh0 = rhorefh[k0];
 #pragma unroll
-  for (int t = 0; t < TILE_Y; ++t) {
-    const int j = min(j0 + lj0 + t, jend - 1);
-    base[t] = i + static_cast<long long>(j) * KL_JJ + static_cast<long long>(k0) * KL_KK;
+    for (int t = 0; t < TILE_Y; ++t) {
+      const int j = min(j0 + lj0 + t, jend - 1);
+      const long long b = i + static_cast<long long>(j) * KL_JJ + static_cast<long long>(k0) * KL_KK;
 #pragma unroll
-    for (int m = 0; m < 6; ++m) uq[t][m] = u[base[t] + (m - 3) * K1];
-    const real wb = kl::interp2(w[base[t] - 1], w[base[t]]);
-    fz_bot[t] = rh0 * kl::flux5x60(wb, uq[t][0], uq[t][1], uq[t][2], uq[t][3], uq[t][4], uq[t][5]);
-    nv_n0[t] = v[base[t] - 1 + J1];
-    nv_n1[t] = v[base[t] + J1];
-    nw_t0[t] = w[base[t] - 1 + K1];
-    nw_t1[t] = w[base[t] + K1];
-    nut[t] = col_ok ? ut[base[t]] : real(0);
+      for (int m = 0; m < 3; ++m) uq[t][m] = u[b + (m - 3) * K1];  // planes below the chunk: not staged
+#pragma unroll
+      for (int m = 3; m < 6; ++m) uq[t][m] = u[b + (m - 3) * K1];
+      const real* wp = ring0 + kWO + vofs + t * kVW;
+      const real wb = kl::interp2(wp[0], wp[1]);
+      fz_bot[t] = rh0 * kl::flux5x60(wb, uq[t][0], uq[t][1], uq[t][2], uq[t][3], uq[t][4], uq[t][5]);
+    }
   }
-  nv_s0 = v[base[0] - 1];
-  nv_s1 = v[base[0]];
 
   for (int k = k0; k < k1; ++k) {
     __syncthreads();  // plane k-1's slot is free
@@ -130,42 +143,22 @@ KL_ENTRY(real* __restrict__ ut, const real* __restrict__ u, const real* __restri
         issue(p);
       }
     }
-    const long long kofs = static_cast<long long>(k - k0) * K1;
-    // this plane's operands, then prefetch the next plane's
-    real cv_n0[TILE_Y], cv_n1[TILE_Y], cw_t0[TILE_Y], cw_t1[TILE_Y], cut[TILE_Y];
-    const real cv_s0 = nv_s0, cv_s1 = nv_s1;
-#pragma unroll
-    for (int t = 0; t < TILE_Y; ++t) {
-      cv_n0[t] = nv_n0[t];
-      cv_n1[t] = nv_n1[t];
-      cw_t0[t] = nw_t0[t];
-      cw_t1[t] = nw_t1[t];
-      cut[t] = nut[t];
-    }
-    if (k + 1 < k1) {
-#pragma unroll
-      for (int t = 0; t < TILE_Y; ++t) {
-        const long long b = base[t] + kofs + K1;
-        nv_n0[t] = v[b - 1 + J1];
-        nv_n1[t] = v[b + J1];
-        nw_t0[t] = w[b - 1 + K1];
-        nw_t1[t] = w[b + K1];
-        nut[t] = col_ok ? ut[b] : real(0);
-      }
-      nv_s0 = v[base[0] + kofs + K1 - 1];
-      nv_s1 = v[base[0] + kofs + K1];
-    }
     if (k < k0 + 3) wait(k);
     wait(k + 3);
-    const real* xy = ring + slot(k) * kPS + colofs;    // plane k at (i, j0+lj0)
-    const real* zf = ring + slot(k + 3) * kPS + colofs;  // plane k+3
+    const real* sk = ring + slot(k) * kPS;
+    const real* xy = sk + colofs;                          // u, plane k at (i, j0+lj0)
+    const real* zf = ring + slot(k + 3) * kPS + colofs;    // u, plane k+3
+    const real* vp = sk + kVO + vofs;                      // v, plane k at (i-1, j0+lj0)
+    const real* wp = ring + slot(k + 1) * kPS + kWO + vofs;  // w, plane k+1 at (i-1, j0+lj0)
+    const real* tp = sk + kTO + tofs;                      // ut, plane k
     const real rh_top = rhorefh[k + 1];
     const real zfac60 = dzi[k] / (rhoref[k] * real(60));
+    const long long kofs = static_cast<long long>(k) * K1;
 
     real ucol[TILE_Y + 6];
 #pragma unroll
     for (int m = 0; m < TILE_Y + 6; ++m) ucol[m] = xy[(m - 3) * kBW];
-    real fy_lo = kl::flux5x60(kl::interp2(cv_s0, cv_s1), ucol[0], ucol[1], ucol[2], ucol[3], ucol[4], ucol[5]);
+    real fy_lo = kl::flux5x60(kl::interp2(vp[0], vp[1]), ucol[0], ucol[1], ucol[2], ucol[3], ucol[4], ucol[5]);
 
 #pragma unroll
     for (int t = 0; t < TILE_Y; ++t) {
@@ -176,12 +169,16 @@ KL_ENTRY(real* __restrict__ ut, const real* __restrict__ u, const real* __restri
       const real fx_e = kl::flux5x60(kl::interp2(x0v, xp1), xm2, xm1, x0v, xp1, xp2, xp3);
       real fx_w = __shfl_up_sync(0xffffffffu, fx_e, 1);
       if (lane == 0) fx_w = kl::flux5x60(kl::interp2(xm1, x0v), row[-3], xm2, xm1, x0v, xp1, xp2);
-      const real fy_hi = kl::flux5x60(kl::interp2(cv_n0[t], cv_n1[t]), ucol[t + 1], ucol[t + 2], ucol[t + 3],
+      const real* vn = vp + (t + 1) * kVW;
+      const real fy_hi = kl::flux5x60(kl::interp2(vn[0], vn[1]), ucol[t + 1], ucol[t + 2], ucol[t + 3],
                                       ucol[t + 4], ucol[t + 5], ucol[t + 6]);
-      const real fz_top = rh_top * kl::flux5x60(kl::interp2(cw_t0[t], cw_t1[t]), q[1], q[2], q[3], q[4], q[5], q[6]);
+      const real* wt_ = wp + t * kVW;
+      const real fz_top = rh_top * kl::flux5x60(kl::interp2(wt_[0], wt_[1]), q[1], q[2], q[3], q[4], q[5], q[6]);
       const int j = j0 + lj0 + t;
-      if (col_ok && j < jend)
-        ut[base[t] + kofs] = cut[t] - ((fx_e - fx_w) * dxi60 + (fy_hi - fy_lo) * dyi60 + (fz_top - fz_bot[t]) * zfac60);
+      if (col_ok && j < jend) {
+        const long long ijk = i + static_cast<long long>(j) * KL_JJ + kofs;
+        ut[ijk] = tp[t * kTW] - ((fx_e - fx_w) * dxi60 + (fy_hi - fy_lo) * dyi60 + (fz_top - fz_bot[t]) * zfac60);
+      }
       fy_lo = fy_hi;
       fz_bot[t] = fz_top;
 #pragma unroll

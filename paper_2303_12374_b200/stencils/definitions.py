@@ -110,8 +110,8 @@ _ZMARCH_PLANE_LIMIT = {
 }
 #: TMA box extents are <= 256 elements; the smem ring must fit the opt-in limit
 _TMA_LIMIT = {
-    "diff_uvw": ['staging != "TMA" || (block_x <= 128 && (block_x + 6) * (block_y * tile_y + 2) * (depth + 2) <= 3072)'],
-    "advec_u": ['staging != "TMA" || (block_x <= 128 && (block_x + 12) * (block_y * tile_y + 6) * (depth + 4) <= 12288)'],
+    "diff_uvw": ['staging != "TMA" || (block_x <= 128 && (block_x + 6) * (block_y * tile_y + 2) * (depth + 2) <= 2048)'],
+    "advec_u": ['staging != "TMA" || (block_x <= 128 && (block_x + 12) * (block_y * tile_y + 6) * (depth + 4) <= 8192)'],
 }
 #: knobs the ZMARCH variant of each kernel fixes (pinned to their defaults)
 _ZMARCH_PINNED = {
@@ -182,15 +182,20 @@ _SMEM = {
 
 
 # TMA ring: 128 B alignment slack + 128 B of mbarriers + ring slots of 128-B
-# aligned field-planes (diff_uvw: depth+2 slots x 4 fields; advec_u: depth+4
-# slots of u, since plane k+3 feeds the z-window); box width = block_x + halo
+# aligned field-planes (diff_uvw: depth+2 slots x (4 halo'd + 3 tendency)
+# fields; advec_u: depth+4 slots of u (3-halo) + v, w, ut, since plane k+3
+# feeds the z-window); box width = block_x + halo
 # plus up to one 16-byte chunk of alignment slack, rounded to 16 B.
 _BW = "(ceil_div((block_x + {H}) * {S} + 16 - {S}, 16) * 16 / {S})"
 _SMEM_TMA = {
-    "diff_uvw": "(256 + (depth + 2) * 4 * ceil_div(" + _BW.format(H=2, S="{S}") +
-                " * (block_y * tile_y + 2) * {S}, 128) * 128)",
-    "advec_u": "(256 + (depth + 4) * ceil_div(" + _BW.format(H=6, S="{S}") +
-               " * (block_y * tile_y + 6) * {S}, 128) * 128)",
+    "diff_uvw": "(256 + (depth + 2) * (4 * ceil_div(" + _BW.format(H=2, S="{S}") +
+                " * (block_y * tile_y + 2) * {S}, 128) * 128 + 3 * ceil_div(" + _BW.format(H=0, S="{S}") +
+                " * (block_y * tile_y) * {S}, 128) * 128))",
+    "advec_u": "(256 + (depth + 4) * (ceil_div(" + _BW.format(H=6, S="{S}") +
+               " * (block_y * tile_y + 6) * {S}, 128) * 128 + ceil_div(" + _BW.format(H=1, S="{S}") +
+               " * (block_y * tile_y + 1) * {S}, 128) * 128 + ceil_div(" + _BW.format(H=1, S="{S}") +
+               " * (block_y * tile_y) * {S}, 128) * 128 + ceil_div(" + _BW.format(H=0, S="{S}") +
+               " * (block_y * tile_y) * {S}, 128) * 128))",
 }
 
 

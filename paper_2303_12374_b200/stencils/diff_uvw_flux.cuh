@@ -10,9 +10,13 @@
 
 namespace {
 
+// Quantities on the z-face k+1/2 carried to the next plane.  The south y-face
+// flux of w at row t is the north one of row t-1, so only the strip's
+// lowest (fyw_lo) is stored separately.
 struct DiffCarry {
   real fzu[TILE_Y], fzv[TILE_Y], gz[TILE_Y];
-  real fxw_p[TILE_Y], fxw_m[TILE_Y], fyw_p[TILE_Y], fyw_m[TILE_Y];
+  real fxw_p[TILE_Y], fxw_m[TILE_Y], fyw_p[TILE_Y];
+  real fyw_lo;
 };
 
 // One plane step.  p0/p1 point at (strip row -1, this column) of planes k and
@@ -36,11 +40,10 @@ __device__ __forceinline__ real from_west(real east, F&& own) {
 #endif
 }
 
-template <bool OUT, int SW>
+template <bool OUT, int SW, class Store>
 __device__ __forceinline__ void diff_step(const real* __restrict__ p0, const real* __restrict__ p1, int fs,
                                           DiffCarry& c, real dxi, real dyi, real c2x, real c2y, real rh1,
-                                          real dzhi1, real rdz, real fac_uv, real fac_w, real* dut, real* dvt,
-                                          real* dwt) {
+                                          real dzhi1, real rdz, real fac_uv, real fac_w, Store&& store) {
   const real q = real(0.25);
   // field accessors on the planes: f = 0 evisc, 1 u, 2 v, 3 w; row offset r (0 = strip row -1), column di
 #define P0(f, r, di) p0[(f) * fs + (r) * SW + (di)]
@@ -53,6 +56,7 @@ __device__ __forceinline__ void diff_step(const real* __restrict__ p0, const rea
   // upper-y quantities of the previous row (row -1 computes them first)
   real exy_i = 0, exy_i1 = 0, fyu = 0, gy = 0, eyz = 0, fyw = 0;
   real u_lo0 = 0, u_lop = 0, w1_lo = 0;
+  real fyw_prev = 0;
 
 #pragma unroll
   for (int t = -1; t < TILE_Y; ++t) {
@@ -88,17 +92,19 @@ __device__ __forceinline__ void diff_step(const real* __restrict__ p0, const rea
         const real fxv_p = exy_i1 * ((v_p - v_0) * dxi + (u_p - u_lop) * dyi);
         const real fxv_m =
             from_west(fxv_p, [&] { return exy_i * ((v_0 - P0(2, r, -1)) * dxi + (u_0 - u_lo0) * dyi); });
-        dut[t] = c2x * (gx_i - gx_im) + (fyu_up - fyu) * dyi + (fzu - c.fzu[t]) * fac_uv;
-        dvt[t] = (fxv_p - fxv_m) * dxi + c2y * (gy_up - gy) + (fzv - c.fzv[t]) * fac_uv;
-        dwt[t] = (c.fxw_p[t] - c.fxw_m[t]) * dxi + (c.fyw_p[t] - c.fyw_m[t]) * dyi + (gz - c.gz[t]) * fac_w;
+        const real fyw_s = t == 0 ? c.fyw_lo : fyw_prev;  // previous plane's south face of this row
+        store(t, c2x * (gx_i - gx_im) + (fyu_up - fyu) * dyi + (fzu - c.fzu[t]) * fac_uv,
+              (fxv_p - fxv_m) * dxi + c2y * (gy_up - gy) + (fzv - c.fzv[t]) * fac_uv,
+              (c.fxw_p[t] - c.fxw_m[t]) * dxi + (c.fyw_p[t] - fyw_s) * dyi + (gz - c.gz[t]) * fac_w);
       }
       c.fzu[t] = fzu;
       c.fzv[t] = fzv;
       c.gz[t] = gz;
-      c.fxw_p[t] = fxw_p;
       c.fxw_m[t] = fxw_m;
+      if (t == 0) c.fyw_lo = fyw;
+      fyw_prev = c.fyw_p[t];  // previous plane's north face of row t = south face of row t+1
       c.fyw_p[t] = fyw_up;
-      c.fyw_m[t] = fyw;
+      c.fxw_p[t] = fxw_p;
     }
 
     // slide the strip: row j+1 becomes row j

@@ -1,14 +1,17 @@
 // diff_uvw_tma.cuh — STAGING == TMA variant of diff_uvw (included by
 // diff_uvw.cu).  Same flux-form plane step as ZMARCH (diff_uvw_flux.cuh), but
-// the halo'd planes of evisc, u, v and w are fetched by the Tensor Memory
-// Accelerator: one elected thread issues cp.async.bulk.tensor.3d copies DEPTH
-// planes ahead of the compute into a (DEPTH+2)-slot shared-memory ring, each
-// slot completing on its own mbarrier (expect_tx bytes).  Staging costs no
-// registers and no load instructions in the compute warps, and DEPTH planes x
-// 4 fields of each block are in flight — the memory-level parallelism the
-// register-prefetch ZMARCH variant lacks (ncu: long_scoreboard-bound at 25%
-// occupancy).  Out-of-box rows/columns are zero-filled by the TMA unit (they
-// only feed cells outside the grid, which are never stored).
+// every operand is fetched by the Tensor Memory Accelerator: one elected
+// thread issues cp.async.bulk.tensor.3d copies DEPTH planes ahead of the
+// compute into a (DEPTH+2)-slot shared-memory ring, each slot completing on
+// its own mbarrier (expect_tx bytes).  A slot holds plane p of
+//   * evisc, u, v, w with a 1-cell x/y halo (the stencil reads planes k, k+1),
+//   * ut, vt, wt without halo (the read half of the read-modify-write),
+// so the compute warps issue no global loads at all — only the final
+// stores of the updated tendencies.  Staging costs no registers, and DEPTH
+// planes x 7 fields of every block are in flight (ncu on the register-staged
+// ZMARCH variant: long_scoreboard-bound at 25% occupancy).  Box starts are
+// rounded down to 16-byte aligned x (TMA faults otherwise); out-of-box
+// rows/columns are zero-filled and only feed cells that are never stored.
 
 #if BLOCK_Z != 1 || TILE_Z != 1 || TILE_X != 1
 #error "diff_uvw TMA requires BLOCK_Z == TILE_Z == TILE_X == 1"
@@ -22,25 +25,29 @@
 
 namespace {
 constexpr int kS = static_cast<int>(sizeof(real));
+constexpr int kE = 16 / kS;  // elements per 16 bytes
 constexpr int kTYT = BLOCK_Y * TILE_Y;
-// Box width: BLOCK_X + 2 halo columns, started at a 16-byte aligned x (TMA
-// faults on an unaligned innermost box start) -> up to 16/kS - 1 extra
-// columns on the left, total rounded to a 16-byte multiple.
+// halo'd box: BLOCK_X + 2 columns plus up to kE-1 alignment columns, 16-B multiple
 constexpr int kBW = (((BLOCK_X + 2) * kS + 16 - kS + 15) / 16) * 16 / kS;
 constexpr int kBH = kTYT + 2;
-constexpr int kFSB = ((kBW * kBH * kS + 127) / 128) * 128;  // bytes per field-plane (128-B aligned)
+// tendency box: BLOCK_X columns (+ alignment slack), no halo
+constexpr int kTW = ((BLOCK_X * kS + 16 - kS + 15) / 16) * 16 / kS;
+constexpr int kFSB = ((kBW * kBH * kS + 127) / 128) * 128;   // bytes per halo'd field-plane
+constexpr int kTSB = ((kTW * kTYT * kS + 127) / 128) * 128;  // bytes per tendency field-plane
 constexpr int kFS = kFSB / kS;
-constexpr int kSlot = 4 * kFS;
+constexpr int kTS = kTSB / kS;
+constexpr int kSlot = 4 * kFS + 3 * kTS;
 constexpr int kNS = DEPTH + 2;
-constexpr unsigned kTxBytes = 4u * kBW * kBH * kS;
-static_assert(kBW <= 256 && kBH <= 256, "TMA box extents are limited to 256");
+constexpr unsigned kTxBytes = 4u * kBW * kBH * kS + 3u * kTW * kTYT * kS;
+static_assert(kBW <= 256 && kBH <= 256 && kTW <= 256, "TMA box extents are limited to 256");
 }  // namespace
 
-// positions: evisc=3 u=4 v=5 w=6, jj=13 kk=14 (definitions.ARG_LAYOUT["diff_uvw"])
-extern "C" __device__ const int kl_tma_spec[1 + 5 * 4] = {4, 3, 13, 14, kBW, kBH, 4, 13, 14, kBW, kBH,
-                                                          5, 13, 14, kBW, kBH, 6, 13, 14, kBW, kBH};
+// positions: ut=0 vt=1 wt=2 evisc=3 u=4 v=5 w=6, jj=13 kk=14 (definitions.ARG_LAYOUT["diff_uvw"])
+extern "C" __device__ const int kl_tma_spec[1 + 5 * 7] = {
+    7, 3, 13, 14, kBW, kBH, 4, 13, 14, kBW, kBH, 5, 13, 14, kBW, kBH, 6, 13, 14, kBW, kBH,
+    0, 13, 14, kTW, kTYT, 1, 13, 14, kTW, kTYT, 2, 13, 14, kTW, kTYT};
 struct __align__(64) KlTmaParams {
-  TmaDesc map[4];
+  TmaDesc map[7];
 };
 
 extern "C" __global__ void __launch_bounds__(KL_THREADS, MIN_BLOCKS)
@@ -68,8 +75,10 @@ KL_ENTRY(real* __restrict__ ut, real* __restrict__ vt, real* __restrict__ wt, co
   const int k1 = min(k0 + ZCHUNK, kend);
   const int tid = threadIdx.x + threadIdx.y * BLOCK_X;
   const int xfirst = i0 - 1 + kl::tma_xoff(evisc);  // tensor x of column i0-1 (all fields share the layout)
-  const int x0 = xfirst & ~(16 / kS - 1);          // 16-byte aligned box start
+  const int x0 = xfirst & ~(kE - 1);               // 16-byte aligned box start
   const int cshift = xfirst - x0;                  // extra leading columns in the tile
+  const int xt0 = (xfirst + 1) & ~(kE - 1);        // tendency box start (column i0)
+  const int tshift = xfirst + 1 - xt0;
   const int kfirst = k0 - 1;                     // first staged plane
 
   // plane p lives in slot (p - kfirst) % kNS; its mbarrier phase is ((p - kfirst) / kNS) & 1
@@ -80,6 +89,8 @@ KL_ENTRY(real* __restrict__ ut, real* __restrict__ vt, real* __restrict__ wt, co
     kl::mbar_expect_tx(bar, kTxBytes);
 #pragma unroll
     for (int f = 0; f < 4; ++f) kl::tma_load_3d(dst + f * kFS, maps + f, bar, x0, j0 - 1, p);
+#pragma unroll
+    for (int f = 0; f < 3; ++f) kl::tma_load_3d(dst + 4 * kFS + f * kTS, maps + 4 + f, bar, xt0, j0, p);
   };
   auto wait = [&](int p) {
     const int rel = p - kfirst;
@@ -102,13 +113,14 @@ KL_ENTRY(real* __restrict__ ut, real* __restrict__ vt, real* __restrict__ wt, co
   const int off = lj0 * kBW + threadIdx.x + 1 + cshift;  // (strip row -1, this column) inside a field-plane
   const int i = i0 + threadIdx.x;
   DiffCarry carry;
-  real dut[TILE_Y], dvt[TILE_Y], dwt[TILE_Y];
+  auto no_store = [](int, real, real, real) {};
 
   wait(kfirst);
   wait(kfirst + 1);
   diff_step<false, kBW>(plane(kfirst) + off, plane(kfirst + 1) + off, kFS, carry, dxi, dyi, c2x, c2y,
-                        rhorefh[k0], dzhi[k0], rhoref[kfirst] * dzi[kfirst], real(0), real(0), dut, dvt, dwt);
+                        rhorefh[k0], dzhi[k0], rhoref[kfirst] * dzi[kfirst], real(0), real(0), no_store);
 
+  const int toff = lj0 * kTW + threadIdx.x + tshift;  // (strip row 0, this column) in a tendency plane
   for (int k = k0; k < k1; ++k) {
     __syncthreads();  // everyone is done with plane k-1's slot
     if (tid == 0) {
@@ -118,32 +130,21 @@ KL_ENTRY(real* __restrict__ ut, real* __restrict__ vt, real* __restrict__ wt, co
         issue(p);
       }
     }
-    // RMW operands of this plane: issue the loads before waiting on the staged plane
-    real ot[TILE_Y], ov[TILE_Y], ow[TILE_Y];
-    const bool col_ok = i < iend;
-#pragma unroll
-    for (int t = 0; t < TILE_Y; ++t) {
-      const int j = j0 + lj0 + t;
-      const long long ijk = i + static_cast<long long>(j) * KL_JJ + static_cast<long long>(k) * KL_KK;
-      const bool ok = col_ok && j < jend;
-      ot[t] = ok ? ut[ijk] : real(0);
-      ov[t] = ok ? vt[ijk] : real(0);
-      ow[t] = ok ? wt[ijk] : real(0);
-    }
     wait(k + 1);
     const real fac_uv = dzi[k] / rhoref[k];
     const real fac_w = real(2) * dzhi[k] / rhorefh[k];
-    diff_step<true, kBW>(plane(k) + off, plane(k + 1) + off, kFS, carry, dxi, dyi, c2x, c2y, rhorefh[k + 1],
-                         dzhi[k + 1], rhoref[k] * dzi[k], fac_uv, fac_w, dut, dvt, dwt);
-#pragma unroll
-    for (int t = 0; t < TILE_Y; ++t) {
+    const real* tend = plane(k) + 4 * kFS + toff;
+    const long long kofs = static_cast<long long>(k) * KL_KK;
+    auto store = [&](int t, real dut, real dvt, real dwt) {
       const int j = j0 + lj0 + t;
-      if (col_ok && j < jend) {
-        const long long ijk = i + static_cast<long long>(j) * KL_JJ + static_cast<long long>(k) * KL_KK;
-        ut[ijk] = ot[t] + dut[t];
-        vt[ijk] = ov[t] + dvt[t];
-        wt[ijk] = ow[t] + dwt[t];
+      if (i < iend && j < jend) {
+        const long long ijk = i + static_cast<long long>(j) * KL_JJ + kofs;
+        ut[ijk] = tend[t * kTW] + dut;
+        vt[ijk] = tend[kTS + t * kTW] + dvt;
+        wt[ijk] = tend[2 * kTS + t * kTW] + dwt;
       }
-    }
+    };
+    diff_step<true, kBW>(plane(k) + off, plane(k + 1) + off, kFS, carry, dxi, dyi, c2x, c2y, rhorefh[k + 1],
+                         dzhi[k + 1], rhoref[k] * dzi[k], fac_uv, fac_w, store);
   }
 }

@@ -92,7 +92,7 @@ KL_ENTRY(real* __restrict__ ut, real* __restrict__ vt, real* __restrict__ wt, co
   const int col = threadIdx.x + 1;
   const int i = i0 + threadIdx.x;
   DiffCarry carry;
-  real dut[TILE_Y], dvt[TILE_Y], dwt[TILE_Y];
+  auto no_store = [](int, real, real, real) {};
 
   {
     real buf[KL_FILL][4];
@@ -106,8 +106,8 @@ KL_ENTRY(real* __restrict__ ut, real* __restrict__ vt, real* __restrict__ wt, co
     const int kp = k0 - 1;
     const real* p0 = ring + (kp % 3) * SLOT + lj0 * KL_SW + col;
     const real* p1 = ring + ((kp + 1) % 3) * SLOT + lj0 * KL_SW + col;
-    diff_step<false, KL_SW>(p0, p1, FS, carry, dxi, dyi, c2x, c2y, rhorefh[kp + 1], dzhi[kp + 1], rhoref[kp] * dzi[kp],
-                     real(0), real(0), dut, dvt, dwt);
+    diff_step<false, KL_SW>(p0, p1, FS, carry, dxi, dyi, c2x, c2y, rhorefh[kp + 1], dzhi[kp + 1],
+                            rhoref[kp] * dzi[kp], real(0), real(0), no_store);
   }
   {
     real buf[KL_FILL][4];
@@ -124,20 +124,18 @@ KL_ENTRY(real* __restrict__ ut, real* __restrict__ vt, real* __restrict__ wt, co
     const real* p1 = ring + ((k + 1) % 3) * SLOT + lj0 * KL_SW + col;
     const real fac_uv = dzi[k] / rhoref[k];
     const real fac_w = real(2) * dzhi[k] / rhorefh[k];
-    diff_step<true, KL_SW>(p0, p1, FS, carry, dxi, dyi, c2x, c2y, rhorefh[k + 1], dzhi[k + 1], rhoref[k] * dzi[k],
-                    fac_uv, fac_w, dut, dvt, dwt);
-    if (i < iend) {
-#pragma unroll
-      for (int t = 0; t < TILE_Y; ++t) {
-        const int j = j0 + lj0 + t;
-        if (j < jend) {
-          const long long ijk = i + static_cast<long long>(j) * KL_JJ + static_cast<long long>(k) * KL_KK;
-          ut[ijk] += dut[t];
-          vt[ijk] += dvt[t];
-          wt[ijk] += dwt[t];
-        }
+    const long long kofs = static_cast<long long>(k) * KL_KK;
+    auto store = [&](int t, real dut, real dvt, real dwt) {
+      const int j = j0 + lj0 + t;
+      if (i < iend && j < jend) {
+        const long long ijk = i + static_cast<long long>(j) * KL_JJ + kofs;
+        ut[ijk] += dut;
+        vt[ijk] += dvt;
+        wt[ijk] += dwt;
       }
-    }
+    };
+    diff_step<true, KL_SW>(p0, p1, FS, carry, dxi, dyi, c2x, c2y, rhorefh[k + 1], dzhi[k + 1], rhoref[k] * dzi[k],
+                           fac_uv, fac_w, store);
     if (more) store_plane(k + 2, buf);
   }
 }

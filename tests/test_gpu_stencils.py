@@ -96,3 +96,22 @@ def test_k_subrange_launch(gpu_ctx, compiler, kernel):
         for name in ref:
             diff = np.max(np.abs(got[name].astype(np.float64) - ref[name]))
             assert diff <= 1e-12 * np.max(np.abs(ref[name])), (cfg["staging"], name, diff)
+
+
+@pytest.mark.parametrize("precision", ["fp32", "fp64"])
+def test_tma_configs_rejected_by_an_earlier_tuner_run(gpu_ctx, compiler, precision):
+    """Regression: advec_u TMA configurations the replay verifier once flagged."""
+    from paper_2303_12374_b200.stencils.layout import GridLayout
+
+    base = _default("advec_u", precision)
+    cases = [dict(block_x=32, block_y=1, tile_y=1, depth=1, zchunk=8, min_blocks=2),
+             dict(block_x=32, block_y=4, tile_y=1, depth=3, zchunk=64, min_blocks=2),
+             dict(block_x=64, block_y=2, tile_y=1, depth=3, zchunk=8, min_blocks=3),
+             dict(block_x=32, block_y=2, tile_y=2, depth=2, zchunk=32, min_blocks=5)]
+    lay = GridLayout(96, 40, 70, precision)
+    ref, _ = oracle_outputs("advec_u", lay)
+    for case in cases:
+        cfg = dict(base, staging="TMA", **case)
+        got = run_config(gpu_ctx, compiler, "advec_u", lay, cfg)
+        err = rel_error(got["ut"], ref["ut"], lay)
+        assert err <= TOL[precision], (case, err)

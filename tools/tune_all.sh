@@ -1,6 +1,6 @@
 # Tune every problem size the benchmark and the BASELINE configs use; writes wisdom + sessions.
 set -x
-OUT=gpurun_out/tune
+OUT=${OUT:-gpurun_out/tune}
 mkdir -p $OUT
 tune() {  # kernel precision grid evals_direct evals_zmarch evals_tma
   for fam in DIRECT:$4 ZMARCH:$5 TMA:$6; do
