@@ -116,7 +116,12 @@ KL_ENTRY(real* __restrict__ ut, const real* __restrict__ u, const real* __restri
   const int tofs = lj0 * kTW + threadIdx.x + tshift;             // (i, j0+lj0) in the ut box
   real uq[TILE_Y][7];
   real fz_bot[TILE_Y];
+  // planes k0..k0+2 are first read as the x/y plane (k) or the w plane (k+1)
+  // of the first steps; every later plane is first read as the z-window
+  // plane (k+3) and waited for there
   wait(k0);
+  wait(k0 + 1);
+  wait(k0 + 2);
   {
     const real* ring0 = ring + slot(k0) * kPS;
     const real rh0 = rhorefh[k0];
@@ -143,7 +148,6 @@ KL_ENTRY(real* __restrict__ ut, const real* __restrict__ u, const real* __restri
         issue(p);
       }
     }
-    if (k < k0 + 3) wait(k);
     wait(k + 3);
     const real* sk = ring + slot(k) * kPS;
     const real* xy = sk + colofs;                          // u, plane k at (i, j0+lj0)

@@ -115,3 +115,20 @@ def test_tma_configs_rejected_by_an_earlier_tuner_run(gpu_ctx, compiler, precisi
         got = run_config(gpu_ctx, compiler, "advec_u", lay, cfg)
         err = rel_error(got["ut"], ref["ut"], lay)
         assert err <= TOL[precision], (case, err)
+
+
+@pytest.mark.parametrize("kernel", ["advec_u", "diff_uvw"])
+def test_tma_repeated_launches_are_stable(gpu_ctx, compiler, kernel):
+    """Intermittent-race guard: the same TMA configuration, launched repeatedly on
+    a grid with many z-chunks, must reproduce the oracle every time (an earlier
+    advec_u TMA build read the w plane of a chunk's first steps before its
+    mbarrier completed — caught by the tuner's replay verification)."""
+    from paper_2303_12374_b200.stencils.layout import GridLayout
+
+    lay = GridLayout(256, 64, 96, "fp32")
+    ref, _ = oracle_outputs(kernel, lay)
+    cfg = dict(_default(kernel, "fp32"), staging="TMA", block_x=128, block_y=1, tile_y=1, depth=2, zchunk=8)
+    for _ in range(4):
+        got = run_config(gpu_ctx, compiler, kernel, lay, cfg)
+        for name in ref:
+            assert rel_error(got[name], ref[name], lay) <= TOL["fp32"], name
