@@ -59,6 +59,9 @@ class SlabDriver:
         self._ev_halo = Event()
         self.kernel_events: list[tuple[Event, Event]] = []
         self.reports = {}
+        self._stream_state = None
+        self._h2d = self._d2h = None
+        self.stream_bytes = (0, 0)  # (h2d, d2h) bytes of the last step_host
 
     # -- setup -------------------------------------------------------------------------
     def resolve(self) -> dict:
@@ -81,11 +84,14 @@ class SlabDriver:
         return self.layout.itot * self.layout.jtot * (ke - kb)
 
     # -- one application step -------------------------------------------------------------
-    def exchange(self) -> None:
+    def exchange(self, after: Event | None = None) -> None:
+        """Halo exchange on the comm stream, ordered after ``after`` (default:
+        the work enqueued on the compute stream so far)."""
         if self.exchanger is None:
             return
-        self._ev_start.record(self.compute)
-        self.comm.wait(self._ev_start)
+        if after is None:
+            after = self._ev_start.record(self.compute)
+        self.comm.wait(after)
         lay = self.layout
         for field, (down, up) in HALO_REACH[self.kernel].items():
             self.exchanger.exchange(self.comm, [self.problem.field_ptr(field)], lay.elem_bytes, lay.kk, lay.kstart,
@@ -112,7 +118,72 @@ class SlabDriver:
                 launched += 1
         return launched
 
+    def step_host(self, host: dict[str, int], chunks: int = 16) -> int:
+        """One step streamed from/to pinned host memory (``stream.py``).
+
+        ``host`` maps every field to a pinned host buffer laid out exactly like
+        the device allocation (``layout.alloc_bytes``); inputs and RMW outputs
+        are read from it, the tendencies written back.  Enqueued on the
+        compute, h2d, d2h (and comm) streams and joined back into ``compute``;
+        returns the number of kernels launched."""
+        from .cuda._abi import check, lib
+        from .stream import stream_plan
+
+        lay = self.layout
+        if self._stream_state is None or self._stream_state[0] != chunks:
+            fields = tuple(self.problem.fields)
+            plan = stream_plan(self.kernel, fields, self.problem.outputs(), self.ranges, lay.kcells, lay.kstart,
+                               lay.kend, self.below, self.above, chunks)
+            args = {st.name: self.problem.args(st.k_range) for st in plan}
+            events = [(Event(), Event()) for _ in plan]
+            if self._h2d is None:
+                self._h2d, self._d2h = Stream.create(), Stream.create()
+                self._ev_join = Event()
+            self._stream_state = (chunks, plan, args, events)
+        _, plan, args, events = self._stream_state
+        plane = lay.kk * lay.elem_bytes
+        lead = lay.lead * lay.elem_bytes
+        dev = {n: a.ptr for n, a in self.problem.fields.items()}
+        ident = self.ctx.ident
+
+        start = self._ev_start.record(self.compute)
+        self._h2d.wait(start)
+        self._d2h.wait(start)
+        n_boundary = sum(1 for st in plan if st.after_halo)
+        for i, st in enumerate(plan):
+            for c in st.uploads:
+                off = lead + c.p0 * plane
+                check(lib().klb_memcpy_htod(dev[c.field] + off, host[c.field] + off, (c.p1 - c.p0) * plane,
+                                            self._h2d.handle))
+            events[i][0].record(self._h2d)
+            if self.exchanger is not None and i + 1 == max(n_boundary, 1):
+                self.exchange(after=events[i][0])
+        order = [i for i, st in enumerate(plan) if not st.after_halo] + [i for i, st in enumerate(plan) if st.after_halo]
+        waited_halo = False
+        for i in order:
+            st = plan[i]
+            self.compute.wait(events[i][0])
+            if st.after_halo and self.exchanger is not None and not waited_halo:
+                self.compute.wait(self._ev_halo)
+                waited_halo = True
+            self.wisdom.launch(ident, args[st.name], stream=self.compute)
+            events[i][1].record(self.compute)
+            self._d2h.wait(events[i][1])
+            for c in st.downloads:
+                off = lead + c.p0 * plane
+                check(lib().klb_memcpy_dtoh(host[c.field] + off, dev[c.field] + off, (c.p1 - c.p0) * plane,
+                                            self._d2h.handle))
+        if self.exchanger is not None and not waited_halo:
+            self.compute.wait(self._ev_halo)
+        self.compute.wait(self._ev_join.record(self._d2h))
+        self.stream_bytes = (sum((c.p1 - c.p0) * plane for st in plan for c in st.uploads),
+                             sum((c.p1 - c.p0) * plane for st in plan for c in st.downloads))
+        return len(plan)
+
     def close(self) -> None:
         self.problem.close()
         if self.comm is not None:
             self.comm.close()
+        for s in (self._h2d, self._d2h):
+            if s is not None:
+                s.close()

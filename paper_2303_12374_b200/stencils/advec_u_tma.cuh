@@ -1,22 +1,38 @@
 // advec_u_tma.cuh — STAGING == TMA variant of advec_u (included by
-// advec_u.cu).  Same flux-form z-march as ZMARCH (advec_u_zmarch.cuh), with
-// every operand fetched by the Tensor Memory Accelerator into a shared-memory
-// ring of DEPTH+4 slots (one mbarrier each).  Slot p holds plane p of
+// advec_u.cu).  Flux-form z-march (see advec_u_zmarch.cuh) with every operand
+// fetched by the Tensor Memory Accelerator into a shared-memory ring of
+// DEPTH+4 slots (one mbarrier each).  Slot p holds plane p of
 //   * u with a 3-cell x/y halo — plane k feeds the x/y stencil of step k and
 //     plane k+3 the z-window (so u[k+3] of every cell comes from the ring);
 //   * v (columns i-1..i, rows j..j+1), w (columns i-1..i) and ut (no halo):
 //     step k reads v and ut of plane k and w of plane k+1;
 // so the compute warps issue no global loads, only the final ut stores.  One
 // elected thread refills the slot vacated by plane k-1 at the start of step
-// k, keeping DEPTH planes beyond the ones being read in flight.  Box starts
-// are rounded down to 16-byte aligned x (TMA requires it).  Requires
-// BLOCK_X % 32 == 0 (warps along x; west fluxes via __shfl_up_sync).
+// k, keeping DEPTH planes beyond the ones being read in flight.
+//
+// A thread owns TILE_X consecutive columns (TILE_X in {1, 2, 4}; CONTIG_X)
+// times a strip of TILE_Y rows.  Per plane it evaluates TILE_X+1 x-faces
+// (the shared faces of its own cells once), TILE_X y-faces per row (the
+// south face carried from the row below) and TILE_X z-faces per row (the
+// bottom face carried from the plane below): 3 + 1/TILE_X + 1/TILE_Y face
+// fluxes per cell.  The advection work is issue-bound in fp32, so the
+// operand reads are vectorised: boxes start at column i0-4, so when the
+// tensor's x alignment makes column i0 16-byte aligned (always, for the
+// GridLayout pitches) every thread's cells sit at vector-aligned shared
+// offsets and a row of TILE_X+8 values is TILE_X+8 / VA loads of VA
+// elements (VA = min(TILE_X, 16 B)), the ut stores VA-wide too; a uniform
+// branch falls back to scalar accesses for any other alignment.  Face
+// velocities are passed as sums (the 1/2 of interp2 is folded into the 1/120
+// scale factors).
 
-#if BLOCK_Z != 1 || TILE_Z != 1 || TILE_X != 1
-#error "advec_u TMA requires BLOCK_Z == TILE_Z == TILE_X == 1"
+#if BLOCK_Z != 1 || TILE_Z != 1
+#error "advec_u TMA requires BLOCK_Z == TILE_Z == 1"
 #endif
-#if BLOCK_X % 32 != 0
-#error "advec_u TMA requires BLOCK_X to be a multiple of the warp size"
+#if TILE_X != 1 && TILE_X != 2 && TILE_X != 4
+#error "advec_u TMA requires TILE_X in {1, 2, 4}"
+#endif
+#if TILE_X > 1 && !CONTIG_X
+#error "advec_u TMA: TILE_X > 1 needs consecutive columns (CONTIG_X)"
 #endif
 #ifndef DEPTH
 #define DEPTH 2
@@ -26,16 +42,21 @@
 
 namespace {
 constexpr int kS = static_cast<int>(sizeof(real));
-constexpr int kE = 16 / kS;
-constexpr int kTYT = BLOCK_Y * TILE_Y;
-constexpr int kBW = (((BLOCK_X + 6) * kS + 16 - kS + 15) / 16) * 16 / kS;  // u: 3-halo + alignment slack
+constexpr int kE = 16 / kS;                // elements per 16 bytes
+constexpr int kTX = TILE_X, kTY = TILE_Y;
+constexpr int kXT = BLOCK_X * kTX;          // columns per block
+constexpr int kTYT = BLOCK_Y * kTY;         // rows per block
+constexpr int kVA = kTX < kE ? kTX : kE;    // vector width (elements) of aligned reads
+__host__ __device__ constexpr int rup(int a, int b) { return (a + b - 1) / b * b; }
+// box widths: start column i0-4 rounded down to 16 B (up to kE-1 slack)
+constexpr int kBW = rup(kXT + 8 + kE - 1, kE);  // u: columns i0-4 .. i0+kXT+3
 constexpr int kBH = kTYT + 6;
-constexpr int kVW = (((BLOCK_X + 1) * kS + 16 - kS + 15) / 16) * 16 / kS;  // v, w: column i-1 + slack
-constexpr int kTW = ((BLOCK_X * kS + 16 - kS + 15) / 16) * 16 / kS;        // ut: no halo
-constexpr int kUB = ((kBW * kBH * kS + 127) / 128) * 128;
-constexpr int kVB = ((kVW * (kTYT + 1) * kS + 127) / 128) * 128;
-constexpr int kWB = ((kVW * kTYT * kS + 127) / 128) * 128;
-constexpr int kTB = ((kTW * kTYT * kS + 127) / 128) * 128;
+constexpr int kVW = rup(kXT + 4 + kE - 1, kE);  // v, w: columns i0-4 .. i0+kXT-1
+constexpr int kTW = rup(kXT + kE - 1, kE);      // ut: columns i0 .. i0+kXT-1
+constexpr int kUB = rup(kBW * kBH * kS, 128);
+constexpr int kVB = rup(kVW * (kTYT + 1) * kS, 128);
+constexpr int kWB = rup(kVW * kTYT * kS, 128);
+constexpr int kTB = rup(kTW * kTYT * kS, 128);
 constexpr int kPB = kUB + kVB + kWB + kTB;  // bytes per plane slot
 constexpr int kPS = kPB / kS;
 constexpr int kVO = kUB / kS, kWO = (kUB + kVB) / kS, kTO = (kUB + kVB + kWB) / kS;  // field offsets in a slot
@@ -43,6 +64,204 @@ constexpr int kNS = DEPTH + 4;
 constexpr unsigned kTxBytes =
     static_cast<unsigned>((kBW * kBH + kVW * (kTYT + 1) + kVW * kTYT + kTW * kTYT) * kS);
 static_assert(kBW <= 256 && kBH <= 256, "TMA box extents are limited to 256");
+
+template <int N>
+struct __align__(N * sizeof(real)) Pack {
+  real v[N];
+};
+
+// d[e] = s[e] for e in [LO, HI), widened to VA-aligned loads of VA elements
+// (s must be VA-element aligned).
+template <int VA, int LO, int HI, int N>
+__device__ __forceinline__ void ld_span(real (&d)[N], const real* s) {
+  constexpr int lo = LO / VA * VA, hi = (HI + VA - 1) / VA * VA;
+  static_assert(hi <= N, "span exceeds the destination");
+#pragma unroll
+  for (int e = lo; e < hi; e += VA) {
+    const Pack<VA> p = *reinterpret_cast<const Pack<VA>*>(s + e);
+#pragma unroll
+    for (int q = 0; q < VA; ++q) d[e + q] = p.v[q];
+  }
+}
+
+template <int VA>
+__device__ __forceinline__ void st_span(real* d, const real (&s)[kTX]) {
+#pragma unroll
+  for (int e = 0; e < kTX; e += VA) {
+    Pack<VA> p;
+#pragma unroll
+    for (int q = 0; q < VA; ++q) p.v[q] = s[e + q];
+    *reinterpret_cast<Pack<VA>*>(d + e) = p;
+  }
+}
+
+// Per-block state of the march (a struct with a member template rather than
+// a generic lambda: NVRTC has no extended device lambdas).
+struct AdvecTma {
+  real* ut;
+  const real* u;
+  const real* rhoref;
+  const real* rhorefh;
+  const real* dzi;
+  real* ring;
+  unsigned long long* full;
+  const TmaDesc* maps;
+  real dxi120, dyi120;
+  int j0, k0, k1, kmax, tid, iend, jend;
+  int xu, xv, xw, xt;  // 16-byte aligned box starts
+  int ic, lj0, uofs, vofs, wofs, tofs;
+
+  __device__ __forceinline__ void issue(int slot, int p) const {
+    unsigned long long* bar = full + slot;
+    real* dst = ring + slot * kPS;
+    kl::mbar_expect_tx(bar, kTxBytes);
+    kl::tma_load_3d(dst, maps + 0, bar, xu, j0 - 3, p);
+    kl::tma_load_3d(dst + kVO, maps + 1, bar, xv, j0, p);
+    kl::tma_load_3d(dst + kWO, maps + 2, bar, xw, j0, p);
+    kl::tma_load_3d(dst + kTO, maps + 3, bar, xt, j0, p);
+  }
+
+  // main loop, VA = vector width of the shared-memory reads / ut stores
+  template <int VA>
+  __device__ __forceinline__ void march() const {
+    constexpr long long K1 = KL_KK;
+    // per-plane z factors of the chunk, filled by the block after the ring's
+    // barrier init (one division per plane instead of one per thread and plane)
+    const real* zprof = ring + kNS * kPS;  // [ZCHUNK][2]: rhorefh[k+1], dzi[k] / (120 rhoref[k])
+    real uq[kTY][kTX][6];  // u[k-2 .. k+3] of every cell (k+3 loaded at step k)
+    real fz_bot[kTY][kTX];
+    // planes k0..k0+2 are first read as the x/y plane (k) or the w plane (k+1)
+    // of the first steps; every later plane is first read as the z-window
+    // plane (k+3) and waited for there.  Slots/parities advance incrementally.
+    kl::mbar_wait(full + 0, 0);
+    kl::mbar_wait(full + 1, 0);
+    kl::mbar_wait(full + 2, 0);
+    {
+      const real rh0 = rhorefh[k0];
+      const real* wp = ring + kWO + wofs;  // slot 0 = plane k0
+#pragma unroll
+      for (int t = 0; t < kTY; ++t) {
+        const int j = min(j0 + lj0 + t, jend - 1);
+        real wr[kTX + 8];
+        wr[3] = wp[t * kVW + 3];
+        ld_span<VA, 4, 4 + kTX>(wr, wp + t * kVW);
+#pragma unroll
+        for (int c = 0; c < kTX; ++c) {
+          const int i = min(ic + c, iend - 1);
+          const long long b = i + static_cast<long long>(j) * KL_JJ + static_cast<long long>(k0) * KL_KK;
+          const real um3 = u[b - 3 * K1];  // planes below the chunk: not staged
+#pragma unroll
+          for (int m = 0; m < 5; ++m) uq[t][c][m] = u[b + (m - 2) * K1];
+          fz_bot[t][c] = rh0 * kl::flux5x60(wr[3 + c] + wr[4 + c], um3, uq[t][c][0], uq[t][c][1], uq[t][c][2],
+                                            uq[t][c][3], uq[t][c][4]);
+        }
+      }
+    }
+
+    int s0 = 0, s1 = 1, s3 = 3, sprev = kNS - 1;  // slots of planes k, k+1, k+3, k-1
+    unsigned ph3 = 0;                              // barrier parity of plane k+3
+    for (int k = k0; k < k1; ++k) {
+      __syncthreads();  // plane k-1's slot is free
+      if (tid == 0) {
+        const int p = k - 1 + kNS;
+        if (k > k0 && p <= kmax) {
+          kl::fence_proxy_async_smem();
+          issue(sprev, p);
+        }
+      }
+      kl::mbar_wait(full + s3, ph3);
+      const real* sk = ring + s0 * kPS;
+      const real* xy = sk + uofs;                       // u, plane k at (ic-4, j0+lj0)
+      const real* zf = ring + s3 * kPS + uofs + 4;      // u, plane k+3 at (ic, j0+lj0)
+      const real* vp = sk + kVO + vofs;                 // v, plane k at (ic-4, j0+lj0)
+      const real* wp = ring + s1 * kPS + kWO + wofs;    // w, plane k+1 at (ic-4, j0+lj0)
+      const real* tp = sk + kTO + tofs;                 // ut, plane k at (ic, j0+lj0)
+      const real rh_top = zprof[2 * (k - k0)];
+      const real zfac120 = zprof[2 * (k - k0) + 1];
+      const long long kofs = static_cast<long long>(k) * K1;
+      sprev = s0;
+      s0 = s1;
+      s1 = s1 + 1 == kNS ? 0 : s1 + 1;
+      s3 = s3 + 1 == kNS ? 0 : s3 + 1;
+      ph3 ^= s3 == 0 ? 1u : 0u;
+
+      // u along y in this thread's columns: rows lj0-3 .. lj0+kTY+2
+      real ucol[kTY + 6][kTX];
+#pragma unroll
+      for (int m = 0; m < kTY + 6; ++m) {
+        if (m >= 3 && m < kTY + 3) continue;  // strip rows: taken from the x rows below
+        real r[kTX + 8];
+        ld_span<VA, 4, 4 + kTX>(r, xy + (m - 3) * kBW);
+#pragma unroll
+        for (int c = 0; c < kTX; ++c) ucol[m][c] = r[4 + c];
+      }
+      real xr[kTY][kTX + 8];  // x rows of the strip: columns ic-4 .. ic+kTX+3
+#pragma unroll
+      for (int t = 0; t < kTY; ++t) {
+        ld_span<VA, 1, kTX + 7>(xr[t], xy + t * kBW);
+#pragma unroll
+        for (int c = 0; c < kTX; ++c) ucol[t + 3][c] = xr[t][4 + c];
+      }
+      // south faces of the strip (row j0+lj0-1/2)
+      real fy_lo[kTX];
+      {
+        real vr[kTX + 8];
+        vr[3] = vp[3];
+        ld_span<VA, 4, 4 + kTX>(vr, vp);
+#pragma unroll
+        for (int c = 0; c < kTX; ++c)
+          fy_lo[c] = kl::flux5x60(vr[3 + c] + vr[4 + c], ucol[0][c], ucol[1][c], ucol[2][c], ucol[3][c], ucol[4][c],
+                                  ucol[5][c]);
+      }
+
+#pragma unroll
+      for (int t = 0; t < kTY; ++t) {
+        // x: faces f = 0..kTX sit between columns ic+f-1 and ic+f
+        real fx[kTX + 1];
+#pragma unroll
+        for (int f = 0; f <= kTX; ++f)
+          fx[f] = kl::flux5x60(xr[t][f + 3] + xr[t][f + 4], xr[t][f + 1], xr[t][f + 2], xr[t][f + 3],
+                               xr[t][f + 4], xr[t][f + 5], xr[t][f + 6]);
+        real vr[kTX + 8], wr[kTX + 8], zr[kTX + 8], tr[kTX + 8], out[kTX];
+        const real* vn = vp + (t + 1) * kVW;
+        vr[3] = vn[3];
+        ld_span<VA, 4, 4 + kTX>(vr, vn);
+        const real* wrow = wp + t * kVW;
+        wr[3] = wrow[3];
+        ld_span<VA, 4, 4 + kTX>(wr, wrow);
+        ld_span<VA, 0, kTX>(zr, zf + t * kBW);
+        ld_span<VA, 0, kTX>(tr, tp + t * kTW);
+#pragma unroll
+        for (int c = 0; c < kTX; ++c) {
+          real* q = uq[t][c];
+          q[5] = zr[c];
+          // y: north face of this row; south face carried from the previous row
+          const real fy_hi = kl::flux5x60(vr[3 + c] + vr[4 + c], ucol[t + 1][c], ucol[t + 2][c], ucol[t + 3][c],
+                                          ucol[t + 4][c], ucol[t + 5][c], ucol[t + 6][c]);
+          // z: top face of this plane; bottom face carried from the previous plane
+          const real fz_top = rh_top * kl::flux5x60(wr[3 + c] + wr[4 + c], q[0], q[1], q[2], q[3], q[4], q[5]);
+          out[c] = tr[c] - ((fx[c + 1] - fx[c]) * dxi120 + (fy_hi - fy_lo[c]) * dyi120 +
+                            (fz_top - fz_bot[t][c]) * zfac120);
+          fy_lo[c] = fy_hi;
+          fz_bot[t][c] = fz_top;
+#pragma unroll
+          for (int m = 0; m < 5; ++m) q[m] = q[m + 1];
+        }
+        const int j = j0 + lj0 + t;
+        if (j < jend) {
+          real* dst = ut + ic + static_cast<long long>(j) * KL_JJ + kofs;
+          if (ic + kTX <= iend) {
+            st_span<VA>(dst, out);
+          } else {
+#pragma unroll
+            for (int c = 0; c < kTX; ++c)
+              if (ic + c < iend) dst[c] = out[c];
+          }
+        }
+      }
+    }
+  }
+};
 }  // namespace
 
 // positions: ut=0 u=1 v=2 w=3, jj=9 kk=10 (definitions.ARG_LAYOUT["advec_u"])
@@ -66,38 +285,50 @@ KL_ENTRY(real* __restrict__ ut, const real* __restrict__ u, const real* __restri
   unsigned long long* full = reinterpret_cast<unsigned long long*>(sbase);
   real* const ring = reinterpret_cast<real*>(sbase + 128);  // [kNS][kPS]
 
-  const unsigned nbx = kl::ceil_div(iend - istart, BLOCK_X);
+  const unsigned nbx = kl::ceil_div(iend - istart, kXT);
   const unsigned nby = kl::ceil_div(jend - jstart, kTYT);
   const unsigned nbz = kl::ceil_div(kend - kstart, ZCHUNK);
   int bx, by, bz;
   kl::unravel(blockIdx.x, nbx, nby, nbz, bx, by, bz);
-  const int i0 = istart + bx * BLOCK_X;
+  const int i0 = istart + bx * kXT;
   const int j0 = jstart + by * kTYT;
   const int k0 = kstart + bz * ZCHUNK;
   const int k1 = min(k0 + ZCHUNK, kend);
-  const int kmax = k1 + 2;  // last plane the z-window reads
   const int tid = threadIdx.x + threadIdx.y * BLOCK_X;
-  const int lane = threadIdx.x & 31;
-  const int xu = i0 - 3 + kl::tma_xoff(u);  // tensor x of column i0-3
-  const int xu0 = xu & ~(kE - 1);            // 16-byte aligned box starts
-  const int xv0 = (xu + 2) & ~(kE - 1);      // column i0-1
-  const int xt0 = (xu + 3) & ~(kE - 1);      // column i0
-  const int ushift = xu - xu0, vshift = xu + 2 - xv0, tshift = xu + 3 - xt0;
-  const real dxi60 = dxi * real(1.0 / 60.0);
-  const real dyi60 = dyi * real(1.0 / 60.0);
-  constexpr long long K1 = KL_KK;
+  // box starts: tensor x of column i0-4 (u, v, w) / i0 (ut) rounded down to
+  // 16 B; the rounding shifts the columns by sh_* within the boxes
+  const int xu = i0 - 4 + kl::tma_xoff(u), xv = i0 - 4 + kl::tma_xoff(v), xw = i0 - 4 + kl::tma_xoff(w);
+  const int xt = i0 + kl::tma_xoff(ut);
+  const int sh_u = xu & (kE - 1), sh_v = xv & (kE - 1), sh_w = xw & (kE - 1), sh_t = xt & (kE - 1);
 
-  auto slot = [&](int p) { return (p - k0) % kNS; };
-  auto issue = [&](int p) {
-    unsigned long long* bar = full + slot(p);
-    real* dst = ring + slot(p) * kPS;
-    kl::mbar_expect_tx(bar, kTxBytes);
-    kl::tma_load_3d(dst, maps + 0, bar, xu0, j0 - 3, p);
-    kl::tma_load_3d(dst + kVO, maps + 1, bar, xv0, j0, p);
-    kl::tma_load_3d(dst + kWO, maps + 2, bar, xv0, j0, p);
-    kl::tma_load_3d(dst + kTO, maps + 3, bar, xt0, j0, p);
-  };
-  auto wait = [&](int p) { kl::mbar_wait(full + slot(p), ((p - k0) / kNS) & 1); };
+  AdvecTma m;
+  m.ut = ut;
+  m.u = u;
+  m.rhoref = rhoref;
+  m.rhorefh = rhorefh;
+  m.dzi = dzi;
+  m.ring = ring;
+  m.full = full;
+  m.maps = maps;
+  m.dxi120 = dxi * real(1.0 / 120.0);
+  m.dyi120 = dyi * real(1.0 / 120.0);
+  m.j0 = j0;
+  m.k0 = k0;
+  m.k1 = k1;
+  m.kmax = k1 + 2;  // last plane the z-window reads
+  m.tid = tid;
+  m.iend = iend;
+  m.jend = jend;
+  m.xu = xu - sh_u;
+  m.xv = xv - sh_v;
+  m.xw = xw - sh_w;
+  m.xt = xt - sh_t;
+  m.ic = i0 + kTX * static_cast<int>(threadIdx.x);  // first column of this thread
+  m.lj0 = threadIdx.y * kTY;
+  m.uofs = sh_u + (m.lj0 + 3) * kBW + kTX * threadIdx.x;  // (ic-4, j0+lj0) in the u box
+  m.vofs = sh_v + m.lj0 * kVW + kTX * threadIdx.x;        // (ic-4, j0+lj0) in the v box
+  m.wofs = sh_w + m.lj0 * kVW + kTX * threadIdx.x;        // (ic-4, j0+lj0) in the w box
+  m.tofs = sh_t + m.lj0 * kTW + kTX * threadIdx.x;        // (ic, j0+lj0) in the ut box
 
   if (tid == 0) {
     for (int s = 0; s < kNS; ++s) kl::mbar_init(full + s, 1);
@@ -105,88 +336,19 @@ KL_ENTRY(real* __restrict__ ut, const real* __restrict__ u, const real* __restri
   }
   __syncthreads();
   if (tid == 0) {
-    for (int p = k0; p <= min(k0 + kNS - 1, kmax); ++p) issue(p);
+    for (int p = k0; p <= min(k0 + kNS - 1, m.kmax); ++p) m.issue(p - k0, p);
   }
-
-  const int i = min(i0 + static_cast<int>(threadIdx.x), iend - 1);
-  const bool col_ok = i0 + static_cast<int>(threadIdx.x) < iend;
-  const int lj0 = threadIdx.y * TILE_Y;
-  const int colofs = (lj0 + 3) * kBW + threadIdx.x + 3 + ushift;  // (i, j0+lj0) in the u box
-  const int vofs = lj0 * kVW + threadIdx.x + vshift;             // (i-1, j0+lj0) in the v / w boxes
-  const int tofs = lj0 * kTW + threadIdx.x + tshift;             // (i, j0+lj0) in the ut box
-  real uq[TILE_Y][7];
-  real fz_bot[TILE_Y];
-  // planes k0..k0+2 are first read as the x/y plane (k) or the w plane (k+1)
-  // of the first steps; every later plane is first read as the z-window
-  // plane (k+3) and waited for there
-  wait(k0);
-  wait(k0 + 1);
-  wait(k0 + 2);
   {
-    const real* ring0 = ring + slot(k0) * kPS;
-    const real rh0 = rhorefh[k0];
-#pragma unroll
-    for (int t = 0; t < TILE_Y; ++t) {
-      const int j = min(j0 + lj0 + t, jend - 1);
-      const long long b = i + static_cast<long long>(j) * KL_JJ + static_cast<long long>(k0) * KL_KK;
-#pragma unroll
-      for (int m = 0; m < 3; ++m) uq[t][m] = u[b + (m - 3) * K1];  // planes below the chunk: not staged
-#pragma unroll
-      for (int m = 3; m < 6; ++m) uq[t][m] = u[b + (m - 3) * K1];
-      const real* wp = ring0 + kWO + vofs + t * kVW;
-      const real wb = kl::interp2(wp[0], wp[1]);
-      fz_bot[t] = rh0 * kl::flux5x60(wb, uq[t][0], uq[t][1], uq[t][2], uq[t][3], uq[t][4], uq[t][5]);
+    real* zprof = ring + kNS * kPS;
+    for (int q = tid; q < k1 - k0; q += KL_THREADS) {
+      zprof[2 * q] = rhorefh[k0 + q + 1];
+      zprof[2 * q + 1] = dzi[k0 + q] / (rhoref[k0 + q] * real(120));
     }
   }
-
-  for (int k = k0; k < k1; ++k) {
-    __syncthreads();  // plane k-1's slot is free
-    if (tid == 0) {
-      const int p = k - 1 + kNS;
-      if (k > k0 && p <= kmax) {
-        kl::fence_proxy_async_smem();
-        issue(p);
-      }
-    }
-    wait(k + 3);
-    const real* sk = ring + slot(k) * kPS;
-    const real* xy = sk + colofs;                          // u, plane k at (i, j0+lj0)
-    const real* zf = ring + slot(k + 3) * kPS + colofs;    // u, plane k+3
-    const real* vp = sk + kVO + vofs;                      // v, plane k at (i-1, j0+lj0)
-    const real* wp = ring + slot(k + 1) * kPS + kWO + vofs;  // w, plane k+1 at (i-1, j0+lj0)
-    const real* tp = sk + kTO + tofs;                      // ut, plane k
-    const real rh_top = rhorefh[k + 1];
-    const real zfac60 = dzi[k] / (rhoref[k] * real(60));
-    const long long kofs = static_cast<long long>(k) * K1;
-
-    real ucol[TILE_Y + 6];
-#pragma unroll
-    for (int m = 0; m < TILE_Y + 6; ++m) ucol[m] = xy[(m - 3) * kBW];
-    real fy_lo = kl::flux5x60(kl::interp2(vp[0], vp[1]), ucol[0], ucol[1], ucol[2], ucol[3], ucol[4], ucol[5]);
-
-#pragma unroll
-    for (int t = 0; t < TILE_Y; ++t) {
-      const real* row = xy + t * kBW;
-      real* q = uq[t];
-      q[6] = zf[t * kBW];
-      const real xm2 = row[-2], xm1 = row[-1], x0v = ucol[t + 3], xp1 = row[1], xp2 = row[2], xp3 = row[3];
-      const real fx_e = kl::flux5x60(kl::interp2(x0v, xp1), xm2, xm1, x0v, xp1, xp2, xp3);
-      real fx_w = __shfl_up_sync(0xffffffffu, fx_e, 1);
-      if (lane == 0) fx_w = kl::flux5x60(kl::interp2(xm1, x0v), row[-3], xm2, xm1, x0v, xp1, xp2);
-      const real* vn = vp + (t + 1) * kVW;
-      const real fy_hi = kl::flux5x60(kl::interp2(vn[0], vn[1]), ucol[t + 1], ucol[t + 2], ucol[t + 3],
-                                      ucol[t + 4], ucol[t + 5], ucol[t + 6]);
-      const real* wt_ = wp + t * kVW;
-      const real fz_top = rh_top * kl::flux5x60(kl::interp2(wt_[0], wt_[1]), q[1], q[2], q[3], q[4], q[5], q[6]);
-      const int j = j0 + lj0 + t;
-      if (col_ok && j < jend) {
-        const long long ijk = i + static_cast<long long>(j) * KL_JJ + kofs;
-        ut[ijk] = tp[t * kTW] - ((fx_e - fx_w) * dxi60 + (fy_hi - fy_lo) * dyi60 + (fz_top - fz_bot[t]) * zfac60);
-      }
-      fy_lo = fy_hi;
-      fz_bot[t] = fz_top;
-#pragma unroll
-      for (int m = 0; m < 6; ++m) q[m] = q[m + 1];
-    }
+  // (the march's first __syncthreads publishes zprof)
+  if (kVA > 1 && (sh_u | sh_v | sh_w | sh_t) == 0) {
+    m.march<kVA>();
+  } else {
+    m.march<1>();
   }
 }

@@ -8,18 +8,16 @@
 //     register window and carries F[k+1/2] to the next plane as F[k-1/2];
 //   * y: a thread owns a contiguous strip of TILE_Y rows; F[j+1/2] of row j is
 //     reused as F[j-1/2] of row j+1 (one extra flux per strip);
-//   * x: warps run along x, F[i-1] (the west face) is the east face of the
-//     neighbouring lane (__shfl_up_sync); lane 0 evaluates its own.
+//   * x: both faces of a cell are evaluated (sharing the west face through a
+//     warp shuffle was measured slower: lane 0's own evaluation runs as a
+//     divergent branch in every warp, costing as many issue slots as it saves).
 // u is staged per plane into a double-buffered shared-memory tile with a
 // 3-cell halo (the x/y stencil reads), the next plane is prefetched into
 // registers before the compute and stored after it — one __syncthreads per
-// plane.  Requires BLOCK_X % 32 == 0 (warps along x).
+// plane.
 
 #if BLOCK_Z != 1 || TILE_Z != 1 || TILE_X != 1
 #error "advec_u ZMARCH requires BLOCK_Z == TILE_Z == TILE_X == 1"
-#endif
-#if BLOCK_X % 32 != 0
-#error "advec_u ZMARCH requires BLOCK_X to be a multiple of the warp size"
 #endif
 
 #define KL_TYT (BLOCK_Y * TILE_Y)
@@ -48,7 +46,6 @@ KL_ENTRY(real* __restrict__ ut, const real* __restrict__ u, const real* __restri
   const int k0 = kstart + bz * ZCHUNK;
   const int k1 = min(k0 + ZCHUNK, kend);
   const int tid = threadIdx.x + threadIdx.y * BLOCK_X;
-  const int lane = threadIdx.x & 31;
   const real dxi60 = dxi * real(1.0 / 60.0);
   const real dyi60 = dyi * real(1.0 / 60.0);
   constexpr long long K1 = KL_KK;
@@ -125,11 +122,10 @@ KL_ENTRY(real* __restrict__ ut, const real* __restrict__ u, const real* __restri
       const long long ijk = base[t] + kofs;
       const real* row = col + t * KL_SW;
       const real* q = uq[t];
-      // x: east face of this cell; west face from the neighbouring lane
+      // x: east and west faces of this cell
       const real xm2 = row[-2], xm1 = row[-1], x0 = ucol[t + 3], xp1 = row[1], xp2 = row[2], xp3 = row[3];
       const real fx_e = kl::flux5x60(kl::interp2(x0, xp1), xm2, xm1, x0, xp1, xp2, xp3);
-      real fx_w = __shfl_up_sync(0xffffffffu, fx_e, 1);
-      if (lane == 0) fx_w = kl::flux5x60(kl::interp2(xm1, x0), row[-3], xm2, xm1, x0, xp1, xp2);
+      const real fx_w = kl::flux5x60(kl::interp2(xm1, x0), row[-3], xm2, xm1, x0, xp1, xp2);
       // y: north face of this row; south face carried from the previous row
       const real vn = kl::interp2(v[ijk - 1 + J1], v[ijk + J1]);
       const real fy_hi = kl::flux5x60(vn, ucol[t + 1], ucol[t + 2], ucol[t + 3], ucol[t + 4], ucol[t + 5], ucol[t + 6]);

@@ -111,12 +111,14 @@ _ZMARCH_PLANE_LIMIT = {
 #: TMA box extents are <= 256 elements; the smem ring must fit the opt-in limit
 _TMA_LIMIT = {
     "diff_uvw": ['staging != "TMA" || (block_x <= 128 && (block_x + 6) * (block_y * tile_y + 2) * (depth + 2) <= 2048)'],
-    "advec_u": ['staging != "TMA" || (block_x <= 128 && (block_x + 12) * (block_y * tile_y + 6) * (depth + 4) <= 8192)'],
+    "advec_u": ['staging != "TMA" || (block_x * tile_x <= 128 && '
+                '(block_x * tile_x + 12) * (block_y * tile_y + 6) * (depth + 4) <= 8192)'],
 }
-#: knobs the ZMARCH variant of each kernel fixes (pinned to their defaults)
+#: knobs the ZMARCH/TMA variants of each kernel fix (pinned to their defaults)
 _ZMARCH_PINNED = {
-    # warps along x (block_x % 32 == 0), one column per thread, contiguous y strip
-    "advec_u": "block_x >= 32 && tile_x == 1 && !unroll_x && !unroll_y && !contiguous_x && !contiguous_y",
+    # a contiguous y strip; one column per thread, or (TMA) tile_x consecutive columns
+    "advec_u": '!unroll_x && !unroll_y && !contiguous_y && '
+               '((tile_x == 1 && !contiguous_x) || (staging == "TMA" && tile_x > 1 && contiguous_x))',
     # one column per thread, a contiguous strip of tile_y rows (flux reuse along y)
     "diff_uvw": "tile_x == 1 && !unroll_x && !unroll_y && !contiguous_x && !contiguous_y",
 }
@@ -156,6 +158,7 @@ _FAMILY_EXTRA = {
     (kernel, fam): {"tile_x": 1, "contiguous_x": False, "contiguous_y": False}
     for kernel in ("diff_uvw", "advec_u") for fam in ("ZMARCH", "TMA")
 }
+_FAMILY_EXTRA["advec_u", "TMA"] = {"contiguous_y": False}  # tile_x in {1, 2, 4} (consecutive columns)
 
 
 def family_space(kernel: str, family: str) -> ConfigSpace:
@@ -186,16 +189,18 @@ _SMEM = {
 # fields; advec_u: depth+4 slots of u (3-halo) + v, w, ut, since plane k+3
 # feeds the z-window); box width = block_x + halo
 # plus up to one 16-byte chunk of alignment slack, rounded to 16 B.
-_BW = "(ceil_div((block_x + {H}) * {S} + 16 - {S}, 16) * 16 / {S})"
+_BW = "(ceil_div(({X} + {H}) * {S} + 16 - {S}, 16) * 16 / {S})"
+_ADVEC_BOX = "ceil_div(" + _BW + " * (block_y * tile_y + {R}) * {S}, 128) * 128"
 _SMEM_TMA = {
-    "diff_uvw": "(256 + (depth + 2) * (4 * ceil_div(" + _BW.format(H=2, S="{S}") +
-                " * (block_y * tile_y + 2) * {S}, 128) * 128 + 3 * ceil_div(" + _BW.format(H=0, S="{S}") +
-                " * (block_y * tile_y) * {S}, 128) * 128))",
-    "advec_u": "(256 + (depth + 4) * (ceil_div(" + _BW.format(H=6, S="{S}") +
-               " * (block_y * tile_y + 6) * {S}, 128) * 128 + ceil_div(" + _BW.format(H=1, S="{S}") +
-               " * (block_y * tile_y + 1) * {S}, 128) * 128 + ceil_div(" + _BW.format(H=1, S="{S}") +
-               " * (block_y * tile_y) * {S}, 128) * 128 + ceil_div(" + _BW.format(H=0, S="{S}") +
-               " * (block_y * tile_y) * {S}, 128) * 128))",
+    # plus the chunk's 5 per-plane z factors
+    "diff_uvw": "(256 + (depth + 2) * (4 * ceil_div(" + _BW.format(X="block_x", H=2, S="{S}") +
+                " * (block_y * tile_y + 2) * {S}, 128) * 128 + 3 * ceil_div(" +
+                _BW.format(X="block_x", H=0, S="{S}") + " * (block_y * tile_y) * {S}, 128) * 128) + 5 * zchunk * {S})",
+    # advec_u boxes start at column i0-4: u (x halo 4+4, y halo 3+3), v (4 + 1 row), w (4), ut (0)
+    # plus the chunk's z factors (2 per plane)
+    "advec_u": "(256 + (depth + 4) * (" + " + ".join(
+        _ADVEC_BOX.format(X="block_x * tile_x", H=h, R=r, S="{S}") for h, r in ((8, 6), (4, 1), (4, 0), (0, 0))) +
+    ") + 2 * zchunk * {S})",
 }
 
 

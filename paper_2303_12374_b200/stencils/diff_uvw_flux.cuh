@@ -23,108 +23,95 @@ struct DiffCarry {
 // k+1 of field 0 (evisc) in the shared-memory ring; fields are `fs` elements
 // apart, rows SW elements.  With OUT=false only the carried upper-z
 // quantities are produced (the prologue at plane k0-1).
-// West-face value from the lane on the left: with warps laid along x
-// (BLOCK_X % 32 == 0) every x-face quantity is evaluated once per face — lane
-// l's east value is lane l+1's west value — and only lane 0 evaluates its own.
-#define KL_XSHFL ((BLOCK_X % 32) == 0)
-
-template <class F>
-__device__ __forceinline__ real from_west(real east, F&& own) {
-#if KL_XSHFL
-  real v = __shfl_up_sync(0xffffffffu, east, 1);
-  if ((threadIdx.x & 31) == 0) v = own();
-  return v;
-#else
-  (void)east;
-  return own();
-#endif
-}
-
+//
+// Register discipline: every value of the strip's next row (19 loads) is read
+// once and slides down to become the current row, so each shared-memory
+// element is loaded once per thread; the 1/4 of the edge viscosity averages is
+// folded into the scale factors qsx = dxi/4, qsy = dyi/4, qfac = fac_uv/4.
+// (x-faces are evaluated by both neighbouring cells: sharing them through
+// warp shuffles costs more issue slots than it saves — lane 0's own
+// evaluation runs as a divergent branch in every warp.)
 template <bool OUT, int SW, class Store>
 __device__ __forceinline__ void diff_step(const real* __restrict__ p0, const real* __restrict__ p1, int fs,
-                                          DiffCarry& c, real dxi, real dyi, real c2x, real c2y, real rh1,
-                                          real dzhi1, real rdz, real fac_uv, real fac_w, Store&& store) {
-  const real q = real(0.25);
-  // field accessors on the planes: f = 0 evisc, 1 u, 2 v, 3 w; row offset r (0 = strip row -1), column di
+                                          DiffCarry& c, real sx, real sy, real qsx, real qsy, real c2x, real c2y,
+                                          real rh1, real dzhi1, real rdz, real qfac, real fac_w, Store&& store) {
 #define P0(f, r, di) p0[(f) * fs + (r) * SW + (di)]
 #define P1(f, r, di) p1[(f) * fs + (r) * SW + (di)]
-  // registers of the current row (starts at strip row -1)
-  real e_0 = P0(0, 0, 0), e_p = P0(0, 0, 1);
-  real u_0 = P0(1, 0, 0), u_p = P0(1, 0, 1);
-  real v_0 = P0(2, 0, 0);
-  real e1_0 = P1(0, 0, 0), w1_0 = P1(3, 0, 0), v1_0 = P1(2, 0, 0);
-  // upper-y quantities of the previous row (row -1 computes them first)
-  real exy_i = 0, exy_i1 = 0, fyu = 0, gy = 0, eyz = 0, fyw = 0;
-  real u_lo0 = 0, u_lop = 0, w1_lo = 0;
-  real fyw_prev = 0;
+  // current row (starts at strip row -1): e/u/v at plane k; f = evisc, w, y = v, x = u at
+  // plane k+1; z = w at plane k
+  real e_m = P0(0, 0, -1), e_0 = P0(0, 0, 0), e_p = P0(0, 0, 1);
+  real u_m = P0(1, 0, -1), u_0 = P0(1, 0, 0), u_p = P0(1, 0, 1);
+  real v_m = P0(2, 0, -1), v_0 = P0(2, 0, 0), v_p = P0(2, 0, 1);
+  real f_m = P1(0, 0, -1), f_0 = P1(0, 0, 0), f_p = P1(0, 0, 1);
+  real w_m = P1(3, 0, -1), w_0 = P1(3, 0, 0), w_p = P1(3, 0, 1);
+  real y_0 = P1(2, 0, 0), x_0 = P1(1, 0, 0), x_p = P1(1, 0, 1), z_0 = P0(3, 0, 0);
+  // upper-y quantities of the previous row
+  real sxy_i = 0, sxy_i1 = 0, fyu = 0, gy = 0, syz = 0, fyw = 0;
+  real u_lo0 = 0, u_lop = 0, w_lo = 0, fyw_prev = 0;
 
 #pragma unroll
   for (int t = -1; t < TILE_Y; ++t) {
-    const int r = t + 1;
-    // upper neighbours (row j+1)
-    const real e_01 = P0(0, r + 1, 0), e_p1 = P0(0, r + 1, 1);
-    const real u_01 = P0(1, r + 1, 0), v_01 = P0(2, r + 1, 0);
-    const real e1_01 = P1(0, r + 1, 0), w1_01 = P1(3, r + 1, 0), v1_01 = P1(2, r + 1, 0);
-    // upper y-face quantities of row j
-    const real exy_i1_up = q * (e_0 + e_p + e_01 + e_p1);
-    const real exy_i_up = from_west(exy_i1_up, [&] { return q * (P0(0, r, -1) + e_0 + P0(0, r + 1, -1) + e_01); });
-    const real fyu_up = exy_i_up * ((u_01 - u_0) * dyi + (v_01 - P0(2, r + 1, -1)) * dxi);
-    const real gy_up = e_0 * (v_01 - v_0);
-    const real eyz_up = q * (e_0 + e_01 + e1_0 + e1_01);
-    const real fyw_up = eyz_up * ((w1_01 - w1_0) * dyi + (v1_01 - v_01) * dzhi1);
+    const int rn = t + 2;  // ring row of the north neighbour row
+    const real en_m = P0(0, rn, -1), en_0 = P0(0, rn, 0), en_p = P0(0, rn, 1);
+    const real un_m = P0(1, rn, -1), un_0 = P0(1, rn, 0), un_p = P0(1, rn, 1);
+    const real vn_m = P0(2, rn, -1), vn_0 = P0(2, rn, 0), vn_p = P0(2, rn, 1);
+    const real fn_m = P1(0, rn, -1), fn_0 = P1(0, rn, 0), fn_p = P1(0, rn, 1);
+    const real wn_m = P1(3, rn, -1), wn_0 = P1(3, rn, 0), wn_p = P1(3, rn, 1);
+    const real yn_0 = P1(2, rn, 0), xn_0 = P1(1, rn, 0), xn_p = P1(1, rn, 1), zn_0 = P0(3, rn, 0);
+
+    // upper y-face quantities of this row (4 x the edge viscosities)
+    const real sxy_i_up = e_m + e_0 + en_m + en_0;
+    const real sxy_i1_up = e_0 + e_p + en_0 + en_p;
+    const real fyu_up = sxy_i_up * ((un_0 - u_0) * sy + (vn_0 - vn_m) * sx);
+    const real gy_up = e_0 * (vn_0 - v_0);
+    const real syz_up = e_0 + en_0 + f_0 + fn_0;
+    const real fyw_up = syz_up * ((wn_0 - w_0) * sy + (yn_0 - vn_0) * dzhi1);
 
     if (t >= 0) {
       // z-face quantities at k+1/2 (the prologue needs them too)
-      const real e1_p = P1(0, r, 1), u1_0 = P1(1, r, 0), u1_p = P1(1, r, 1), w1_p = P1(3, r, 1);
-      const real w1_m = P1(3, r, -1);
-      const real exz_i1 = q * (e_0 + e_p + e1_0 + e1_p);
-      const real exz_i = from_west(exz_i1, [&] { return q * (P0(0, r, -1) + e_0 + P1(0, r, -1) + e1_0); });
-      const real fzu = rh1 * exz_i * ((u1_0 - u_0) * dzhi1 + (w1_0 - w1_m) * dxi);
-      const real fzv = rh1 * eyz * ((v1_0 - v_0) * dzhi1 + (w1_0 - w1_lo) * dyi);
-      const real gz = rdz * e_0 * (w1_0 - P0(3, r, 0));
-      const real fxw_p = exz_i1 * ((w1_p - w1_0) * dxi + (u1_p - u_p) * dzhi1);
-      const real fxw_m = from_west(fxw_p, [&] { return exz_i * ((w1_0 - w1_m) * dxi + (u1_0 - u_0) * dzhi1); });
-
+      const real sxz_i = e_m + e_0 + f_m + f_0;
+      const real sxz_i1 = e_0 + e_p + f_0 + f_p;
+      const real fzu = rh1 * sxz_i * ((x_0 - u_0) * dzhi1 + (w_0 - w_m) * sx);
+      const real fzv = rh1 * syz * ((y_0 - v_0) * dzhi1 + (w_0 - w_lo) * sy);
+      const real gz = rdz * e_0 * (w_0 - z_0);
+      const real fxw_p = sxz_i1 * ((w_p - w_0) * sx + (x_p - u_p) * dzhi1);
+      const real fxw_m = sxz_i * ((w_0 - w_m) * sx + (x_0 - u_0) * dzhi1);
       if (OUT) {
-        const real v_p = P0(2, r, 1);
         const real gx_i = e_0 * (u_p - u_0);
-        const real gx_im = from_west(gx_i, [&] { return P0(0, r, -1) * (u_0 - P0(1, r, -1)); });
-        const real fxv_p = exy_i1 * ((v_p - v_0) * dxi + (u_p - u_lop) * dyi);
-        const real fxv_m =
-            from_west(fxv_p, [&] { return exy_i * ((v_0 - P0(2, r, -1)) * dxi + (u_0 - u_lo0) * dyi); });
+        const real gx_im = e_m * (u_0 - u_m);
+        const real fxv_p = sxy_i1 * ((v_p - v_0) * sx + (u_p - u_lop) * sy);
+        const real fxv_m = sxy_i * ((v_0 - v_m) * sx + (u_0 - u_lo0) * sy);
         const real fyw_s = t == 0 ? c.fyw_lo : fyw_prev;  // previous plane's south face of this row
-        store(t, c2x * (gx_i - gx_im) + (fyu_up - fyu) * dyi + (fzu - c.fzu[t]) * fac_uv,
-              (fxv_p - fxv_m) * dxi + c2y * (gy_up - gy) + (fzv - c.fzv[t]) * fac_uv,
-              (c.fxw_p[t] - c.fxw_m[t]) * dxi + (c.fyw_p[t] - fyw_s) * dyi + (gz - c.gz[t]) * fac_w);
+        store(t, c2x * (gx_i - gx_im) + (fyu_up - fyu) * qsy + (fzu - c.fzu[t]) * qfac,
+              (fxv_p - fxv_m) * qsx + c2y * (gy_up - gy) + (fzv - c.fzv[t]) * qfac,
+              (c.fxw_p[t] - c.fxw_m[t]) * qsx + (c.fyw_p[t] - fyw_s) * qsy + (gz - c.gz[t]) * fac_w);
       }
       c.fzu[t] = fzu;
       c.fzv[t] = fzv;
       c.gz[t] = gz;
       c.fxw_m[t] = fxw_m;
+      c.fxw_p[t] = fxw_p;
       if (t == 0) c.fyw_lo = fyw;
       fyw_prev = c.fyw_p[t];  // previous plane's north face of row t = south face of row t+1
       c.fyw_p[t] = fyw_up;
-      c.fxw_p[t] = fxw_p;
     }
 
-    // slide the strip: row j+1 becomes row j
+    // slide the strip: the north row becomes the current row
     u_lo0 = u_0;
     u_lop = u_p;
-    w1_lo = w1_0;
-    exy_i = exy_i_up;
-    exy_i1 = exy_i1_up;
+    w_lo = w_0;
+    sxy_i = sxy_i_up;
+    sxy_i1 = sxy_i1_up;
     fyu = fyu_up;
     gy = gy_up;
-    eyz = eyz_up;
+    syz = syz_up;
     fyw = fyw_up;
-    e_0 = e_01;
-    e_p = e_p1;
-    u_0 = u_01;
-    u_p = P0(1, r + 1, 1);
-    v_0 = v_01;
-    e1_0 = e1_01;
-    w1_0 = w1_01;
-    v1_0 = v1_01;
+    e_m = en_m; e_0 = en_0; e_p = en_p;
+    u_m = un_m; u_0 = un_0; u_p = un_p;
+    v_m = vn_m; v_0 = vn_0; v_p = vn_p;
+    f_m = fn_m; f_0 = fn_0; f_p = fn_p;
+    w_m = wn_m; w_0 = wn_0; w_p = wn_p;
+    y_0 = yn_0; x_0 = xn_0; x_p = xn_p; z_0 = zn_0;
   }
 #undef P0
 #undef P1

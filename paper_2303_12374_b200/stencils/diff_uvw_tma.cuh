@@ -82,21 +82,15 @@ KL_ENTRY(real* __restrict__ ut, real* __restrict__ vt, real* __restrict__ wt, co
   const int kfirst = k0 - 1;                     // first staged plane
 
   // plane p lives in slot (p - kfirst) % kNS; its mbarrier phase is ((p - kfirst) / kNS) & 1
-  auto issue = [&](int p) {
-    const int rel = p - kfirst;
-    unsigned long long* bar = full + rel % kNS;
-    real* dst = ring + (rel % kNS) * kSlot;
+  auto issue = [&](int slot, int p) {
+    unsigned long long* bar = full + slot;
+    real* dst = ring + slot * kSlot;
     kl::mbar_expect_tx(bar, kTxBytes);
 #pragma unroll
     for (int f = 0; f < 4; ++f) kl::tma_load_3d(dst + f * kFS, maps + f, bar, x0, j0 - 1, p);
 #pragma unroll
     for (int f = 0; f < 3; ++f) kl::tma_load_3d(dst + 4 * kFS + f * kTS, maps + 4 + f, bar, xt0, j0, p);
   };
-  auto wait = [&](int p) {
-    const int rel = p - kfirst;
-    kl::mbar_wait(full + rel % kNS, (rel / kNS) & 1);
-  };
-  auto plane = [&](int p) { return ring + ((p - kfirst) % kNS) * kSlot; };
 
   if (tid == 0) {
     for (int s = 0; s < kNS; ++s) kl::mbar_init(full + s, 1);
@@ -104,36 +98,51 @@ KL_ENTRY(real* __restrict__ ut, real* __restrict__ vt, real* __restrict__ wt, co
   }
   __syncthreads();
   if (tid == 0) {
-    for (int p = kfirst; p <= min(kfirst + kNS - 1, k1); ++p) issue(p);
+    for (int p = kfirst; p <= min(kfirst + kNS - 1, k1); ++p) issue(p - kfirst, p);
+  }
+  // per-plane factors of the chunk (one division per plane and block instead
+  // of two per thread and plane; published by the loop's first __syncthreads)
+  real* const zprof = ring + kNS * kSlot;  // [ZCHUNK][5]
+  for (int q = tid; q < k1 - k0; q += KL_THREADS) {
+    const int k = k0 + q;
+    zprof[5 * q + 0] = rhorefh[k + 1];
+    zprof[5 * q + 1] = dzhi[k + 1];
+    zprof[5 * q + 2] = rhoref[k] * dzi[k];
+    zprof[5 * q + 3] = real(0.25) * dzi[k] / rhoref[k];
+    zprof[5 * q + 4] = real(2) * dzhi[k] / rhorefh[k];
   }
 
   const real c2x = real(2) * dxi * dxi;
   const real c2y = real(2) * dyi * dyi;
+  const real qsx = real(0.25) * dxi, qsy = real(0.25) * dyi;
   const int lj0 = threadIdx.y * TILE_Y;
   const int off = lj0 * kBW + threadIdx.x + 1 + cshift;  // (strip row -1, this column) inside a field-plane
   const int i = i0 + threadIdx.x;
   DiffCarry carry;
   auto no_store = [](int, real, real, real) {};
 
-  wait(kfirst);
-  wait(kfirst + 1);
-  diff_step<false, kBW>(plane(kfirst) + off, plane(kfirst + 1) + off, kFS, carry, dxi, dyi, c2x, c2y,
+  kl::mbar_wait(full + 0, 0);  // plane kfirst
+  kl::mbar_wait(full + 1, 0);  // plane k0
+  diff_step<false, kBW>(ring + off, ring + kSlot + off, kFS, carry, dxi, dyi, qsx, qsy, c2x, c2y,
                         rhorefh[k0], dzhi[k0], rhoref[kfirst] * dzi[kfirst], real(0), real(0), no_store);
 
   const int toff = lj0 * kTW + threadIdx.x + tshift;  // (strip row 0, this column) in a tendency plane
+  int sprev = 0, sk = 1, sk1 = 2 % kNS;  // slots of planes k-1, k, k+1
+  unsigned ph1 = 0;                      // barrier parity of plane k+1
   for (int k = k0; k < k1; ++k) {
     __syncthreads();  // everyone is done with plane k-1's slot
     if (tid == 0) {
       const int p = k - 1 + kNS;  // refill the slot plane k-1 vacated
       if (p <= k1) {
         kl::fence_proxy_async_smem();
-        issue(p);
+        issue(sprev, p);
       }
     }
-    wait(k + 1);
-    const real fac_uv = dzi[k] / rhoref[k];
-    const real fac_w = real(2) * dzhi[k] / rhorefh[k];
-    const real* tend = plane(k) + 4 * kFS + toff;
+    kl::mbar_wait(full + sk1, ph1);
+    const real* zp = zprof + 5 * (k - k0);
+    const real* pk = ring + sk * kSlot;
+    const real* pk1 = ring + sk1 * kSlot;
+    const real* tend = pk + 4 * kFS + toff;
     const long long kofs = static_cast<long long>(k) * KL_KK;
     auto store = [&](int t, real dut, real dvt, real dwt) {
       const int j = j0 + lj0 + t;
@@ -144,7 +153,11 @@ KL_ENTRY(real* __restrict__ ut, real* __restrict__ vt, real* __restrict__ wt, co
         wt[ijk] = tend[2 * kTS + t * kTW] + dwt;
       }
     };
-    diff_step<true, kBW>(plane(k) + off, plane(k + 1) + off, kFS, carry, dxi, dyi, c2x, c2y, rhorefh[k + 1],
-                         dzhi[k + 1], rhoref[k] * dzi[k], fac_uv, fac_w, store);
+    diff_step<true, kBW>(pk + off, pk1 + off, kFS, carry, dxi, dyi, qsx, qsy, c2x, c2y, zp[0], zp[1], zp[2], zp[3],
+                         zp[4], store);
+    sprev = sk;
+    sk = sk1;
+    sk1 = sk1 + 1 == kNS ? 0 : sk1 + 1;
+    ph1 ^= sk1 == 0 ? 1u : 0u;
   }
 }

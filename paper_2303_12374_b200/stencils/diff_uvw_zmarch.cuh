@@ -88,6 +88,7 @@ KL_ENTRY(real* __restrict__ ut, real* __restrict__ vt, real* __restrict__ wt, co
 
   const real c2x = real(2) * dxi * dxi;
   const real c2y = real(2) * dyi * dyi;
+  const real qsx = real(0.25) * dxi, qsy = real(0.25) * dyi;
   const int lj0 = threadIdx.y * TILE_Y;  // first strip row (tile-local)
   const int col = threadIdx.x + 1;
   const int i = i0 + threadIdx.x;
@@ -106,7 +107,7 @@ KL_ENTRY(real* __restrict__ ut, real* __restrict__ vt, real* __restrict__ wt, co
     const int kp = k0 - 1;
     const real* p0 = ring + (kp % 3) * SLOT + lj0 * KL_SW + col;
     const real* p1 = ring + ((kp + 1) % 3) * SLOT + lj0 * KL_SW + col;
-    diff_step<false, KL_SW>(p0, p1, FS, carry, dxi, dyi, c2x, c2y, rhorefh[kp + 1], dzhi[kp + 1],
+    diff_step<false, KL_SW>(p0, p1, FS, carry, dxi, dyi, qsx, qsy, c2x, c2y, rhorefh[kp + 1], dzhi[kp + 1],
                             rhoref[kp] * dzi[kp], real(0), real(0), no_store);
   }
   {
@@ -122,7 +123,7 @@ KL_ENTRY(real* __restrict__ ut, real* __restrict__ vt, real* __restrict__ wt, co
     if (more) load_plane(k + 2, buf);  // prefetch; stored after the compute
     const real* p0 = ring + (k % 3) * SLOT + lj0 * KL_SW + col;
     const real* p1 = ring + ((k + 1) % 3) * SLOT + lj0 * KL_SW + col;
-    const real fac_uv = dzi[k] / rhoref[k];
+    const real qfac = real(0.25) * dzi[k] / rhoref[k];
     const real fac_w = real(2) * dzhi[k] / rhorefh[k];
     const long long kofs = static_cast<long long>(k) * KL_KK;
     auto store = [&](int t, real dut, real dvt, real dwt) {
@@ -134,8 +135,8 @@ KL_ENTRY(real* __restrict__ ut, real* __restrict__ vt, real* __restrict__ wt, co
         wt[ijk] += dwt;
       }
     };
-    diff_step<true, KL_SW>(p0, p1, FS, carry, dxi, dyi, c2x, c2y, rhorefh[k + 1], dzhi[k + 1], rhoref[k] * dzi[k],
-                           fac_uv, fac_w, store);
+    diff_step<true, KL_SW>(p0, p1, FS, carry, dxi, dyi, qsx, qsy, c2x, c2y, rhorefh[k + 1], dzhi[k + 1], rhoref[k] * dzi[k],
+                           qfac, fac_w, store);
     if (more) store_plane(k + 2, buf);
   }
 }

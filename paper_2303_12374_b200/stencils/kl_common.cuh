@@ -88,24 +88,28 @@ __device__ __forceinline__ unsigned ceil_div(unsigned a, unsigned b) { return (a
 template <typename T>
 __device__ __forceinline__ T interp2(T a, T b) { return T(0.5) * (a + b); }
 
-// 60 * interp6_ws(a..f): 6th-order centred face value, unscaled.
+__device__ __forceinline__ float fma_(float a, float b, float c) { return fmaf(a, b, c); }
+__device__ __forceinline__ double fma_(double a, double b, double c) { return fma(a, b, c); }
+// 60 * interp6_ws(a..f): 6th-order centred face value, unscaled
+// (pair sums, then two FMAs: 37 (c+d) - 8 (b+e) + (a+f)).
 template <typename T>
 __device__ __forceinline__ T i6x60(T a, T b, T c, T d, T e, T f) {
-  return T(37) * (c + d) - T(8) * (b + e) + (a + f);
+  return fma_(T(37), c + d, fma_(T(-8), b + e, a + f));
 }
-
-// 60 * interp5_ws(a..f): the odd (upwind-correction) part, unscaled.
+// 60 * interp5_ws(a..f): the odd (upwind-correction) part, unscaled
+// (10 (d-c) - 5 (e-b) + (f-a)).
 template <typename T>
 __device__ __forceinline__ T i5x60(T a, T b, T c, T d, T e, T f) {
-  return T(10) * (d - c) - T(5) * (e - b) + (f - a);
+  return fma_(T(10), d - c, fma_(T(-5), e - b, f - a));
 }
-
 // 60 * (vel * interp6_ws - |vel| * interp5_ws): 5th-order upwind flux.
+// Called with vel = interp2(...) it is 60x the MicroHH face flux; the
+// flux-form kernels pass the un-halved velocity SUM and fold the 1/2 into
+// their final scale (120 instead of 60).
 template <typename T>
 __device__ __forceinline__ T flux5x60(T vel, T a, T b, T c, T d, T e, T f) {
   return vel * i6x60(a, b, c, d, e, f) - fabs(vel) * i5x60(a, b, c, d, e, f);
 }
-
 }  // namespace kl
 
 #endif  // KL_COMMON_CUH

@@ -72,7 +72,8 @@ def test_virtual_ranks_match_single_grid(gpu_ctx, tmp_path, kernel, staging):
             got = drv.problem.download(name)[g:g + count]
             want = ref[name][g + off:g + off + count]
             # same configuration everywhere -> identical per-cell arithmetic; allow last-bit
-            # differences from lane-0 recomputation vs shuffled faces at chunk edges
+            # differences where a carried face is evaluated in the prologue instead of the
+            # loop body (FMA contraction may differ between the two)
             err = np.max(np.abs(got - want)) / np.max(np.abs(want))
             assert err <= 1e-13, (drv.rank, name, err)
         assert drv.wisdom.reports and all(r.configuration == cfg for r in drv.wisdom.reports)
@@ -98,3 +99,55 @@ def test_nccl_single_rank_exchange_is_a_noop(gpu_ctx):
     drv.close()
     ex.close()
     assert ver.value >= 22700
+
+
+@pytest.mark.parametrize("kernel", ["advec_u", "diff_uvw"])
+def test_host_streamed_step_matches_device_step(gpu_ctx, tmp_path, kernel):
+    """SlabDriver.step_host (fields in pinned host memory, chunked H2D |
+    launch | D2H on three streams) returns the same tendencies as step() on
+    device-resident fields, and leaves the host inputs untouched."""
+    from paper_2303_12374_b200.cuda import HostPinned, NvrtcCompiler
+    from paper_2303_12374_b200.cuda._abi import check, lib
+    from paper_2303_12374_b200.slab import SlabDriver
+    from paper_2303_12374_b200.stencils.definitions import definition_for
+    from paper_2303_12374_b200.wisdom import WisdomFile, WisdomRecord
+
+    grid, precision = (64, 40, 37), "fp64"
+    d = definition_for(kernel, precision)
+    cfg = d.space.default_config()[0]
+    cfg.update(staging="TMA", zchunk=8, block_x=32, block_y=4, depth=2)
+    WisdomFile(d.kernel_key(), records=[WisdomRecord(gpu_ctx.ident, (1, 1, 1), cfg, 1.0)]).save(
+        tmp_path / f"{d.kernel_key()}.wisdom")
+    drv = SlabDriver(kernel, precision, grid, gpu_ctx, compiler=NvrtcCompiler(gpu_ctx), wisdom_dir=tmp_path)
+    prob, lay = drv.problem, drv.layout
+    nbytes = lay.alloc_bytes
+    host = {}
+    for n in prob.fields:
+        host[n] = HostPinned(nbytes)
+        check(lib().klb_memcpy_dtoh(host[n].ptr, prob.fields[n].ptr, nbytes, None))
+    gpu_ctx.synchronize()
+    before = {n: host[n].array(lay.dtype).copy() for n in host}
+    drv.step()
+    gpu_ctx.synchronize()
+    ref = {n: prob.download(n).copy() for n in prob.outputs()}
+    # scramble the device copies: step_host must bring everything it reads from the host
+    for n, arr in prob.fields.items():
+        check(lib().klb_memset_d8(arr.ptr, 0xFF, nbytes, None))
+    gpu_ctx.synchronize()
+    launches = drv.step_host({n: b.ptr for n, b in host.items()}, chunks=5)
+    drv.compute.synchronize()
+    assert launches == 5
+    h2d, d2h = drv.stream_bytes
+    plane = lay.kk * lay.elem_bytes
+    assert d2h == len(ref) * lay.ktot * plane
+    for n in prob.fields:
+        got = host[n].array(lay.dtype)
+        if n in ref:
+            have, want = lay.interior(lay.host_view(got)), lay.interior(ref[n])
+            err = np.max(np.abs(have - want)) / np.max(np.abs(want))
+            assert err <= 1e-13, (n, err)
+        else:
+            assert np.array_equal(got, before[n]), n
+    for b in host.values():
+        b.free()
+    drv.close()

@@ -132,3 +132,77 @@ def test_tma_repeated_launches_are_stable(gpu_ctx, compiler, kernel):
         got = run_config(gpu_ctx, compiler, kernel, lay, cfg)
         for name in ref:
             assert rel_error(got[name], ref[name], lay) <= TOL["fp32"], name
+
+
+@pytest.mark.parametrize("precision", ["fp32", "fp64"])
+def test_advec_tma_column_tiles_match_oracle(gpu_ctx, compiler, precision):
+    """advec_u TMA with tile_x consecutive columns per thread (vectorised
+    shared-memory reads / ut stores), on grids whose x extent leaves partial
+    thread tiles and partial blocks."""
+    from paper_2303_12374_b200.stencils.layout import GridLayout
+
+    from paper_2303_12374_b200.stencils.definitions import definition_for
+
+    space = definition_for("advec_u", precision).space
+    base = _default("advec_u", precision)
+    cases = [dict(block_x=32, block_y=4, tile_x=2, tile_y=2, depth=2, zchunk=16),
+             dict(block_x=16, block_y=8, tile_x=4, tile_y=1, depth=1, zchunk=8),
+             dict(block_x=16, block_y=2, tile_x=4, tile_y=3, depth=3, zchunk=64),
+             dict(block_x=64, block_y=1, tile_x=2, tile_y=4, depth=1, zchunk=32)]
+    for grid in ((45, 23, 19), (130, 37, 41)):
+        lay = GridLayout(*grid, precision)
+        ref, _ = oracle_outputs("advec_u", lay)
+        for case in cases:
+            cfg = dict(base, staging="TMA", contiguous_x=True, **case)
+            assert space.is_valid(cfg), case
+            got = run_config(gpu_ctx, compiler, "advec_u", lay, cfg)
+            err = rel_error(got["ut"], ref["ut"], lay)
+            assert err <= TOL[precision], (grid, case, err)
+
+
+@pytest.mark.parametrize("precision", ["fp32", "fp64"])
+def test_advec_tma_misaligned_fields_use_scalar_path(gpu_ctx, compiler, precision):
+    """Fields whose interior rows are NOT 16-byte aligned (pointers shifted by
+    one element, as a replayed capture or a foreign allocation may be): the
+    kernel's uniform fallback to scalar shared-memory access must give the
+    same result as the aligned, vectorised path."""
+    from paper_2303_12374_b200.capture import scalar_env_from_args
+    from paper_2303_12374_b200.cuda import DeviceArray, DeviceBuffer
+    from paper_2303_12374_b200.cuda._abi import check, lib
+    from paper_2303_12374_b200.stencils.layout import GridLayout
+    from paper_2303_12374_b200.stencils.problem import StencilProblem
+
+    lay = GridLayout(70, 29, 23, precision)
+    ref, _ = oracle_outputs("advec_u", lay)
+    cfg = dict(_default("advec_u", precision), staging="TMA", contiguous_x=True, block_x=32, block_y=4, tile_x=2,
+               tile_y=2, depth=2, zchunk=8)
+    prob = StencilProblem("advec_u", lay, gpu_ctx)
+    shifted = {}
+    try:
+        args = []
+        for a in prob.args():
+            if isinstance(a, DeviceBuffer) and a.element_count == lay.span_elems:
+                arr = DeviceArray(lay.alloc_bytes + 64)
+                dst = arr.ptr + lay.elem_bytes  # one element off the 16-byte grid
+                check(lib().klb_memcpy_dtod(dst, a.ptr - lay.lead * lay.elem_bytes, lay.alloc_bytes, None))
+                shifted[a.position] = arr
+                a = DeviceBuffer(a.position, a.role, a.element_type, dst + lay.lead * lay.elem_bytes,
+                                 a.element_count, owner=arr)
+            args.append(a)
+        gpu_ctx.synchronize()
+        d = prob.definition
+        env = scalar_env_from_args(args)
+        problem = d.derive_problem_size(env)
+        exe = compiler.compile(d.render_compile_request(cfg, problem, env), gpu_ctx.ident)
+        exe.load()
+        exe.launch(d.derive_geometry(cfg, problem, env), args, timed=True)
+        out = args[0]
+        flat = np.frombuffer(shifted[0].download(lay.alloc_bytes, offset_bytes=lay.elem_bytes), dtype=lay.dtype)
+        got = lay.host_view(flat)
+        assert out.ptr % 16 != (prob.field_ptr("ut") % 16)
+        err = rel_error(got, ref["ut"], lay)
+        assert err <= TOL[precision], err
+    finally:
+        for arr in shifted.values():
+            arr.free()
+        prob.close()

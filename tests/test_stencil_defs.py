@@ -5,7 +5,7 @@ import pytest
 
 from paper_2303_12374_b200.backend import DeviceIdent
 from paper_2303_12374_b200.capture import scalar_env_from_args, ScalarArg
-from paper_2303_12374_b200.stencils.definitions import ARG_LAYOUT, KERNELS, PRECISIONS, definition_for
+from paper_2303_12374_b200.stencils.definitions import ARG_LAYOUT, FAMILY_PINS, KERNELS, PRECISIONS, definition_for
 from paper_2303_12374_b200.stencils.layout import GridLayout
 
 B200 = DeviceIdent("NVIDIA B200", "Blackwell", {"compute_capability": "10.0"})
@@ -60,6 +60,12 @@ def test_nvrtc_compiles_sampled_configs(kernel, precision):
     problem = d.derive_problem_size(env)
     comp = NvrtcCompiler()
     cfgs = d.space.sample_random(3, 3) + [c for c in d.space.sample_random(4, 300) if c["staging"] == "ZMARCH"][:2]
+    for staging, bx in (("ZMARCH", 16), ("TMA", 16), ("TMA", 64)):
+        cfg = d.space.default_config()[0]
+        cfg.update(FAMILY_PINS[staging], tile_x=1, contiguous_x=False, contiguous_y=False, block_x=bx, block_y=4,
+                   zchunk=16, depth=1 if staging == "TMA" else 0)
+        assert d.space.is_valid(cfg), cfg
+        cfgs.append(cfg)
     futures = comp.compile_many([d.render_compile_request(c, problem, env) for c in cfgs], B200)
     for fut in futures:
         img = fut.result()

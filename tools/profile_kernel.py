@@ -20,6 +20,7 @@ def main():
     ap.add_argument("--grid", default="512,512,512")
     ap.add_argument("--config", default="default")
     ap.add_argument("--launches", type=int, default=3)
+    ap.add_argument("--wisdom", default="wisdom")
     a = ap.parse_args()
     from paper_2303_12374_b200.capture import CapturePolicy
     from paper_2303_12374_b200.cuda import NvrtcCompiler, open_device
@@ -35,7 +36,7 @@ def main():
     problem = d.derive_problem_size(env)
     comp = NvrtcCompiler(ctx)
     if a.config == "wisdom":
-        wk = WisdomKernel(d, comp, wisdom_dir="wisdom", capture_policy=CapturePolicy())
+        wk = WisdomKernel(d, comp, wisdom_dir=a.wisdom, capture_policy=CapturePolicy())
         handle, cfg, kind = wk.resolve(ctx.ident, problem, env)
     else:
         cfg = d.space.default_config()[0]

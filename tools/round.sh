@@ -1,7 +1,11 @@
-# tests -> tuning -> bench in one box session
+# tests -> tuning -> bench in one box session.  OUT=gpurun_out/<tag>
 set -x
-timeout 900 python -m pytest tests -q -m gpu -x 2>&1 | tail -5
-OUT=gpurun_out/tune2 timeout 2400 bash tools/tune_all.sh > gpurun_out/tune2_log.txt 2>&1
-tail -3 gpurun_out/tune2_log.txt
-timeout 900 python bench.py --wisdom gpurun_out/tune2/wisdom > gpurun_out/bench2.json 2> gpurun_out/bench2.err
-tail -2 gpurun_out/bench2.err; head -c 600 gpurun_out/bench2.json
+OUT=${OUT:-gpurun_out/round}
+mkdir -p $OUT
+timeout 900 python -m pytest tests -q -m gpu -x > $OUT/pytest.txt 2>&1; rc=$?
+tail -5 $OUT/pytest.txt
+[ $rc = 0 ] || exit $rc
+OUT=$OUT/tune timeout 3000 bash tools/tune_all.sh > $OUT/tune_log.txt 2>&1
+tail -3 $OUT/tune_log.txt
+timeout 900 python bench.py --wisdom $OUT/tune/wisdom > $OUT/bench.json 2> $OUT/bench.err
+tail -2 $OUT/bench.err; head -c 1500 $OUT/bench.json
