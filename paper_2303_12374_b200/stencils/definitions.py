@@ -108,24 +108,32 @@ _ZMARCH_PLANE_LIMIT = {
     "advec_u": "(block_x + 6) * (block_y * tile_y + 6) <= 6144",
     "diff_uvw": "(block_x + 2) * (block_y * tile_y + 2) <= 1024",
 }
+#: opt-in shared memory per block on B200 (cudaDevAttrMaxSharedMemoryPerBlockOptin,
+#: 227 KB); the executor re-checks the live device's value before launching
+SMEM_OPTIN_BYTES = 232448
 #: TMA box extents are <= 256 elements; the smem ring must fit the opt-in limit
 _TMA_LIMIT = {
-    "diff_uvw": ['staging != "TMA" || (block_x <= 128 && (block_x + 6) * (block_y * tile_y + 2) * (depth + 2) <= 2048)'],
-    "advec_u": ['staging != "TMA" || (block_x * tile_x <= 128 && '
-                '(block_x * tile_x + 12) * (block_y * tile_y + 6) * (depth + 4) <= 8192)'],
+    "diff_uvw": ['staging != "TMA" || (block_x * tile_x <= 128 && {SMEM_TMA} <= ' + str(SMEM_OPTIN_BYTES) + ")"],
+    "advec_u": ['staging != "TMA" || (block_x * tile_x <= 128 && {SMEM_TMA} <= ' + str(SMEM_OPTIN_BYTES) + ")"],
 }
 #: knobs the ZMARCH/TMA variants of each kernel fix (pinned to their defaults)
 _ZMARCH_PINNED = {
     # a contiguous y strip; one column per thread, or (TMA) tile_x consecutive columns
     "advec_u": '!unroll_x && !unroll_y && !contiguous_y && '
                '((tile_x == 1 && !contiguous_x) || (staging == "TMA" && tile_x > 1 && contiguous_x))',
-    # one column per thread, a contiguous strip of tile_y rows (flux reuse along y)
-    "diff_uvw": "tile_x == 1 && !unroll_x && !unroll_y && !contiguous_x && !contiguous_y",
+    # a contiguous strip of tile_y rows (flux reuse along y); one column per
+    # thread, or (TMA) tile_x consecutive columns (x-face reuse)
+    "diff_uvw": '!unroll_x && !unroll_y && !contiguous_y && '
+                '((tile_x == 1 && !contiguous_x) || (staging == "TMA" && tile_x > 1 && contiguous_x))',
 }
 
 
 @lru_cache(maxsize=None)
-def stencil_space(kernel: str = "advec_u") -> ConfigSpace:
+def stencil_space(kernel: str = "advec_u", precision: str = "fp32") -> ConfigSpace:
+    """The kernel's space: Table 2 x the B200 knobs, restricted per precision
+    (shared-memory limits depend on the element size, so the fp32 and fp64
+    spaces — and their fingerprints — may differ)."""
+    size = 4 if precision == "fp32" else 8
     params = table2_params() + [
         TunableParam("staging", STAGING_VALUES, "DIRECT"),
         TunableParam("zchunk", ZCHUNK_VALUES, 1),
@@ -141,8 +149,10 @@ def stencil_space(kernel: str = "advec_u") -> ConfigSpace:
         'staging == "DIRECT" || block_x * block_y >= 32',
         # register-resident tiles: the tile loops are always unrolled when marching
         f'staging == "DIRECT" || ({_ZMARCH_PINNED[kernel]})',
-        f'staging == "DIRECT" || ({_ZMARCH_PLANE_LIMIT[kernel]})',
-    ] + _TMA_LIMIT.get(kernel, [])
+        # (diff_uvw's TMA ring is bounded by its own shared-memory restriction below)
+        (f'staging != "ZMARCH" || ({_ZMARCH_PLANE_LIMIT[kernel]})' if kernel == "diff_uvw" else
+         f'staging == "DIRECT" || ({_ZMARCH_PLANE_LIMIT[kernel]})'),
+    ] + [r.replace("{SMEM_TMA}", _SMEM_TMA[kernel].format(S=size)) for r in _TMA_LIMIT.get(kernel, [])]
     return ConfigSpace(params, restrictions)
 
 
@@ -158,10 +168,12 @@ _FAMILY_EXTRA = {
     (kernel, fam): {"tile_x": 1, "contiguous_x": False, "contiguous_y": False}
     for kernel in ("diff_uvw", "advec_u") for fam in ("ZMARCH", "TMA")
 }
-_FAMILY_EXTRA["advec_u", "TMA"] = {"contiguous_y": False}  # tile_x in {1, 2, 4} (consecutive columns)
+# tile_x in {1, 2, 4} (consecutive columns)
+_FAMILY_EXTRA["advec_u", "TMA"] = {"contiguous_y": False}
+_FAMILY_EXTRA["diff_uvw", "TMA"] = {"contiguous_y": False}
 
 
-def family_space(kernel: str, family: str) -> ConfigSpace:
+def family_space(kernel: str, family: str, precision: str = "fp32") -> ConfigSpace:
     """The kernel's space with the family's fixed knobs narrowed to one value.
 
     Every point is valid in (and measured as) the full ``stencil_space`` — the
@@ -170,7 +182,7 @@ def family_space(kernel: str, family: str) -> ConfigSpace:
     reach them.  Tuning runs one session per family and keeps the best in the
     kernel's wisdom file (keep-best append, wisdom.py:151-178).
     """
-    full = stencil_space(kernel)
+    full = stencil_space(kernel, precision)
     pins = dict(FAMILY_PINS[family], **_FAMILY_EXTRA.get((kernel, family), {}))
     params = [TunableParam(p.name, (pins[p.name],), pins[p.name]) if p.name in pins else p for p in full.params]
     return ConfigSpace(params, full.restrictions)
@@ -193,9 +205,10 @@ _BW = "(ceil_div(({X} + {H}) * {S} + 16 - {S}, 16) * 16 / {S})"
 _ADVEC_BOX = "ceil_div(" + _BW + " * (block_y * tile_y + {R}) * {S}, 128) * 128"
 _SMEM_TMA = {
     # plus the chunk's 5 per-plane z factors
-    "diff_uvw": "(256 + (depth + 2) * (4 * ceil_div(" + _BW.format(X="block_x", H=2, S="{S}") +
-                " * (block_y * tile_y + 2) * {S}, 128) * 128 + 3 * ceil_div(" +
-                _BW.format(X="block_x", H=0, S="{S}") + " * (block_y * tile_y) * {S}, 128) * 128) + 5 * zchunk * {S})",
+    # halo'd box kXT + 2 kE wide (kE = 16 / S), tendency box kXT wide (rounded to 16 B)
+    "diff_uvw": "(256 + (depth + 2) * (4 * ceil_div(ceil_div(block_x * tile_x * {S} + 32, 16) * 16"
+                " * (block_y * tile_y + 2), 128) * 128 + 3 * ceil_div(ceil_div(block_x * tile_x * {S}, 16) * 16"
+                " * (block_y * tile_y), 128) * 128) + 5 * zchunk * {S})",
     # advec_u boxes start at column i0-4: u (x halo 4+4, y halo 3+3), v (4 + 1 row), w (4), ut (0)
     # plus the chunk's z factors (2 per plane)
     "advec_u": "(256 + (depth + 4) * (" + " + ".join(
@@ -205,7 +218,7 @@ _SMEM_TMA = {
 
 
 def _definition(kernel: str, precision: str) -> KernelDefinition:
-    space = stencil_space(kernel)
+    space = stencil_space(kernel, precision)
     p = lambda n: f"arg{_pos(kernel, n)}"  # noqa: E731
     size = 4 if precision == "fp32" else 8
     # z extent of one block: block_z*tile_z under DIRECT (zchunk pinned to 1),

@@ -1,45 +1,348 @@
 // diff_uvw_tma.cuh — STAGING == TMA variant of diff_uvw (included by
-// diff_uvw.cu).  Same flux-form plane step as ZMARCH (diff_uvw_flux.cuh), but
-// every operand is fetched by the Tensor Memory Accelerator: one elected
+// diff_uvw.cu).  Flux-form z-march (the reuse scheme of diff_uvw_flux.cuh)
+// with every operand fetched by the Tensor Memory Accelerator: one elected
 // thread issues cp.async.bulk.tensor.3d copies DEPTH planes ahead of the
 // compute into a (DEPTH+2)-slot shared-memory ring, each slot completing on
 // its own mbarrier (expect_tx bytes).  A slot holds plane p of
 //   * evisc, u, v, w with a 1-cell x/y halo (the stencil reads planes k, k+1),
 //   * ut, vt, wt without halo (the read half of the read-modify-write),
-// so the compute warps issue no global loads at all — only the final
-// stores of the updated tendencies.  Staging costs no registers, and DEPTH
-// planes x 7 fields of every block are in flight (ncu on the register-staged
-// ZMARCH variant: long_scoreboard-bound at 25% occupancy).  Box starts are
-// rounded down to 16-byte aligned x (TMA faults otherwise); out-of-box
-// rows/columns are zero-filled and only feed cells that are never stored.
+// so the compute warps issue no global loads — only the final stores of the
+// updated tendencies.  Staging costs no registers, and DEPTH planes x 7
+// fields of every block are in flight.
+//
+// A thread owns TILE_X consecutive columns (TILE_X in {1, 2, 4}; CONTIG_X)
+// times a strip of TILE_Y rows.  Every face quantity of A.3 is evaluated
+// once per thread: x-faces (the x fluxes, the xy/xz edge viscosities) TILE_X+1
+// times per row for TILE_X cells, y-faces carried from the row below, z-faces
+// carried from the plane below.  Halo'd boxes start at column i0-kE (kE =
+// elements per 16 bytes), so when column i0 is 16-byte aligned in every field
+// (always, for GridLayout pitches) a thread's cells sit at vector-aligned
+// shared offsets: a row of TILE_X+2 values is TILE_X/VA + 2 loads of VA
+// elements (VA = min(TILE_X, kE)), and the tendency reads and stores are
+// VA-wide too.  A uniform branch falls back to scalar shared reads (and
+// global tendency reads) for any other alignment.  Out-of-box rows/columns
+// are zero-filled by TMA and only feed cells that are never stored.
 
-#if BLOCK_Z != 1 || TILE_Z != 1 || TILE_X != 1
-#error "diff_uvw TMA requires BLOCK_Z == TILE_Z == TILE_X == 1"
+#if BLOCK_Z != 1 || TILE_Z != 1
+#error "diff_uvw TMA requires BLOCK_Z == TILE_Z == 1"
+#endif
+#if TILE_X != 1 && TILE_X != 2 && TILE_X != 4
+#error "diff_uvw TMA requires TILE_X in {1, 2, 4}"
+#endif
+#if TILE_X > 1 && !CONTIG_X
+#error "diff_uvw TMA: TILE_X > 1 needs consecutive columns (CONTIG_X)"
 #endif
 #ifndef DEPTH
 #define DEPTH 2
 #endif
 
-#include "diff_uvw_flux.cuh"
 #include "kl_tma.cuh"
 
 namespace {
 constexpr int kS = static_cast<int>(sizeof(real));
 constexpr int kE = 16 / kS;  // elements per 16 bytes
-constexpr int kTYT = BLOCK_Y * TILE_Y;
-// halo'd box: BLOCK_X + 2 columns plus up to kE-1 alignment columns, 16-B multiple
-constexpr int kBW = (((BLOCK_X + 2) * kS + 16 - kS + 15) / 16) * 16 / kS;
+constexpr int kTX = TILE_X, kTY = TILE_Y;
+constexpr int kXT = BLOCK_X * kTX;   // columns per block
+constexpr int kTYT = BLOCK_Y * kTY;  // rows per block
+constexpr int kVA = kTX < kE ? kTX : kE;
+__host__ __device__ constexpr int rup(int a, int b) { return (a + b - 1) / b * b; }
+// halo'd box: columns from (i0 - kE) rounded down to 16 B, kXT + 2 kE wide
+constexpr int kBW = rup(kXT + 2 * kE, kE);
 constexpr int kBH = kTYT + 2;
-// tendency box: BLOCK_X columns (+ alignment slack), no halo
-constexpr int kTW = ((BLOCK_X * kS + 16 - kS + 15) / 16) * 16 / kS;
-constexpr int kFSB = ((kBW * kBH * kS + 127) / 128) * 128;   // bytes per halo'd field-plane
-constexpr int kTSB = ((kTW * kTYT * kS + 127) / 128) * 128;  // bytes per tendency field-plane
+constexpr int kTW = rup(kXT, kE);  // tendency box: columns i0 .. i0+kXT-1 (start rounded down)
+constexpr int kFSB = rup(kBW * kBH * kS, 128);   // bytes per halo'd field-plane
+constexpr int kTSB = rup(kTW * kTYT * kS, 128);  // bytes per tendency field-plane
 constexpr int kFS = kFSB / kS;
 constexpr int kTS = kTSB / kS;
 constexpr int kSlot = 4 * kFS + 3 * kTS;
 constexpr int kNS = DEPTH + 2;
 constexpr unsigned kTxBytes = 4u * kBW * kBH * kS + 3u * kTW * kTYT * kS;
 static_assert(kBW <= 256 && kBH <= 256 && kTW <= 256, "TMA box extents are limited to 256");
+
+template <int N>
+struct __align__(N * sizeof(real)) Pack {
+  real v[N];
+};
+
+// d[m] = s[m - 1] for m in [0, kTX + 2): columns -1 .. kTX of a thread's cells
+// (s points at its first column; VA-element aligned when VA > 1).
+template <int VA>
+__device__ __forceinline__ void ld_row(real (&d)[kTX + 2], const real* s) {
+  if (VA == 1) {
+#pragma unroll
+    for (int m = 0; m < kTX + 2; ++m) d[m] = s[m - 1];
+  } else {
+    real b[kTX + 2 * VA];
+#pragma unroll
+    for (int e = 0; e < kTX + 2 * VA; e += VA) {
+      const Pack<VA> p = *reinterpret_cast<const Pack<VA>*>(s - VA + e);
+#pragma unroll
+      for (int q = 0; q < VA; ++q) b[e + q] = p.v[q];
+    }
+#pragma unroll
+    for (int m = 0; m < kTX + 2; ++m) d[m] = b[VA - 1 + m];
+  }
+}
+
+// d[m] = s[m] for m in [0, N), N in {kTX, kTX + 1}
+template <int VA, int N>
+__device__ __forceinline__ void ld_span(real (&d)[N], const real* s) {
+  if (VA == 1) {
+#pragma unroll
+    for (int m = 0; m < N; ++m) d[m] = s[m];
+  } else {
+    constexpr int R = rup(N, VA);
+    real b[R];
+#pragma unroll
+    for (int e = 0; e < R; e += VA) {
+      const Pack<VA> p = *reinterpret_cast<const Pack<VA>*>(s + e);
+#pragma unroll
+      for (int q = 0; q < VA; ++q) b[e + q] = p.v[q];
+    }
+#pragma unroll
+    for (int m = 0; m < N; ++m) d[m] = b[m];
+  }
+}
+
+// One shared-memory row of the strip: e/u/v at plane k, f = evisc, w,
+// y = v, x = u at plane k+1, z = w at plane k; index m <-> column m-1 for the
+// (kTX+2)-wide rows, column m for y, x (kTX+1 wide) and z.
+struct Row {
+  real e[kTX + 2], u[kTX + 2], v[kTX + 2], f[kTX + 2], w[kTX + 2];
+  real y[kTX], x[kTX + 1], z[kTX];
+};
+
+// Quantities on the z-face k+1/2 carried to the next plane (per strip row
+// and column; FXW per x-face).  The south y-face flux of w at row t is the
+// north one of row t-1, so only the strip's lowest (fyw_lo) is stored apart.
+struct Carry {
+  real fzu[kTY][kTX], fzv[kTY][kTX], gz[kTY][kTX], fyw_p[kTY][kTX];
+  real fxw[kTY][kTX + 1];
+  real fyw_lo[kTX];
+};
+
+struct Scales {
+  real sx, sy, qsx, qsy, c2x, c2y;
+};
+
+// Per-plane factors: rh1 = rhorefh[k+1], dzhi1 = dzhi[k+1], rdz =
+// rhoref[k]*dzi[k], qfac = dzi[k]/(4 rhoref[k]), fac_w = 2 dzhi[k]/rhorefh[k].
+struct PlaneFactors {
+  real rh1, dzhi1, rdz, qfac, fac_w;
+};
+
+// One plane step.  h0/h1: plane k / k+1 slots, pointing at (strip row -1,
+// first column) of field 0 with field f at +hof[f]; with OUT=false only the
+// carried upper-z quantities are produced (the prologue at plane k0-1).
+template <bool OUT, int VA, class Store>
+__device__ __forceinline__ void plane_step(const real* h0, const real* h1, const int (&hof)[4], Carry& c,
+                                           const Scales& s, const PlaneFactors& z, Store&& store) {
+  Row cur, nrt;
+  auto load = [&](Row& r, int row) {
+    const int ro = row * kBW;
+    ld_row<VA>(r.e, h0 + hof[0] + ro);
+    ld_row<VA>(r.u, h0 + hof[1] + ro);
+    ld_row<VA>(r.v, h0 + hof[2] + ro);
+    ld_row<VA>(r.f, h1 + hof[0] + ro);
+    ld_row<VA>(r.w, h1 + hof[3] + ro);
+    ld_span<VA, kTX>(r.y, h1 + hof[2] + ro);
+    ld_span<VA, kTX + 1>(r.x, h1 + hof[1] + ro);
+    ld_span<VA, kTX>(r.z, h0 + hof[3] + ro);
+  };
+  load(cur, 0);
+  // y-face quantities of the current row's lower face (from the previous row)
+  real sxy[kTX + 1], fyu[kTX], gy[kTX], syz[kTX], fyw[kTX], ulo[kTX + 1], wlo[kTX], fyw_prev[kTX];
+#pragma unroll
+  for (int q = 0; q < kTX; ++q) fyw_prev[q] = real(0);
+
+#pragma unroll
+  for (int t = -1; t < kTY; ++t) {
+    load(nrt, t + 2);
+    // upper y-face quantities of this row (4 x the edge viscosities)
+    real sxy_up[kTX + 1], fyu_up[kTX], gy_up[kTX], syz_up[kTX], fyw_up[kTX];
+#pragma unroll
+    for (int f = 0; f <= kTX; ++f) sxy_up[f] = (cur.e[f] + cur.e[f + 1]) + (nrt.e[f] + nrt.e[f + 1]);
+#pragma unroll
+    for (int q = 0; q < kTX; ++q) {
+      fyu_up[q] = sxy_up[q] * ((nrt.u[q + 1] - cur.u[q + 1]) * s.sy + (nrt.v[q + 1] - nrt.v[q]) * s.sx);
+      gy_up[q] = cur.e[q + 1] * (nrt.v[q + 1] - cur.v[q + 1]);
+      syz_up[q] = (cur.e[q + 1] + nrt.e[q + 1]) + (cur.f[q + 1] + nrt.f[q + 1]);
+      fyw_up[q] = syz_up[q] * ((nrt.w[q + 1] - cur.w[q + 1]) * s.sy + (nrt.y[q] - nrt.v[q + 1]) * z.dzhi1);
+    }
+
+    if (t >= 0) {
+      // x-faces f (between columns f-1 and f) of the xz edge viscosity and w's x flux
+      real sxz[kTX + 1], fxw[kTX + 1];
+#pragma unroll
+      for (int f = 0; f <= kTX; ++f) {
+        sxz[f] = (cur.e[f] + cur.e[f + 1]) + (cur.f[f] + cur.f[f + 1]);
+        fxw[f] = sxz[f] * ((cur.w[f + 1] - cur.w[f]) * s.sx + (cur.x[f] - cur.u[f + 1]) * z.dzhi1);
+      }
+      real fzu[kTX], fzv[kTX], gz[kTX];
+#pragma unroll
+      for (int q = 0; q < kTX; ++q) {
+        fzu[q] = z.rh1 * sxz[q] * ((cur.x[q] - cur.u[q + 1]) * z.dzhi1 + (cur.w[q + 1] - cur.w[q]) * s.sx);
+        fzv[q] = z.rh1 * syz[q] * ((cur.y[q] - cur.v[q + 1]) * z.dzhi1 + (cur.w[q + 1] - wlo[q]) * s.sy);
+        gz[q] = z.rdz * cur.e[q + 1] * (cur.w[q + 1] - cur.z[q]);
+      }
+      if (OUT) {
+        real gx[kTX + 1], fxv[kTX + 1];
+#pragma unroll
+        for (int f = 0; f <= kTX; ++f) {
+          gx[f] = cur.e[f] * (cur.u[f + 1] - cur.u[f]);
+          fxv[f] = sxy[f] * ((cur.v[f + 1] - cur.v[f]) * s.sx + (cur.u[f + 1] - ulo[f]) * s.sy);
+        }
+        real dut[kTX], dvt[kTX], dwt[kTX];
+#pragma unroll
+        for (int q = 0; q < kTX; ++q) {
+          const real fyw_s = t == 0 ? c.fyw_lo[q] : fyw_prev[q];  // previous plane's south face of this row
+          dut[q] = s.c2x * (gx[q + 1] - gx[q]) + (fyu_up[q] - fyu[q]) * s.qsy + (fzu[q] - c.fzu[t][q]) * z.qfac;
+          dvt[q] = (fxv[q + 1] - fxv[q]) * s.qsx + s.c2y * (gy_up[q] - gy[q]) + (fzv[q] - c.fzv[t][q]) * z.qfac;
+          dwt[q] = (c.fxw[t][q + 1] - c.fxw[t][q]) * s.qsx + (c.fyw_p[t][q] - fyw_s) * s.qsy +
+                   (gz[q] - c.gz[t][q]) * z.fac_w;
+        }
+        store(t, dut, dvt, dwt);
+      }
+#pragma unroll
+      for (int q = 0; q < kTX; ++q) {
+        c.fzu[t][q] = fzu[q];
+        c.fzv[t][q] = fzv[q];
+        c.gz[t][q] = gz[q];
+        if (t == 0) c.fyw_lo[q] = fyw[q];
+        fyw_prev[q] = c.fyw_p[t][q];  // previous plane's north face of row t = south face of row t+1
+        c.fyw_p[t][q] = fyw_up[q];
+      }
+#pragma unroll
+      for (int f = 0; f <= kTX; ++f) c.fxw[t][f] = fxw[f];
+    }
+
+    // slide the strip: the north row becomes the current row
+#pragma unroll
+    for (int f = 0; f <= kTX; ++f) {
+      ulo[f] = cur.u[f + 1];
+      sxy[f] = sxy_up[f];
+    }
+#pragma unroll
+    for (int q = 0; q < kTX; ++q) {
+      wlo[q] = cur.w[q + 1];
+      fyu[q] = fyu_up[q];
+      gy[q] = gy_up[q];
+      syz[q] = syz_up[q];
+      fyw[q] = fyw_up[q];
+    }
+    cur = nrt;
+  }
+}
+
+// Per-block state of the march (member template instead of a generic lambda:
+// NVRTC has no extended device lambdas).
+struct DiffTma {
+  real *ut, *vt, *wt;
+  const real* zprof;  // [ZCHUNK][5] per-plane factors
+  real* ring;
+  unsigned long long* full;
+  const TmaDesc* maps;
+  Scales sc;
+  PlaneFactors pro;  // factors of the prologue plane k0-1
+  int j0, k0, k1, tid, iend, jend, ic, lj0;
+  int xh[4], xt;  // 16-byte aligned box starts (halo'd fields / tendencies)
+  int hof[4];     // (strip row -1, column ic) of each halo'd field inside a slot
+  int tofs;       // (strip row 0, column ic) inside a tendency plane
+
+  __device__ __forceinline__ void issue(int slot, int p) const {
+    unsigned long long* bar = full + slot;
+    real* dst = ring + slot * kSlot;
+    kl::mbar_expect_tx(bar, kTxBytes);
+#pragma unroll
+    for (int f = 0; f < 4; ++f) kl::tma_load_3d(dst + f * kFS, maps + f, bar, xh[f], j0 - 1, p);
+#pragma unroll
+    for (int f = 0; f < 3; ++f) kl::tma_load_3d(dst + 4 * kFS + f * kTS, maps + 4 + f, bar, xt, j0, p);
+  }
+
+  template <int VA>
+  __device__ __forceinline__ void march() const {
+    Carry carry;
+    auto no_store = [](int, const real(&)[kTX], const real(&)[kTX], const real(&)[kTX]) {};
+    const int kfirst = k0 - 1;
+    kl::mbar_wait(full + 0, 0);  // plane kfirst
+    kl::mbar_wait(full + 1, 0);  // plane k0
+    plane_step<false, VA>(ring, ring + kSlot, hof, carry, sc, pro, no_store);
+
+    int sprev = 0, sk = 1, sk1 = 2 % kNS;  // slots of planes k-1, k, k+1
+    unsigned ph1 = 0;                      // barrier parity of plane k+1
+    for (int k = k0; k < k1; ++k) {
+      __syncthreads();  // everyone is done with plane k-1's slot
+      if (tid == 0) {
+        const int p = k - 1 + kNS;  // refill the slot plane k-1 vacated
+        if (p <= k1) {
+          kl::fence_proxy_async_smem();
+          issue(sprev, p);
+        }
+      }
+      kl::mbar_wait(full + sk1, ph1);
+      const real* zp = zprof + 5 * (k - k0);
+      const PlaneFactors pf{zp[0], zp[1], zp[2], zp[3], zp[4]};
+      const real* pk = ring + sk * kSlot;
+      const real* pk1 = ring + sk1 * kSlot;
+      const real* tend = pk + 4 * kFS + tofs;
+      const long long kofs = static_cast<long long>(k) * KL_KK;
+      auto store = [&](int t, const real(&dut)[kTX], const real(&dvt)[kTX], const real(&dwt)[kTX]) {
+        const int j = j0 + lj0 + t;
+        if (j >= jend) return;
+        const long long ijk = ic + static_cast<long long>(j) * KL_JJ + kofs;
+        real o[3][kTX];
+        if (VA > 1) {
+          ld_span<VA, kTX>(o[0], tend + t * kTW);
+          ld_span<VA, kTX>(o[1], tend + kTS + t * kTW);
+          ld_span<VA, kTX>(o[2], tend + 2 * kTS + t * kTW);
+        } else {  // unaligned layout: the tendency boxes may not cover the columns
+#pragma unroll
+          for (int q = 0; q < kTX; ++q) {
+            const bool in = ic + q < iend;
+            o[0][q] = in ? ut[ijk + q] : real(0);
+            o[1][q] = in ? vt[ijk + q] : real(0);
+            o[2][q] = in ? wt[ijk + q] : real(0);
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < kTX; ++q) {
+          o[0][q] += dut[q];
+          o[1][q] += dvt[q];
+          o[2][q] += dwt[q];
+        }
+        if (VA > 1 && ic + kTX <= iend) {
+#pragma unroll
+          for (int e = 0; e < kTX; e += VA) {
+            Pack<VA> a, b, d;
+#pragma unroll
+            for (int q = 0; q < VA; ++q) {
+              a.v[q] = o[0][e + q];
+              b.v[q] = o[1][e + q];
+              d.v[q] = o[2][e + q];
+            }
+            *reinterpret_cast<Pack<VA>*>(ut + ijk + e) = a;
+            *reinterpret_cast<Pack<VA>*>(vt + ijk + e) = b;
+            *reinterpret_cast<Pack<VA>*>(wt + ijk + e) = d;
+          }
+        } else {
+#pragma unroll
+          for (int q = 0; q < kTX; ++q) {
+            if (ic + q < iend) {
+              ut[ijk + q] = o[0][q];
+              vt[ijk + q] = o[1][q];
+              wt[ijk + q] = o[2][q];
+            }
+          }
+        }
+      };
+      plane_step<true, VA>(pk, pk1, hof, carry, sc, pf, store);
+      sprev = sk;
+      sk = sk1;
+      sk1 = sk1 + 1 == kNS ? 0 : sk1 + 1;
+      ph1 ^= sk1 == 0 ? 1u : 0u;
+    }
+  }
+};
 }  // namespace
 
 // positions: ut=0 vt=1 wt=2 evisc=3 u=4 v=5 w=6, jj=13 kk=14 (definitions.ARG_LAYOUT["diff_uvw"])
@@ -55,42 +358,60 @@ KL_ENTRY(real* __restrict__ ut, real* __restrict__ vt, real* __restrict__ wt, co
          const real* __restrict__ u, const real* __restrict__ v, const real* __restrict__ w,
          const real* __restrict__ dzi, const real* __restrict__ dzhi, const real* __restrict__ rhoref,
          const real* __restrict__ rhorefh, const real dxi, const real dyi, const int jj, const int kk,
-         const int istart, const int jstart, const int kstart, const int iend, const int jend, const int kend, const __grid_constant__ KlTmaParams tma) {
+         const int istart, const int jstart, const int kstart, const int iend, const int jend, const int kend,
+         const __grid_constant__ KlTmaParams tma) {
   if (jj != KL_JJ || kk != KL_KK) __trap();
-  // param-space address of the descriptors (__grid_constant__: no local copy)
-  const TmaDesc* const maps = &tma.map[0];
   extern __shared__ __align__(128) unsigned char kl_smem_raw[];
   unsigned char* base = kl_smem_raw + ((128u - (kl::smem_u32(kl_smem_raw) & 127u)) & 127u);
   unsigned long long* full = reinterpret_cast<unsigned long long*>(base);  // kNS mbarriers
-  real* const ring = reinterpret_cast<real*>(base + 128);                  // [kNS][4][kFS]
+  real* const ring = reinterpret_cast<real*>(base + 128);                  // [kNS][kSlot]
 
-  const unsigned nbx = kl::ceil_div(iend - istart, BLOCK_X);
+  const unsigned nbx = kl::ceil_div(iend - istart, kXT);
   const unsigned nby = kl::ceil_div(jend - jstart, kTYT);
   const unsigned nbz = kl::ceil_div(kend - kstart, ZCHUNK);
   int bx, by, bz;
   kl::unravel(blockIdx.x, nbx, nby, nbz, bx, by, bz);
-  const int i0 = istart + bx * BLOCK_X;
-  const int j0 = jstart + by * kTYT;
-  const int k0 = kstart + bz * ZCHUNK;
-  const int k1 = min(k0 + ZCHUNK, kend);
+  const int i0 = istart + bx * kXT;
   const int tid = threadIdx.x + threadIdx.y * BLOCK_X;
-  const int xfirst = i0 - 1 + kl::tma_xoff(evisc);  // tensor x of column i0-1 (all fields share the layout)
-  const int x0 = xfirst & ~(kE - 1);               // 16-byte aligned box start
-  const int cshift = xfirst - x0;                  // extra leading columns in the tile
-  const int xt0 = (xfirst + 1) & ~(kE - 1);        // tendency box start (column i0)
-  const int tshift = xfirst + 1 - xt0;
-  const int kfirst = k0 - 1;                     // first staged plane
 
-  // plane p lives in slot (p - kfirst) % kNS; its mbarrier phase is ((p - kfirst) / kNS) & 1
-  auto issue = [&](int slot, int p) {
-    unsigned long long* bar = full + slot;
-    real* dst = ring + slot * kSlot;
-    kl::mbar_expect_tx(bar, kTxBytes);
+  DiffTma m;
+  m.ut = ut;
+  m.vt = vt;
+  m.wt = wt;
+  m.ring = ring;
+  m.full = full;
+  m.maps = &tma.map[0];  // param-space address of the descriptors (__grid_constant__: no local copy)
+  m.j0 = jstart + by * kTYT;
+  m.k0 = kstart + bz * ZCHUNK;
+  m.k1 = min(m.k0 + ZCHUNK, kend);
+  m.tid = tid;
+  m.iend = iend;
+  m.jend = jend;
+  m.ic = i0 + kTX * static_cast<int>(threadIdx.x);
+  m.lj0 = threadIdx.y * kTY;
+  // box starts: tensor x of column i0-kE (halo'd) / i0 (tendencies) rounded
+  // down to 16 B (each base pointer may carry its own sub-16-byte offset,
+  // tma_xoff); the fast path needs column i0 at box column kE (halo'd) / 0
+  const real* hp[4] = {evisc, u, v, w};
+  const int xt = i0 + kl::tma_xoff(ut);
+  m.xt = xt & ~(kE - 1);
+  bool aligned = xt == m.xt && kl::tma_xoff(vt) == kl::tma_xoff(ut) && kl::tma_xoff(wt) == kl::tma_xoff(ut);
 #pragma unroll
-    for (int f = 0; f < 4; ++f) kl::tma_load_3d(dst + f * kFS, maps + f, bar, x0, j0 - 1, p);
-#pragma unroll
-    for (int f = 0; f < 3; ++f) kl::tma_load_3d(dst + 4 * kFS + f * kTS, maps + 4 + f, bar, xt0, j0, p);
-  };
+  for (int f = 0; f < 4; ++f) {
+    const int x = i0 - kE + kl::tma_xoff(hp[f]);
+    m.xh[f] = x & ~(kE - 1);
+    aligned = aligned && x == m.xh[f];
+    m.hof[f] = f * kFS + m.lj0 * kBW + (x - m.xh[f]) + kE + kTX * static_cast<int>(threadIdx.x);
+  }
+  m.tofs = m.lj0 * kTW + (xt - m.xt) + kTX * static_cast<int>(threadIdx.x);
+  m.sc.sx = dxi;
+  m.sc.sy = dyi;
+  m.sc.qsx = real(0.25) * dxi;
+  m.sc.qsy = real(0.25) * dyi;
+  m.sc.c2x = real(2) * dxi * dxi;
+  m.sc.c2y = real(2) * dyi * dyi;
+  const int kfirst = m.k0 - 1;
+  m.pro = PlaneFactors{rhorefh[m.k0], dzhi[m.k0], rhoref[kfirst] * dzi[kfirst], real(0), real(0)};
 
   if (tid == 0) {
     for (int s = 0; s < kNS; ++s) kl::mbar_init(full + s, 1);
@@ -98,66 +419,23 @@ KL_ENTRY(real* __restrict__ ut, real* __restrict__ vt, real* __restrict__ wt, co
   }
   __syncthreads();
   if (tid == 0) {
-    for (int p = kfirst; p <= min(kfirst + kNS - 1, k1); ++p) issue(p - kfirst, p);
+    for (int p = kfirst; p <= min(kfirst + kNS - 1, m.k1); ++p) m.issue(p - kfirst, p);
   }
   // per-plane factors of the chunk (one division per plane and block instead
-  // of two per thread and plane; published by the loop's first __syncthreads)
+  // of two per thread and plane; published by the march's first __syncthreads)
   real* const zprof = ring + kNS * kSlot;  // [ZCHUNK][5]
-  for (int q = tid; q < k1 - k0; q += KL_THREADS) {
-    const int k = k0 + q;
+  for (int q = tid; q < m.k1 - m.k0; q += KL_THREADS) {
+    const int k = m.k0 + q;
     zprof[5 * q + 0] = rhorefh[k + 1];
     zprof[5 * q + 1] = dzhi[k + 1];
     zprof[5 * q + 2] = rhoref[k] * dzi[k];
     zprof[5 * q + 3] = real(0.25) * dzi[k] / rhoref[k];
     zprof[5 * q + 4] = real(2) * dzhi[k] / rhorefh[k];
   }
-
-  const real c2x = real(2) * dxi * dxi;
-  const real c2y = real(2) * dyi * dyi;
-  const real qsx = real(0.25) * dxi, qsy = real(0.25) * dyi;
-  const int lj0 = threadIdx.y * TILE_Y;
-  const int off = lj0 * kBW + threadIdx.x + 1 + cshift;  // (strip row -1, this column) inside a field-plane
-  const int i = i0 + threadIdx.x;
-  DiffCarry carry;
-  auto no_store = [](int, real, real, real) {};
-
-  kl::mbar_wait(full + 0, 0);  // plane kfirst
-  kl::mbar_wait(full + 1, 0);  // plane k0
-  diff_step<false, kBW>(ring + off, ring + kSlot + off, kFS, carry, dxi, dyi, qsx, qsy, c2x, c2y,
-                        rhorefh[k0], dzhi[k0], rhoref[kfirst] * dzi[kfirst], real(0), real(0), no_store);
-
-  const int toff = lj0 * kTW + threadIdx.x + tshift;  // (strip row 0, this column) in a tendency plane
-  int sprev = 0, sk = 1, sk1 = 2 % kNS;  // slots of planes k-1, k, k+1
-  unsigned ph1 = 0;                      // barrier parity of plane k+1
-  for (int k = k0; k < k1; ++k) {
-    __syncthreads();  // everyone is done with plane k-1's slot
-    if (tid == 0) {
-      const int p = k - 1 + kNS;  // refill the slot plane k-1 vacated
-      if (p <= k1) {
-        kl::fence_proxy_async_smem();
-        issue(sprev, p);
-      }
-    }
-    kl::mbar_wait(full + sk1, ph1);
-    const real* zp = zprof + 5 * (k - k0);
-    const real* pk = ring + sk * kSlot;
-    const real* pk1 = ring + sk1 * kSlot;
-    const real* tend = pk + 4 * kFS + toff;
-    const long long kofs = static_cast<long long>(k) * KL_KK;
-    auto store = [&](int t, real dut, real dvt, real dwt) {
-      const int j = j0 + lj0 + t;
-      if (i < iend && j < jend) {
-        const long long ijk = i + static_cast<long long>(j) * KL_JJ + kofs;
-        ut[ijk] = tend[t * kTW] + dut;
-        vt[ijk] = tend[kTS + t * kTW] + dvt;
-        wt[ijk] = tend[2 * kTS + t * kTW] + dwt;
-      }
-    };
-    diff_step<true, kBW>(pk + off, pk1 + off, kFS, carry, dxi, dyi, qsx, qsy, c2x, c2y, zp[0], zp[1], zp[2], zp[3],
-                         zp[4], store);
-    sprev = sk;
-    sk = sk1;
-    sk1 = sk1 + 1 == kNS ? 0 : sk1 + 1;
-    ph1 ^= sk1 == 0 ? 1u : 0u;
+  m.zprof = zprof;
+  if (kVA > 1 && aligned) {
+    m.march<kVA>();
+  } else {
+    m.march<1>();
   }
 }

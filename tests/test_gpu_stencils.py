@@ -61,7 +61,7 @@ def _sample_configs(kernel, precision, n, seed):
     space = definition_for(kernel, precision).space
     cfgs = []
     for fam in FAMILY_PINS:
-        for c in family_space(kernel, fam).sample_random(seed, n):
+        for c in family_space(kernel, fam, precision).sample_random(seed, n):
             assert space.is_valid(c)
             cfgs.append(c)
     return cfgs
@@ -161,7 +161,41 @@ def test_advec_tma_column_tiles_match_oracle(gpu_ctx, compiler, precision):
 
 
 @pytest.mark.parametrize("precision", ["fp32", "fp64"])
-def test_advec_tma_misaligned_fields_use_scalar_path(gpu_ctx, compiler, precision):
+def test_diff_tma_column_tiles_match_oracle(gpu_ctx, compiler, precision):
+    """diff_uvw TMA with tile_x consecutive columns per thread (x-face reuse,
+    vectorised shared-memory reads and tendency stores), on grids whose x/y
+    extents leave partial thread tiles and partial blocks."""
+    from paper_2303_12374_b200.stencils.definitions import definition_for
+    from paper_2303_12374_b200.stencils.layout import GridLayout
+
+    space = definition_for("diff_uvw", precision).space
+    base = _default("diff_uvw", precision)
+    cases = [dict(block_x=32, block_y=4, tile_x=2, tile_y=2, depth=2, zchunk=16, contiguous_x=True),
+             dict(block_x=16, block_y=8, tile_x=4, tile_y=1, depth=1, zchunk=8, contiguous_x=True),
+             dict(block_x=16, block_y=2, tile_x=4, tile_y=4, depth=3, zchunk=64, contiguous_x=True),
+             dict(block_x=64, block_y=2, tile_x=1, tile_y=4, depth=1, zchunk=32, unravel="XYZ"),
+             dict(block_x=128, block_y=2, tile_x=1, tile_y=4, depth=1, zchunk=64, unravel="XYZ")]
+    for grid in ((45, 23, 19), (130, 37, 41)):
+        lay = GridLayout(*grid, precision)
+        ref, _ = oracle_outputs("diff_uvw", lay)
+        for case in cases:
+            cfg = dict(base, staging="TMA", **case)
+            assert space.is_valid(cfg), case
+            got = run_config(gpu_ctx, compiler, "diff_uvw", lay, cfg)
+            for name in ref:
+                err = rel_error(got[name], ref[name], lay)
+                assert err <= TOL[precision], (grid, case, name, err)
+
+
+_MISALIGNED_CFG = {
+    "advec_u": dict(staging="TMA", contiguous_x=True, block_x=32, block_y=4, tile_x=2, tile_y=2, depth=2, zchunk=8),
+    "diff_uvw": dict(staging="TMA", contiguous_x=True, block_x=16, block_y=4, tile_x=4, tile_y=2, depth=2, zchunk=8),
+}
+
+
+@pytest.mark.parametrize("kernel", ["advec_u", "diff_uvw"])
+@pytest.mark.parametrize("precision", ["fp32", "fp64"])
+def test_tma_misaligned_fields_use_scalar_path(gpu_ctx, compiler, kernel, precision):
     """Fields whose interior rows are NOT 16-byte aligned (pointers shifted by
     one element, as a replayed capture or a foreign allocation may be): the
     kernel's uniform fallback to scalar shared-memory access must give the
@@ -173,10 +207,9 @@ def test_advec_tma_misaligned_fields_use_scalar_path(gpu_ctx, compiler, precisio
     from paper_2303_12374_b200.stencils.problem import StencilProblem
 
     lay = GridLayout(70, 29, 23, precision)
-    ref, _ = oracle_outputs("advec_u", lay)
-    cfg = dict(_default("advec_u", precision), staging="TMA", contiguous_x=True, block_x=32, block_y=4, tile_x=2,
-               tile_y=2, depth=2, zchunk=8)
-    prob = StencilProblem("advec_u", lay, gpu_ctx)
+    ref, _ = oracle_outputs(kernel, lay)
+    cfg = dict(_default(kernel, precision), **_MISALIGNED_CFG[kernel])
+    prob = StencilProblem(kernel, lay, gpu_ctx)
     shifted = {}
     try:
         args = []
@@ -196,12 +229,11 @@ def test_advec_tma_misaligned_fields_use_scalar_path(gpu_ctx, compiler, precisio
         exe = compiler.compile(d.render_compile_request(cfg, problem, env), gpu_ctx.ident)
         exe.load()
         exe.launch(d.derive_geometry(cfg, problem, env), args, timed=True)
-        out = args[0]
-        flat = np.frombuffer(shifted[0].download(lay.alloc_bytes, offset_bytes=lay.elem_bytes), dtype=lay.dtype)
-        got = lay.host_view(flat)
-        assert out.ptr % 16 != (prob.field_ptr("ut") % 16)
-        err = rel_error(got, ref["ut"], lay)
-        assert err <= TOL[precision], err
+        assert args[0].ptr % 16 != (prob.field_ptr("ut") % 16)
+        for pos, name in enumerate(prob.outputs()):
+            flat = np.frombuffer(shifted[pos].download(lay.alloc_bytes, offset_bytes=lay.elem_bytes), dtype=lay.dtype)
+            err = rel_error(lay.host_view(flat), ref[name], lay)
+            assert err <= TOL[precision], (name, err)
     finally:
         for arr in shifted.values():
             arr.free()
