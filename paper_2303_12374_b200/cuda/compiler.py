@@ -29,6 +29,7 @@ import threading
 import time
 from concurrent.futures import ThreadPoolExecutor
 from dataclasses import dataclass
+from pathlib import Path
 from typing import Sequence
 
 from ..backend import CompileError, CompilerInterface, DeviceIdent, ExecutableHandle, LaunchError
@@ -63,6 +64,30 @@ def _arch_for(device: DeviceIdent | None, ctx: DeviceContext | None) -> str:
         major, minor = (int(x) for x in str(cc).split("."))
         return f"sm_{major}{minor}{'a' if major >= 9 else ''}"
     return "sm_100a"
+
+
+_SOURCE_DIR = Path(os.environ.get("KL_NVRTC_SOURCE_DIR", Path(__file__).resolve().parents[2] / "build" / "nvrtc_src"))
+_written: set[str] = set()
+
+
+def _program_name(source: str) -> bytes:
+    """NVRTC program name = the path of an on-disk mirror of the source, so
+    ``-lineinfo`` line tables resolve (``ncu --import-source on`` shows the
+    stencil source next to the SASS).  Falls back to a bare name when the
+    directory is not writable — the name only labels debug information."""
+    digest = hashlib.sha256(source.encode()).hexdigest()[:16]
+    path = _SOURCE_DIR / f"kl_{digest}.cu"
+    if digest not in _written:
+        try:
+            _SOURCE_DIR.mkdir(parents=True, exist_ok=True)
+            if not path.exists():
+                tmp = path.with_suffix(f".{os.getpid()}.tmp")
+                tmp.write_text(source)
+                os.replace(tmp, path)
+            _written.add(digest)
+        except OSError:
+            return b"kltune_kernel.cu"
+    return str(path).encode()
 
 
 class NvrtcCompiler(CompilerInterface):
@@ -103,7 +128,7 @@ class NvrtcCompiler(CompilerInterface):
         image, size = C.c_void_p(), C.c_size_t()
         lowered, log = C.c_void_p(), C.c_void_p()
         t0 = time.perf_counter()
-        rc = lib().klb_compile(request.source.encode(), b"kltune_kernel.cu", request.entry.encode(), opt_arr,
+        rc = lib().klb_compile(request.source.encode(), _program_name(request.source), request.entry.encode(), opt_arr,
                                len(options), C.byref(image), C.byref(size), C.byref(lowered), C.byref(log))
         elapsed = time.perf_counter() - t0
         log_text = C.string_at(log.value).decode("utf-8", "replace") if log.value else ""

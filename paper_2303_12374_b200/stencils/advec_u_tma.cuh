@@ -38,6 +38,7 @@
 #define DEPTH 2
 #endif
 
+#include "kl_pack.cuh"
 #include "kl_tma.cuh"
 
 namespace {
@@ -61,6 +62,10 @@ constexpr int kPB = kUB + kVB + kWB + kTB;  // bytes per plane slot
 constexpr int kPS = kPB / kS;
 constexpr int kVO = kUB / kS, kWO = (kUB + kVB) / kS, kTO = (kUB + kVB + kWB) / kS;  // field offsets in a slot
 constexpr int kNS = DEPTH + 4;
+// fp32 with column tiles: pairs of neighbouring columns share packed
+// FADD2/FMUL2/FFMA2 instructions (kl_pack.cuh)
+constexpr bool kPack = sizeof(real) == 4 && kTX >= 2;
+constexpr int kP = kTX / 2 > 0 ? kTX / 2 : 1;  // column pairs per thread
 constexpr unsigned kTxBytes =
     static_cast<unsigned>((kBW * kBH + kVW * (kTYT + 1) + kVW * kTYT + kTW * kTYT) * kS);
 static_assert(kBW <= 256 && kBH <= 256, "TMA box extents are limited to 256");
@@ -261,6 +266,187 @@ struct AdvecTma {
       }
     }
   }
+
+  // main loop of the packed variant (fp32, TILE_X in {2, 4}, aligned layout):
+  // the same flux-form march with the arithmetic of column pairs (c, c+1)
+  // in f2 registers.  x faces: the first-level operand sums of a face pair
+  // mix even- and odd-aligned columns, so they are scalar FADDs whose results
+  // pair up freely; everything after them is packed.  y and z faces read
+  // operands of the same column pair, which the vectorised shared loads
+  // already hold as aligned register pairs.
+  template <int VA>
+  __device__ __forceinline__ void march2() const {
+    using kl::f2;
+    constexpr long long K1 = KL_KK;
+    const real* zprof = ring + kNS * kPS;  // [ZCHUNK][2]: rhorefh[k+1], dzi[k] / (120 rhoref[k])
+    f2 uq[kTY][kP][6];  // u[k-2 .. k+3] of every column pair
+    f2 fz_bot[kTY][kP];
+    kl::mbar_wait(full + 0, 0);
+    kl::mbar_wait(full + 1, 0);
+    kl::mbar_wait(full + 2, 0);
+    {
+      const f2 rh0(rhorefh[k0]);
+      const real* wp = ring + kWO + wofs;  // slot 0 = plane k0
+#pragma unroll
+      for (int t = 0; t < kTY; ++t) {
+        const int j = min(j0 + lj0 + t, jend - 1);
+        real wr[kTX + 8];
+        wr[3] = wp[t * kVW + 3];
+        ld_span<VA, 4, 4 + kTX>(wr, wp + t * kVW);
+#pragma unroll
+        for (int p = 0; p < kP; ++p) {
+          const int c = 2 * p;
+          const long long rowk = static_cast<long long>(j) * KL_JJ + static_cast<long long>(k0) * KL_KK;
+          const long long b0 = min(ic + c, iend - 1) + rowk, b1 = min(ic + c + 1, iend - 1) + rowk;
+          const f2 um3(u[b0 - 3 * K1], u[b1 - 3 * K1]);  // planes below the chunk: not staged
+#pragma unroll
+          for (int m = 0; m < 5; ++m) uq[t][p][m] = f2(u[b0 + (m - 2) * K1], u[b1 + (m - 2) * K1]);
+          const f2 vel(wr[3 + c] + wr[4 + c], wr[4 + c] + wr[5 + c]);
+          fz_bot[t][p] = rh0 * kl::flux5x60(vel, um3, uq[t][p][0], uq[t][p][1], uq[t][p][2], uq[t][p][3],
+                                             uq[t][p][4]);
+        }
+      }
+    }
+    const f2 dx2(dxi120), dy2(dyi120);
+
+    int s0 = 0, s1 = 1, s3 = 3, sprev = kNS - 1;  // slots of planes k, k+1, k+3, k-1
+    unsigned ph3 = 0;                              // barrier parity of plane k+3
+    for (int k = k0; k < k1; ++k) {
+      __syncthreads();  // plane k-1's slot is free
+      if (tid == 0) {
+        const int p = k - 1 + kNS;
+        if (k > k0 && p <= kmax) {
+          kl::fence_proxy_async_smem();
+          issue(sprev, p);
+        }
+      }
+      kl::mbar_wait(full + s3, ph3);
+      const real* sk = ring + s0 * kPS;
+      const real* xy = sk + uofs;                     // u, plane k at (ic-4, j0+lj0)
+      const real* zf = ring + s3 * kPS + uofs + 4;    // u, plane k+3 at (ic, j0+lj0)
+      const real* vp = sk + kVO + vofs;               // v, plane k at (ic-4, j0+lj0)
+      const real* wp = ring + s1 * kPS + kWO + wofs;  // w, plane k+1 at (ic-4, j0+lj0)
+      const real* tp = sk + kTO + tofs;               // ut, plane k at (ic, j0+lj0)
+      const f2 rh_top(zprof[2 * (k - k0)]);
+      const f2 zfac(zprof[2 * (k - k0) + 1]);
+      const long long kofs = static_cast<long long>(k) * K1;
+      sprev = s0;
+      s0 = s1;
+      s1 = s1 + 1 == kNS ? 0 : s1 + 1;
+      s3 = s3 + 1 == kNS ? 0 : s3 + 1;
+      ph3 ^= s3 == 0 ? 1u : 0u;
+
+      // u along y in this thread's columns: rows lj0-3 .. lj0+kTY+2
+      real ucol[kTY + 6][kTX];
+#pragma unroll
+      for (int m = 0; m < kTY + 6; ++m) {
+        if (m >= 3 && m < kTY + 3) continue;  // strip rows: taken from the x rows below
+        real r[kTX + 8];
+        ld_span<VA, 4, 4 + kTX>(r, xy + (m - 3) * kBW);
+#pragma unroll
+        for (int c = 0; c < kTX; ++c) ucol[m][c] = r[4 + c];
+      }
+      real xr[kTY][kTX + 8];  // x rows of the strip: columns ic-4 .. ic+kTX+3
+#pragma unroll
+      for (int t = 0; t < kTY; ++t) {
+        ld_span<VA, 1, kTX + 7>(xr[t], xy + t * kBW);
+#pragma unroll
+        for (int c = 0; c < kTX; ++c) ucol[t + 3][c] = xr[t][4 + c];
+      }
+      auto ucp = [&](int m, int p) { return f2(ucol[m][2 * p], ucol[m][2 * p + 1]); };
+      // south faces of the strip (row j0+lj0-1/2)
+      f2 fy_lo[kP];
+      {
+        real vr[kTX + 8];
+        vr[3] = vp[3];
+        ld_span<VA, 4, 4 + kTX>(vr, vp);
+#pragma unroll
+        for (int p = 0; p < kP; ++p) {
+          const int c = 2 * p;
+          const f2 vel(vr[3 + c] + vr[4 + c], vr[4 + c] + vr[5 + c]);
+          fy_lo[p] = kl::flux5x60(vel, ucp(0, p), ucp(1, p), ucp(2, p), ucp(3, p), ucp(4, p), ucp(5, p));
+        }
+      }
+
+#pragma unroll
+      for (int t = 0; t < kTY; ++t) {
+        // x: faces f = 0..kTX sit between columns ic+f-1 and ic+f; face pairs
+        // (f, f+1) from scalar first-level sums, the last face alone
+        const real* r = xr[t];
+        real fx[kTX + 1];
+#pragma unroll
+        for (int f = 0; f < kTX; f += 2) {
+          const f2 s_cd(r[f + 3] + r[f + 4], r[f + 4] + r[f + 5]);
+          const f2 s_be(r[f + 2] + r[f + 5], r[f + 3] + r[f + 6]);
+          const f2 s_af(r[f + 1] + r[f + 6], r[f + 2] + r[f + 7]);
+          const f2 d_dc(r[f + 4] - r[f + 3], r[f + 5] - r[f + 4]);
+          const f2 d_eb(r[f + 5] - r[f + 2], r[f + 6] - r[f + 3]);
+          const f2 d_fa(r[f + 6] - r[f + 1], r[f + 7] - r[f + 2]);
+          const f2 fl = kl::flux5x60_sd(s_cd, s_cd, s_be, s_af, d_dc, d_eb, d_fa);
+          fx[f] = fl.lo();
+          fx[f + 1] = fl.hi();
+        }
+        fx[kTX] = kl::flux5x60(r[kTX + 3] + r[kTX + 4], r[kTX + 1], r[kTX + 2], r[kTX + 3], r[kTX + 4],
+                               r[kTX + 5], r[kTX + 6]);
+        real vr[kTX + 8], wr[kTX + 8], zr[kTX + 8], tr[kTX + 8], out[kTX];
+        const real* vn = vp + (t + 1) * kVW;
+        vr[3] = vn[3];
+        ld_span<VA, 4, 4 + kTX>(vr, vn);
+        const real* wrow = wp + t * kVW;
+        wr[3] = wrow[3];
+        ld_span<VA, 4, 4 + kTX>(wr, wrow);
+        ld_span<VA, 0, kTX>(zr, zf + t * kBW);
+        ld_span<VA, 0, kTX>(tr, tp + t * kTW);
+#pragma unroll
+        for (int p = 0; p < kP; ++p) {
+          const int c = 2 * p;
+          f2* q = uq[t][p];
+          q[5] = f2(zr[c], zr[c + 1]);
+          // y: north face of this row; south face carried from the previous row
+          const f2 vel_n(vr[3 + c] + vr[4 + c], vr[4 + c] + vr[5 + c]);
+          const f2 fy_hi = kl::flux5x60(vel_n, ucp(t + 1, p), ucp(t + 2, p), ucp(t + 3, p), ucp(t + 4, p),
+                                        ucp(t + 5, p), ucp(t + 6, p));
+          // z: top face of this plane; bottom face carried from the previous plane
+          const f2 vel_t(wr[3 + c] + wr[4 + c], wr[4 + c] + wr[5 + c]);
+          const f2 fz_top = rh_top * kl::flux5x60(vel_t, q[0], q[1], q[2], q[3], q[4], q[5]);
+          const f2 dfx(fx[c + 1] - fx[c], fx[c + 2] - fx[c + 1]);
+          const f2 o = f2(tr[c], tr[c + 1]) -
+                       kl::fma2(fz_top - fz_bot[t][p], zfac, kl::fma2(fy_hi - fy_lo[p], dy2, dfx * dx2));
+          out[c] = o.lo();
+          out[c + 1] = o.hi();
+          fy_lo[p] = fy_hi;
+          fz_bot[t][p] = fz_top;
+#pragma unroll
+          for (int m = 0; m < 5; ++m) q[m] = q[m + 1];
+        }
+        const int j = j0 + lj0 + t;
+        if (j < jend) {
+          real* dst = ut + ic + static_cast<long long>(j) * KL_JJ + kofs;
+          if (ic + kTX <= iend) {
+            st_span<VA>(dst, out);
+          } else {
+#pragma unroll
+            for (int c = 0; c < kTX; ++c)
+              if (ic + c < iend) dst[c] = out[c];
+          }
+        }
+      }
+    }
+  }
+};
+}  // namespace
+
+namespace {
+// selects the packed main loop without instantiating it for fp64 / TILE_X == 1
+template <bool kPacked>
+struct Marcher {
+  template <int VA>
+  static __device__ __forceinline__ void run(const AdvecTma& m) { m.march<VA>(); }
+};
+template <>
+struct Marcher<true> {
+  template <int VA>
+  static __device__ __forceinline__ void run(const AdvecTma& m) { m.march2<VA>(); }
 };
 }  // namespace
 
@@ -347,7 +533,7 @@ KL_ENTRY(real* __restrict__ ut, const real* __restrict__ u, const real* __restri
   }
   // (the march's first __syncthreads publishes zprof)
   if (kVA > 1 && (sh_u | sh_v | sh_w | sh_t) == 0) {
-    m.march<kVA>();
+    Marcher<kPack>::template run<kVA>(m);
   } else {
     m.march<1>();
   }

@@ -181,8 +181,13 @@ __device__ __forceinline__ void plane_step(const real* h0, const real* h1, const
       real fzu[kTX], fzv[kTX], gz[kTX];
 #pragma unroll
       for (int q = 0; q < kTX; ++q) {
-        fzu[q] = z.rh1 * sxz[q] * ((cur.x[q] - cur.u[q + 1]) * z.dzhi1 + (cur.w[q + 1] - cur.w[q]) * s.sx);
-        fzv[q] = z.rh1 * syz[q] * ((cur.y[q] - cur.v[q + 1]) * z.dzhi1 + (cur.w[q + 1] - wlo[q]) * s.sy);
+        // the stress tensor is symmetric: u's z flux through the top face is
+        // rhorefh[k+1] x w's x flux through the west face of the cell above
+        // (both tau_xz at (i-1/2, k+1/2)), and v's z flux is rhorefh[k+1] x
+        // w's y flux through the south face (tau_yz at (j-1/2, k+1/2), the
+        // previous row's fyw_up) — evaluated once, reused
+        fzu[q] = z.rh1 * fxw[q];
+        fzv[q] = z.rh1 * fyw[q];
         gz[q] = z.rdz * cur.e[q + 1] * (cur.w[q + 1] - cur.z[q]);
       }
       if (OUT) {

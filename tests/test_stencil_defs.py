@@ -70,3 +70,59 @@ def test_nvrtc_compiles_sampled_configs(kernel, precision):
     for fut in futures:
         img = fut.result()
         assert img.lowered_name == f"{kernel}_{precision}" and len(img.cubin) > 1000
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+@pytest.mark.parametrize("precision", list(PRECISIONS))
+def test_tma_shared_memory_fits_the_optin_limit(kernel, precision):
+    """Every TMA point of the (precision-specific) space launches within the
+    B200 opt-in shared-memory limit, and the restriction admits large tiles
+    (the ring is bounded by bytes, not by a fixed cell count)."""
+    from paper_2303_12374_b200.stencils.definitions import SMEM_OPTIN_BYTES, family_space
+
+    d = definition_for(kernel, precision)
+    lay = GridLayout(512, 512, 512, precision)
+    env = scalar_env_from_args(scalars(kernel, lay))
+    problem = d.derive_problem_size(env)
+    cfgs = family_space(kernel, "TMA", precision).sample_random(5, 400)
+    assert cfgs
+    biggest = 0
+    for c in cfgs:
+        assert d.space.is_valid(c)
+        smem = d.derive_geometry(c, problem, env).shared_mem_bytes
+        assert 0 < smem <= SMEM_OPTIN_BYTES, c
+        biggest = max(biggest, smem)
+    assert biggest > 96 * 1024
+    assert any(c["tile_x"] > 1 for c in cfgs)
+
+
+def test_space_fingerprints_differ_by_precision_only_where_limits_do():
+    keys = {(k, p): definition_for(k, p).space.fingerprint() for k in KERNELS for p in PRECISIONS}
+    assert keys["diff_uvw", "fp32"] != keys["diff_uvw", "fp64"]
+    assert keys["advec_u", "fp32"] != keys["advec_u", "fp64"]
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_nvrtc_compiles_column_tiles(kernel):
+    """TMA column tiles (tile_x consecutive columns; the fp32 advec_u ones use
+    packed FFMA2/FADD2 arithmetic) compile for sm_100a in both precisions."""
+    from paper_2303_12374_b200.cuda._abi import library_path
+    from paper_2303_12374_b200.cuda.compiler import NvrtcCompiler
+
+    if not library_path().exists():
+        pytest.skip("libklb200.so not built")
+    comp = NvrtcCompiler()
+    for precision in PRECISIONS:
+        d = definition_for(kernel, precision)
+        lay = GridLayout(64, 24, 16, precision)
+        env = scalar_env_from_args(scalars(kernel, lay))
+        problem = d.derive_problem_size(env)
+        reqs = []
+        for tx, bx in ((2, 32), (4, 16)):
+            cfg = d.space.default_config()[0]
+            cfg.update(FAMILY_PINS["TMA"], tile_x=tx, contiguous_x=True, contiguous_y=False, block_x=bx, block_y=4,
+                       tile_y=2, zchunk=16, depth=1)
+            assert d.space.is_valid(cfg), cfg
+            reqs.append(d.render_compile_request(cfg, problem, env))
+        for fut in comp.compile_many(reqs, B200):
+            assert len(fut.result().cubin) > 1000
