@@ -36,6 +36,7 @@
 #define DEPTH 2
 #endif
 
+#include "kl_pack.cuh"
 #include "kl_tma.cuh"
 
 namespace {
@@ -57,6 +58,10 @@ constexpr int kTS = kTSB / kS;
 constexpr int kSlot = 4 * kFS + 3 * kTS;
 constexpr int kNS = DEPTH + 2;
 constexpr unsigned kTxBytes = 4u * kBW * kBH * kS + 3u * kTW * kTYT * kS;
+// fp32 with column tiles: the arithmetic of column pairs runs on packed
+// FADD2/FMUL2/FFMA2 (kl_pack.cuh)
+constexpr bool kPack = sizeof(real) == 4 && kTX >= 2;
+constexpr int kP = kTX / 2 > 0 ? kTX / 2 : 1;  // column pairs per thread
 static_assert(kBW <= 256 && kBH <= 256 && kTW <= 256, "TMA box extents are limited to 256");
 
 template <int N>
@@ -151,7 +156,7 @@ __device__ __forceinline__ void plane_step(const real* h0, const real* h1, const
   };
   load(cur, 0);
   // y-face quantities of the current row's lower face (from the previous row)
-  real sxy[kTX + 1], fyu[kTX], gy[kTX], syz[kTX], fyw[kTX], ulo[kTX + 1], wlo[kTX], fyw_prev[kTX];
+  real sxy[kTX + 1], fyu[kTX], gy[kTX], fyw[kTX], ulo[kTX + 1], fyw_prev[kTX];
 #pragma unroll
   for (int q = 0; q < kTX; ++q) fyw_prev[q] = real(0);
 
@@ -229,15 +234,189 @@ __device__ __forceinline__ void plane_step(const real* h0, const real* h1, const
     }
 #pragma unroll
     for (int q = 0; q < kTX; ++q) {
-      wlo[q] = cur.w[q + 1];
       fyu[q] = fyu_up[q];
       gy[q] = gy_up[q];
-      syz[q] = syz_up[q];
       fyw[q] = fyw_up[q];
     }
     cur = nrt;
   }
 }
+
+// Carried z-face quantities of the packed variant (column pairs in f2; the
+// x-face flux of w stays per face, its differences mix column parities).
+struct Carry2 {
+  kl::f2 fzu[kTY][kP], fzv[kTY][kP], gz[kTY][kP], fyw_p[kTY][kP];
+  real fxw[kTY][kTX + 1];
+  kl::f2 fyw_lo[kP];
+};
+
+// Packed plane step (fp32, kTX in {2, 4}): plane_step's arithmetic with the
+// quantities of column pairs (c, c+1) in f2 registers.  x-face quantities
+// need columns (f-1, f), whose pairs straddle the aligned register pairs the
+// vectorised shared loads produce, so their first-level sums/differences are
+// scalar (their results pair up freely) and the rest is packed for face pairs
+// (0,1), (2,3) with the last face scalar.  Cell-centred and y/z quantities
+// read aligned pairs directly.
+template <bool OUT, int VA, class Store>
+__device__ __forceinline__ void plane_step2(const real* h0, const real* h1, const int (&hof)[4], Carry2& c,
+                                            const Scales& s, const PlaneFactors& z, Store&& store) {
+  using kl::f2;
+  Row cur, nrt;
+  auto load = [&](Row& r, int row) {
+    const int ro = row * kBW;
+    ld_row<VA>(r.e, h0 + hof[0] + ro);
+    ld_row<VA>(r.u, h0 + hof[1] + ro);
+    ld_row<VA>(r.v, h0 + hof[2] + ro);
+    ld_row<VA>(r.f, h1 + hof[0] + ro);
+    ld_row<VA>(r.w, h1 + hof[3] + ro);
+    ld_span<VA, kTX>(r.y, h1 + hof[2] + ro);
+    ld_span<VA, kTX + 1>(r.x, h1 + hof[1] + ro);
+    ld_span<VA, kTX>(r.z, h0 + hof[3] + ro);
+  };
+  // (T[1+c], T[2+c]) = columns (c, c+1) of a (kTX+2)-wide row; (T[c], T[c+1]) of y/x/z
+  auto pr = [](const real* a, int c) { return f2(a[1 + c], a[2 + c]); };
+  auto pc = [](const real* a, int c) { return f2(a[c], a[c + 1]); };
+  const f2 sx(s.sx), sy(s.sy), dz1(z.dzhi1), rh1(z.rh1), rdz(z.rdz);
+  load(cur, 0);
+  // per-face sums of the current row's lower face, carried from the row below
+  real eS[kTX + 1], dv[kTX + 1], sxy_l[kTX + 1];  // e pair sums, v differences, 4x edge viscosity
+  f2 fyu[kP], gy[kP], fyw[kP], ulo[kP];
+  real ulo_last = 0;
+  f2 fyw_prev[kP];
+#pragma unroll
+  for (int f = 0; f <= kTX; ++f) eS[f] = cur.e[f] + cur.e[f + 1];
+
+#pragma unroll
+  for (int t = -1; t < kTY; ++t) {
+    load(nrt, t + 2);
+    // north row: e pair sums and v differences per face (scalar)
+    real eN[kTX + 1], dvn[kTX + 1], sxy_up[kTX + 1];
+#pragma unroll
+    for (int f = 0; f <= kTX; ++f) {
+      eN[f] = nrt.e[f] + nrt.e[f + 1];
+      dvn[f] = nrt.v[f + 1] - nrt.v[f];
+      sxy_up[f] = eS[f] + eN[f];
+    }
+    f2 fyu_up[kP], gy_up[kP], syz_up[kP], fyw_up[kP];
+#pragma unroll
+    for (int p = 0; p < kP; ++p) {
+      const int q = 2 * p;
+      const f2 e = pr(cur.e, q), en = pr(nrt.e, q), v = pr(cur.v, q), vn = pr(nrt.v, q);
+      fyu_up[p] = f2(sxy_up[q], sxy_up[q + 1]) * kl::fma2(pr(nrt.u, q) - pr(cur.u, q), sy, f2(dvn[q], dvn[q + 1]) * sx);
+      gy_up[p] = e * (vn - v);
+      syz_up[p] = (e + en) + (pr(cur.f, q) + pr(nrt.f, q));
+      fyw_up[p] = syz_up[p] * kl::fma2(pr(nrt.w, q) - pr(cur.w, q), sy, (pc(nrt.y, q) - vn) * dz1);
+    }
+
+    if (t >= 0) {
+      // x-faces: sxz (4x the xz edge viscosity) and w's x flux (= tau_xz)
+      real fxw[kTX + 1];
+#pragma unroll
+      for (int f = 0; f < kTX; f += 2) {
+        const f2 sxz = f2(eS[f], eS[f + 1]) + f2(cur.f[f] + cur.f[f + 1], cur.f[f + 1] + cur.f[f + 2]);
+        const f2 dw(cur.w[f + 1] - cur.w[f], cur.w[f + 2] - cur.w[f + 1]);
+        const f2 fl = sxz * kl::fma2(dw, sx, (pc(cur.x, f) - pr(cur.u, f)) * dz1);
+        fxw[f] = fl.lo();
+        fxw[f + 1] = fl.hi();
+      }
+      {
+        constexpr int f = kTX;
+        const real sxz = eS[f] + (cur.f[f] + cur.f[f + 1]);
+        fxw[f] = sxz * ((cur.w[f + 1] - cur.w[f]) * s.sx + (cur.x[f] - cur.u[f + 1]) * z.dzhi1);
+      }
+      f2 fzu[kP], fzv[kP], gz[kP];
+#pragma unroll
+      for (int p = 0; p < kP; ++p) {
+        const int q = 2 * p;
+        // symmetric stress: u's z flux = rhorefh[k+1] tau_xz (w's west-face x
+        // flux), v's z flux = rhorefh[k+1] tau_yz (the previous row's fyw_up)
+        fzu[p] = rh1 * f2(fxw[q], fxw[q + 1]);
+        fzv[p] = rh1 * fyw[p];
+        gz[p] = rdz * pr(cur.e, q) * (pr(cur.w, q) - pc(cur.z, q));
+      }
+      if (OUT) {
+        real gx[kTX + 1], fxv[kTX + 1];
+#pragma unroll
+        for (int f = 0; f <= kTX; ++f) gx[f] = cur.e[f] * (cur.u[f + 1] - cur.u[f]);
+#pragma unroll
+        for (int f = 0; f < kTX; f += 2) {
+          const f2 dul = pr(cur.u, f) - ulo[f / 2];
+          const f2 fl = f2(sxy_l[f], sxy_l[f + 1]) * kl::fma2(f2(dv[f], dv[f + 1]), sx, dul * sy);
+          fxv[f] = fl.lo();
+          fxv[f + 1] = fl.hi();
+        }
+        fxv[kTX] = sxy_l[kTX] * (dv[kTX] * s.sx + (cur.u[kTX + 1] - ulo_last) * s.sy);
+        const f2 c2x(s.c2x), c2y(s.c2y), qsx(s.qsx), qsy(s.qsy), qfac(z.qfac), facw(z.fac_w);
+        real dut[kTX], dvt[kTX], dwt[kTX];
+#pragma unroll
+        for (int p = 0; p < kP; ++p) {
+          const int q = 2 * p;
+          const f2 fyw_s = t == 0 ? c.fyw_lo[p] : fyw_prev[p];  // previous plane's south face of this row
+          const f2 dgx(gx[q + 1] - gx[q], gx[q + 2] - gx[q + 1]);
+          const f2 dfxv(fxv[q + 1] - fxv[q], fxv[q + 2] - fxv[q + 1]);
+          const f2 dfxw(c.fxw[t][q + 1] - c.fxw[t][q], c.fxw[t][q + 2] - c.fxw[t][q + 1]);
+          const f2 a = kl::fma2(c2x, dgx, kl::fma2(fyu_up[p] - fyu[p], qsy, (fzu[p] - c.fzu[t][p]) * qfac));
+          const f2 b = kl::fma2(dfxv, qsx, kl::fma2(c2y, gy_up[p] - gy[p], (fzv[p] - c.fzv[t][p]) * qfac));
+          const f2 d = kl::fma2(dfxw, qsx, kl::fma2(c.fyw_p[t][p] - fyw_s, qsy, (gz[p] - c.gz[t][p]) * facw));
+          dut[q] = a.lo();
+          dut[q + 1] = a.hi();
+          dvt[q] = b.lo();
+          dvt[q + 1] = b.hi();
+          dwt[q] = d.lo();
+          dwt[q + 1] = d.hi();
+        }
+        store(t, dut, dvt, dwt);
+      }
+#pragma unroll
+      for (int p = 0; p < kP; ++p) {
+        c.fzu[t][p] = fzu[p];
+        c.fzv[t][p] = fzv[p];
+        c.gz[t][p] = gz[p];
+        if (t == 0) c.fyw_lo[p] = fyw[p];
+        fyw_prev[p] = c.fyw_p[t][p];  // previous plane's north face of row t = south face of row t+1
+        c.fyw_p[t][p] = fyw_up[p];
+      }
+#pragma unroll
+      for (int f = 0; f <= kTX; ++f) c.fxw[t][f] = fxw[f];
+    }
+
+    // slide the strip: the north row becomes the current row
+#pragma unroll
+    for (int f = 0; f <= kTX; ++f) {
+      eS[f] = eN[f];
+      dv[f] = dvn[f];
+      sxy_l[f] = sxy_up[f];
+    }
+#pragma unroll
+    for (int p = 0; p < kP; ++p) {
+      ulo[p] = pr(cur.u, 2 * p);
+      fyu[p] = fyu_up[p];
+      gy[p] = gy_up[p];
+      fyw[p] = fyw_up[p];
+    }
+    ulo_last = cur.u[kTX + 1];
+    cur = nrt;
+  }
+}
+
+template <bool kPacked>
+struct Step {
+  using CarryT = Carry;
+  template <bool OUT, int VA, class Store>
+  static __device__ __forceinline__ void run(const real* h0, const real* h1, const int (&hof)[4], CarryT& c,
+                                             const Scales& s, const PlaneFactors& z, Store&& store) {
+    plane_step<OUT, VA>(h0, h1, hof, c, s, z, store);
+  }
+};
+template <>
+struct Step<true> {
+  using CarryT = Carry2;
+  template <bool OUT, int VA, class Store>
+  static __device__ __forceinline__ void run(const real* h0, const real* h1, const int (&hof)[4], CarryT& c,
+                                             const Scales& s, const PlaneFactors& z, Store&& store) {
+    plane_step2<OUT, VA>(h0, h1, hof, c, s, z, store);
+  }
+};
 
 // Per-block state of the march (member template instead of a generic lambda:
 // NVRTC has no extended device lambdas).
@@ -264,14 +443,15 @@ struct DiffTma {
     for (int f = 0; f < 3; ++f) kl::tma_load_3d(dst + 4 * kFS + f * kTS, maps + 4 + f, bar, xt, j0, p);
   }
 
-  template <int VA>
+  template <int VA, bool PK = false>
   __device__ __forceinline__ void march() const {
-    Carry carry;
+    using S = Step<PK>;
+    typename S::CarryT carry;
     auto no_store = [](int, const real(&)[kTX], const real(&)[kTX], const real(&)[kTX]) {};
     const int kfirst = k0 - 1;
     kl::mbar_wait(full + 0, 0);  // plane kfirst
     kl::mbar_wait(full + 1, 0);  // plane k0
-    plane_step<false, VA>(ring, ring + kSlot, hof, carry, sc, pro, no_store);
+    S::template run<false, VA>(ring, ring + kSlot, hof, carry, sc, pro, no_store);
 
     int sprev = 0, sk = 1, sk1 = 2 % kNS;  // slots of planes k-1, k, k+1
     unsigned ph1 = 0;                      // barrier parity of plane k+1
@@ -291,10 +471,18 @@ struct DiffTma {
       const real* pk1 = ring + sk1 * kSlot;
       const real* tend = pk + 4 * kFS + tofs;
       const long long kofs = static_cast<long long>(k) * KL_KK;
+      // this plane's (strip row 0, first column) in each tendency: rows are
+      // then immediate offsets (t * KL_JJ) from three per-plane pointers
+      const long long base = ic + static_cast<long long>(j0 + lj0) * KL_JJ + kofs;
+      real* const up = ut + base;
+      real* const vp = vt + base;
+      real* const wp = wt + base;
+      const bool full_x = ic + kTX <= iend;
       auto store = [&](int t, const real(&dut)[kTX], const real(&dvt)[kTX], const real(&dwt)[kTX]) {
-        const int j = j0 + lj0 + t;
-        if (j >= jend) return;
-        const long long ijk = ic + static_cast<long long>(j) * KL_JJ + kofs;
+        if (j0 + lj0 + t >= jend) return;
+        real* const ur = up + t * KL_JJ;
+        real* const vr = vp + t * KL_JJ;
+        real* const wr = wp + t * KL_JJ;
         real o[3][kTX];
         if (VA > 1) {
           ld_span<VA, kTX>(o[0], tend + t * kTW);
@@ -304,9 +492,9 @@ struct DiffTma {
 #pragma unroll
           for (int q = 0; q < kTX; ++q) {
             const bool in = ic + q < iend;
-            o[0][q] = in ? ut[ijk + q] : real(0);
-            o[1][q] = in ? vt[ijk + q] : real(0);
-            o[2][q] = in ? wt[ijk + q] : real(0);
+            o[0][q] = in ? ur[q] : real(0);
+            o[1][q] = in ? vr[q] : real(0);
+            o[2][q] = in ? wr[q] : real(0);
           }
         }
 #pragma unroll
@@ -315,7 +503,7 @@ struct DiffTma {
           o[1][q] += dvt[q];
           o[2][q] += dwt[q];
         }
-        if (VA > 1 && ic + kTX <= iend) {
+        if (VA > 1 && full_x) {
 #pragma unroll
           for (int e = 0; e < kTX; e += VA) {
             Pack<VA> a, b, d;
@@ -325,22 +513,22 @@ struct DiffTma {
               b.v[q] = o[1][e + q];
               d.v[q] = o[2][e + q];
             }
-            *reinterpret_cast<Pack<VA>*>(ut + ijk + e) = a;
-            *reinterpret_cast<Pack<VA>*>(vt + ijk + e) = b;
-            *reinterpret_cast<Pack<VA>*>(wt + ijk + e) = d;
+            *reinterpret_cast<Pack<VA>*>(ur + e) = a;
+            *reinterpret_cast<Pack<VA>*>(vr + e) = b;
+            *reinterpret_cast<Pack<VA>*>(wr + e) = d;
           }
         } else {
 #pragma unroll
           for (int q = 0; q < kTX; ++q) {
             if (ic + q < iend) {
-              ut[ijk + q] = o[0][q];
-              vt[ijk + q] = o[1][q];
-              wt[ijk + q] = o[2][q];
+              ur[q] = o[0][q];
+              vr[q] = o[1][q];
+              wr[q] = o[2][q];
             }
           }
         }
       };
-      plane_step<true, VA>(pk, pk1, hof, carry, sc, pf, store);
+      S::template run<true, VA>(pk, pk1, hof, carry, sc, pf, store);
       sprev = sk;
       sk = sk1;
       sk1 = sk1 + 1 == kNS ? 0 : sk1 + 1;
@@ -439,7 +627,7 @@ KL_ENTRY(real* __restrict__ ut, real* __restrict__ vt, real* __restrict__ wt, co
   }
   m.zprof = zprof;
   if (kVA > 1 && aligned) {
-    m.march<kVA>();
+    m.march<kVA, kPack>();
   } else {
     m.march<1>();
   }
