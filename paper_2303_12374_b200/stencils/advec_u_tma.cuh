@@ -1,14 +1,17 @@
 // advec_u_tma.cuh — STAGING == TMA variant of advec_u (included by
 // advec_u.cu).  Flux-form z-march (see advec_u_zmarch.cuh) with every operand
-// fetched by the Tensor Memory Accelerator into a shared-memory ring of
-// DEPTH+4 slots (one mbarrier each).  Slot p holds plane p of
-//   * u with a 3-cell x/y halo — plane k feeds the x/y stencil of step k and
-//     plane k+3 the z-window (so u[k+3] of every cell comes from the ring);
-//   * v (columns i-1..i, rows j..j+1), w (columns i-1..i) and ut (no halo):
-//     step k reads v and ut of plane k and w of plane k+1;
+// fetched by the Tensor Memory Accelerator into two shared-memory rings, one
+// mbarrier per slot:
+//   * u, with a 3-cell x/y halo, in DEPTH+4 slots — plane k feeds the x/y
+//     stencil of step k and plane k+3 the z-window (so u[k+3] of every cell
+//     comes from the ring);
+//   * v (columns i-1..i, rows j..j+1), w (columns i-1..i) and ut (no halo)
+//     in DEPTH+2 slots — step k reads v and ut of plane k and w of plane k+1;
 // so the compute warps issue no global loads, only the final ut stores.  One
-// elected thread refills the slot vacated by plane k-1 at the start of step
-// k, keeping DEPTH planes beyond the ones being read in flight.
+// elected thread refills the slots vacated by plane k-1 at the start of step
+// k, keeping DEPTH planes beyond the ones being read in flight in both rings
+// (the halo-free fields do not occupy the three extra slots the z-window
+// needs, which leaves the shared memory for deeper prefetch or more blocks).
 //
 // A thread owns TILE_X consecutive columns (TILE_X in {1, 2, 4}; CONTIG_X)
 // times a strip of TILE_Y rows.  Per plane it evaluates TILE_X+1 x-faces
@@ -58,17 +61,23 @@ constexpr int kUB = rup(kBW * kBH * kS, 128);
 constexpr int kVB = rup(kVW * (kTYT + 1) * kS, 128);
 constexpr int kWB = rup(kVW * kTYT * kS, 128);
 constexpr int kTB = rup(kTW * kTYT * kS, 128);
-constexpr int kPB = kUB + kVB + kWB + kTB;  // bytes per plane slot
-constexpr int kPS = kPB / kS;
-constexpr int kVO = kUB / kS, kWO = (kUB + kVB) / kS, kTO = (kUB + kVB + kWB) / kS;  // field offsets in a slot
-constexpr int kNS = DEPTH + 4;
+// two rings: u planes (kNU slots: plane k feeds the x/y stencil of step k,
+// plane k+3 the z-window) and v/w/ut planes (kNV slots: step k reads v, ut
+// of plane k and w of plane k+1) — the halo-free fields are not kept for the
+// three extra planes the z-window needs
+constexpr int kNU = DEPTH + 4;
+constexpr int kNV = DEPTH + 2;
+constexpr int kUS = kUB / kS;                 // elements per u slot
+constexpr int kVS = (kVB + kWB + kTB) / kS;   // elements per v/w/ut slot
+constexpr int kVO = 0, kWO = kVB / kS, kTO = (kVB + kWB) / kS;  // field offsets in a v/w/ut slot
 // fp32 with column tiles: pairs of neighbouring columns share packed
 // FADD2/FMUL2/FFMA2 instructions (kl_pack.cuh)
 constexpr bool kPack = sizeof(real) == 4 && kTX >= 2;
 constexpr int kP = kTX / 2 > 0 ? kTX / 2 : 1;  // column pairs per thread
-constexpr unsigned kTxBytes =
-    static_cast<unsigned>((kBW * kBH + kVW * (kTYT + 1) + kVW * kTYT + kTW * kTYT) * kS);
+constexpr unsigned kTxU = static_cast<unsigned>(kBW * kBH * kS);
+constexpr unsigned kTxV = static_cast<unsigned>((kVW * (kTYT + 1) + kVW * kTYT + kTW * kTYT) * kS);
 static_assert(kBW <= 256 && kBH <= 256, "TMA box extents are limited to 256");
+static_assert(kNU + kNV <= 16, "mbarriers must fit the 128-byte header");
 
 template <int N>
 struct __align__(N * sizeof(real)) Pack {
@@ -108,42 +117,98 @@ struct AdvecTma {
   const real* rhoref;
   const real* rhorefh;
   const real* dzi;
-  real* ring;
-  unsigned long long* full;
+  real* ring_u;  // [kNU][kUS]
+  real* ring_v;  // [kNV][kVS]
+  const real* zprof;  // [ZCHUNK][2]: rhorefh[k+1], dzi[k] / (120 rhoref[k])
+  unsigned long long* bar_u;  // kNU mbarriers
+  unsigned long long* bar_v;  // kNV mbarriers
   const TmaDesc* maps;
   real dxi120, dyi120;
-  int j0, k0, k1, kmax, tid, iend, jend;
+  int j0, k0, k1, tid, iend, jend;
   int xu, xv, xw, xt;  // 16-byte aligned box starts
   int ic, lj0, uofs, vofs, wofs, tofs;
 
-  __device__ __forceinline__ void issue(int slot, int p) const {
-    unsigned long long* bar = full + slot;
-    real* dst = ring + slot * kPS;
-    kl::mbar_expect_tx(bar, kTxBytes);
-    kl::tma_load_3d(dst, maps + 0, bar, xu, j0 - 3, p);
+  __device__ __forceinline__ void issue_u(int slot, int p) const {
+    kl::mbar_expect_tx(bar_u + slot, kTxU);
+    kl::tma_load_3d(ring_u + slot * kUS, maps + 0, bar_u + slot, xu, j0 - 3, p);
+  }
+  __device__ __forceinline__ void issue_v(int slot, int p) const {
+    unsigned long long* bar = bar_v + slot;
+    real* dst = ring_v + slot * kVS;
+    kl::mbar_expect_tx(bar, kTxV);
     kl::tma_load_3d(dst + kVO, maps + 1, bar, xv, j0, p);
     kl::tma_load_3d(dst + kWO, maps + 2, bar, xw, j0, p);
     kl::tma_load_3d(dst + kTO, maps + 3, bar, xt, j0, p);
+  }
+  // first fills: u planes k0 .. k1+2 (the last the z-window reads), v/w/ut
+  // planes k0 .. k1 (w of plane k1 feeds the last step's top face)
+  __device__ __forceinline__ void prime() const {
+    for (int p = k0; p <= min(k0 + kNU - 1, k1 + 2); ++p) issue_u(p - k0, p);
+    for (int p = k0; p <= min(k0 + kNV - 1, k1); ++p) issue_v(p - k0, p);
+  }
+
+  // Ring positions at step k: slots of u planes k, k+3, k-1 and of v/w/ut
+  // planes k, k+1, k-1, with the barrier parities of the planes waited for.
+  struct Cursor {
+    int u0 = 0, u3 = 3, uprev = kNU - 1;
+    int v0 = 0, v1 = 1, vprev = kNV - 1;
+    unsigned ph_u3 = 0, ph_v1 = 0;
+  };
+  // Planes of step k: u (x/y stencil), u k+3 (z-window), v, w (plane k+1), ut.
+  struct Planes {
+    const real *xy, *zf, *vp, *wp, *tp;
+  };
+
+  // Planes read before the march: u k0..k0+2 (first read as x/y planes) and
+  // v/w/ut k0 (w of plane k0 feeds the prologue); every later u plane is
+  // first read as the z-window plane (k+3), every later v/w/ut plane as the
+  // w plane (k+1), and waited for there.
+  __device__ __forceinline__ void wait_first() const {
+    kl::mbar_wait(bar_u + 0, 0);
+    kl::mbar_wait(bar_u + 1, 0);
+    kl::mbar_wait(bar_u + 2, 0);
+    kl::mbar_wait(bar_v + 0, 0);
+  }
+
+  // Start of step k: refill the slots plane k-1 vacated, wait for the planes
+  // this step reads first, advance the cursor.
+  __device__ __forceinline__ Planes begin_step(int k, Cursor& c) const {
+    __syncthreads();  // every thread is done with plane k-1's slots
+    if (tid == 0 && k > k0) {
+      const int pu = k - 1 + kNU, pv = k - 1 + kNV;
+      kl::fence_proxy_async_smem();
+      if (pu <= k1 + 2) issue_u(c.uprev, pu);
+      if (pv <= k1) issue_v(c.vprev, pv);
+    }
+    kl::mbar_wait(bar_u + c.u3, c.ph_u3);
+    kl::mbar_wait(bar_v + c.v1, c.ph_v1);
+    Planes pl;
+    pl.xy = ring_u + c.u0 * kUS + uofs;             // u, plane k at (ic-4, j0+lj0)
+    pl.zf = ring_u + c.u3 * kUS + uofs + 4;         // u, plane k+3 at (ic, j0+lj0)
+    pl.vp = ring_v + c.v0 * kVS + kVO + vofs;       // v, plane k at (ic-4, j0+lj0)
+    pl.wp = ring_v + c.v1 * kVS + kWO + wofs;       // w, plane k+1 at (ic-4, j0+lj0)
+    pl.tp = ring_v + c.v0 * kVS + kTO + tofs;       // ut, plane k at (ic, j0+lj0)
+    c.uprev = c.u0;
+    c.u0 = c.u0 + 1 == kNU ? 0 : c.u0 + 1;
+    c.u3 = c.u3 + 1 == kNU ? 0 : c.u3 + 1;
+    c.ph_u3 ^= c.u3 == 0 ? 1u : 0u;
+    c.vprev = c.v0;
+    c.v0 = c.v1;
+    c.v1 = c.v1 + 1 == kNV ? 0 : c.v1 + 1;
+    c.ph_v1 ^= c.v1 == 0 ? 1u : 0u;
+    return pl;
   }
 
   // main loop, VA = vector width of the shared-memory reads / ut stores
   template <int VA>
   __device__ __forceinline__ void march() const {
     constexpr long long K1 = KL_KK;
-    // per-plane z factors of the chunk, filled by the block after the ring's
-    // barrier init (one division per plane instead of one per thread and plane)
-    const real* zprof = ring + kNS * kPS;  // [ZCHUNK][2]: rhorefh[k+1], dzi[k] / (120 rhoref[k])
     real uq[kTY][kTX][6];  // u[k-2 .. k+3] of every cell (k+3 loaded at step k)
     real fz_bot[kTY][kTX];
-    // planes k0..k0+2 are first read as the x/y plane (k) or the w plane (k+1)
-    // of the first steps; every later plane is first read as the z-window
-    // plane (k+3) and waited for there.  Slots/parities advance incrementally.
-    kl::mbar_wait(full + 0, 0);
-    kl::mbar_wait(full + 1, 0);
-    kl::mbar_wait(full + 2, 0);
+    wait_first();
     {
       const real rh0 = rhorefh[k0];
-      const real* wp = ring + kWO + wofs;  // slot 0 = plane k0
+      const real* wp = ring_v + kWO + wofs;  // v/w/ut slot 0 = plane k0
 #pragma unroll
       for (int t = 0; t < kTY; ++t) {
         const int j = min(j0 + lj0 + t, jend - 1);
@@ -163,32 +228,13 @@ struct AdvecTma {
       }
     }
 
-    int s0 = 0, s1 = 1, s3 = 3, sprev = kNS - 1;  // slots of planes k, k+1, k+3, k-1
-    unsigned ph3 = 0;                              // barrier parity of plane k+3
+    Cursor cur;
     for (int k = k0; k < k1; ++k) {
-      __syncthreads();  // plane k-1's slot is free
-      if (tid == 0) {
-        const int p = k - 1 + kNS;
-        if (k > k0 && p <= kmax) {
-          kl::fence_proxy_async_smem();
-          issue(sprev, p);
-        }
-      }
-      kl::mbar_wait(full + s3, ph3);
-      const real* sk = ring + s0 * kPS;
-      const real* xy = sk + uofs;                       // u, plane k at (ic-4, j0+lj0)
-      const real* zf = ring + s3 * kPS + uofs + 4;      // u, plane k+3 at (ic, j0+lj0)
-      const real* vp = sk + kVO + vofs;                 // v, plane k at (ic-4, j0+lj0)
-      const real* wp = ring + s1 * kPS + kWO + wofs;    // w, plane k+1 at (ic-4, j0+lj0)
-      const real* tp = sk + kTO + tofs;                 // ut, plane k at (ic, j0+lj0)
+      const Planes pl = begin_step(k, cur);
+      const real *xy = pl.xy, *zf = pl.zf, *vp = pl.vp, *wp = pl.wp, *tp = pl.tp;
       const real rh_top = zprof[2 * (k - k0)];
       const real zfac120 = zprof[2 * (k - k0) + 1];
       const long long kofs = static_cast<long long>(k) * K1;
-      sprev = s0;
-      s0 = s1;
-      s1 = s1 + 1 == kNS ? 0 : s1 + 1;
-      s3 = s3 + 1 == kNS ? 0 : s3 + 1;
-      ph3 ^= s3 == 0 ? 1u : 0u;
 
       // u along y in this thread's columns: rows lj0-3 .. lj0+kTY+2
       real ucol[kTY + 6][kTX];
@@ -278,15 +324,12 @@ struct AdvecTma {
   __device__ __forceinline__ void march2() const {
     using kl::f2;
     constexpr long long K1 = KL_KK;
-    const real* zprof = ring + kNS * kPS;  // [ZCHUNK][2]: rhorefh[k+1], dzi[k] / (120 rhoref[k])
     f2 uq[kTY][kP][6];  // u[k-2 .. k+3] of every column pair
     f2 fz_bot[kTY][kP];
-    kl::mbar_wait(full + 0, 0);
-    kl::mbar_wait(full + 1, 0);
-    kl::mbar_wait(full + 2, 0);
+    wait_first();
     {
       const f2 rh0(rhorefh[k0]);
-      const real* wp = ring + kWO + wofs;  // slot 0 = plane k0
+      const real* wp = ring_v + kWO + wofs;  // v/w/ut slot 0 = plane k0
 #pragma unroll
       for (int t = 0; t < kTY; ++t) {
         const int j = min(j0 + lj0 + t, jend - 1);
@@ -309,32 +352,13 @@ struct AdvecTma {
     }
     const f2 dx2(dxi120), dy2(dyi120);
 
-    int s0 = 0, s1 = 1, s3 = 3, sprev = kNS - 1;  // slots of planes k, k+1, k+3, k-1
-    unsigned ph3 = 0;                              // barrier parity of plane k+3
+    Cursor cur;
     for (int k = k0; k < k1; ++k) {
-      __syncthreads();  // plane k-1's slot is free
-      if (tid == 0) {
-        const int p = k - 1 + kNS;
-        if (k > k0 && p <= kmax) {
-          kl::fence_proxy_async_smem();
-          issue(sprev, p);
-        }
-      }
-      kl::mbar_wait(full + s3, ph3);
-      const real* sk = ring + s0 * kPS;
-      const real* xy = sk + uofs;                     // u, plane k at (ic-4, j0+lj0)
-      const real* zf = ring + s3 * kPS + uofs + 4;    // u, plane k+3 at (ic, j0+lj0)
-      const real* vp = sk + kVO + vofs;               // v, plane k at (ic-4, j0+lj0)
-      const real* wp = ring + s1 * kPS + kWO + wofs;  // w, plane k+1 at (ic-4, j0+lj0)
-      const real* tp = sk + kTO + tofs;               // ut, plane k at (ic, j0+lj0)
+      const Planes pl = begin_step(k, cur);
+      const real *xy = pl.xy, *zf = pl.zf, *vp = pl.vp, *wp = pl.wp, *tp = pl.tp;
       const f2 rh_top(zprof[2 * (k - k0)]);
       const f2 zfac(zprof[2 * (k - k0) + 1]);
       const long long kofs = static_cast<long long>(k) * K1;
-      sprev = s0;
-      s0 = s1;
-      s1 = s1 + 1 == kNS ? 0 : s1 + 1;
-      s3 = s3 + 1 == kNS ? 0 : s3 + 1;
-      ph3 ^= s3 == 0 ? 1u : 0u;
 
       // u along y in this thread's columns: rows lj0-3 .. lj0+kTY+2
       real ucol[kTY + 6][kTX];
@@ -468,8 +492,10 @@ KL_ENTRY(real* __restrict__ ut, const real* __restrict__ u, const real* __restri
   const TmaDesc* const maps = &tma.map[0];
   extern __shared__ __align__(128) unsigned char kl_smem_raw[];
   unsigned char* sbase = kl_smem_raw + ((128u - (kl::smem_u32(kl_smem_raw) & 127u)) & 127u);
-  unsigned long long* full = reinterpret_cast<unsigned long long*>(sbase);
-  real* const ring = reinterpret_cast<real*>(sbase + 128);  // [kNS][kPS]
+  unsigned long long* bars = reinterpret_cast<unsigned long long*>(sbase);  // kNU + kNV <= 16 mbarriers
+  real* const ring_u = reinterpret_cast<real*>(sbase + 128);                 // [kNU][kUS]
+  real* const ring_v = ring_u + kNU * kUS;                                    // [kNV][kVS]
+  real* const zprof = ring_v + kNV * kVS;                                     // [ZCHUNK][2]
 
   const unsigned nbx = kl::ceil_div(iend - istart, kXT);
   const unsigned nby = kl::ceil_div(jend - jstart, kTYT);
@@ -493,15 +519,17 @@ KL_ENTRY(real* __restrict__ ut, const real* __restrict__ u, const real* __restri
   m.rhoref = rhoref;
   m.rhorefh = rhorefh;
   m.dzi = dzi;
-  m.ring = ring;
-  m.full = full;
+  m.ring_u = ring_u;
+  m.ring_v = ring_v;
+  m.zprof = zprof;
+  m.bar_u = bars;
+  m.bar_v = bars + kNU;
   m.maps = maps;
   m.dxi120 = dxi * real(1.0 / 120.0);
   m.dyi120 = dyi * real(1.0 / 120.0);
   m.j0 = j0;
   m.k0 = k0;
   m.k1 = k1;
-  m.kmax = k1 + 2;  // last plane the z-window reads
   m.tid = tid;
   m.iend = iend;
   m.jend = jend;
@@ -517,19 +545,14 @@ KL_ENTRY(real* __restrict__ ut, const real* __restrict__ u, const real* __restri
   m.tofs = sh_t + m.lj0 * kTW + kTX * threadIdx.x;        // (ic, j0+lj0) in the ut box
 
   if (tid == 0) {
-    for (int s = 0; s < kNS; ++s) kl::mbar_init(full + s, 1);
+    for (int s = 0; s < kNU + kNV; ++s) kl::mbar_init(bars + s, 1);
     kl::mbar_init_fence();
   }
   __syncthreads();
-  if (tid == 0) {
-    for (int p = k0; p <= min(k0 + kNS - 1, m.kmax); ++p) m.issue(p - k0, p);
-  }
-  {
-    real* zprof = ring + kNS * kPS;
-    for (int q = tid; q < k1 - k0; q += KL_THREADS) {
-      zprof[2 * q] = rhorefh[k0 + q + 1];
-      zprof[2 * q + 1] = dzi[k0 + q] / (rhoref[k0 + q] * real(120));
-    }
+  if (tid == 0) m.prime();
+  for (int q = tid; q < k1 - k0; q += KL_THREADS) {
+    zprof[2 * q] = rhorefh[k0 + q + 1];
+    zprof[2 * q + 1] = dzi[k0 + q] / (rhoref[k0 + q] * real(120));
   }
   // (the march's first __syncthreads publishes zprof)
   if (kVA > 1 && (sh_u | sh_v | sh_w | sh_t) == 0) {

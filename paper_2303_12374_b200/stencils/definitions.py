@@ -196,11 +196,11 @@ _SMEM = {
 }
 
 
-# TMA ring: 128 B alignment slack + 128 B of mbarriers + ring slots of 128-B
+# TMA rings: 128 B alignment slack + 128 B of mbarriers + ring slots of 128-B
 # aligned field-planes (diff_uvw: depth+2 slots x (4 halo'd + 3 tendency)
-# fields; advec_u: depth+4 slots of u (3-halo) + v, w, ut, since plane k+3
-# feeds the z-window); box width = block_x + halo
-# plus up to one 16-byte chunk of alignment slack, rounded to 16 B.
+# fields; advec_u: depth+4 slots of u (3-halo; plane k+3 feeds the z-window)
+# and depth+2 slots of v, w, ut); box width = columns + halo plus up to one
+# 16-byte chunk of alignment slack, rounded to 16 B.
 _BW = "(ceil_div(({X} + {H}) * {S} + 16 - {S}, 16) * 16 / {S})"
 _ADVEC_BOX = "ceil_div(" + _BW + " * (block_y * tile_y + {R}) * {S}, 128) * 128"
 _SMEM_TMA = {
@@ -211,8 +211,10 @@ _SMEM_TMA = {
                 " * (block_y * tile_y), 128) * 128) + 5 * zchunk * {S})",
     # advec_u boxes start at column i0-4: u (x halo 4+4, y halo 3+3), v (4 + 1 row), w (4), ut (0)
     # plus the chunk's z factors (2 per plane)
-    "advec_u": "(256 + (depth + 4) * (" + " + ".join(
-        _ADVEC_BOX.format(X="block_x * tile_x", H=h, R=r, S="{S}") for h, r in ((8, 6), (4, 1), (4, 0), (0, 0))) +
+    # in two rings: u in depth+4 slots, v/w/ut in depth+2 slots (advec_u_tma.cuh)
+    "advec_u": "(256 + (depth + 4) * " + _ADVEC_BOX.format(X="block_x * tile_x", H=8, R=6, S="{S}") +
+    " + (depth + 2) * (" + " + ".join(
+        _ADVEC_BOX.format(X="block_x * tile_x", H=h, R=r, S="{S}") for h, r in ((4, 1), (4, 0), (0, 0))) +
     ") + 2 * zchunk * {S})",
 }
 
