@@ -93,9 +93,13 @@ class SlabDriver:
             after = self._ev_start.record(self.compute)
         self.comm.wait(after)
         lay = self.layout
-        for field, (down, up) in HALO_REACH[self.kernel].items():
-            self.exchanger.exchange(self.comm, [self.problem.field_ptr(field)], lay.elem_bytes, lay.kk, lay.kstart,
-                                    lay.kend, down, up, self.below, self.above)
+        # fields with the same reach share one NCCL group (diff_uvw: all four)
+        groups: dict[tuple[int, int], list[int]] = {}
+        for field, reach in HALO_REACH[self.kernel].items():
+            groups.setdefault(reach, []).append(self.problem.field_ptr(field))
+        for (down, up), ptrs in groups.items():
+            self.exchanger.exchange(self.comm, ptrs, lay.elem_bytes, lay.kk, lay.kstart, lay.kend, down, up,
+                                    self.below, self.above)
         self._ev_halo.record(self.comm)
 
     def step(self, time_kernel: tuple[Event, Event] | None = None) -> int:
