@@ -24,7 +24,15 @@ from .backend import STATUS_OK
 from .tuner import Budget, save_session, tune
 from .wisdom import append_result, load_or_create, wisdom_path
 
-__all__ = ["tune_problem", "main"]
+__all__ = ["tune_problem", "main", "FOCUSED_TMA"]
+
+#: The focused TMA sub-space the wisdom sessions enumerate exhaustively: XYZ
+#: launch order (y-neighbour blocks run together, so their shared halo rows
+#: are L2 hits — measured 20% faster than the other orders on diff_uvw
+#: 1024^3), no register cap, zchunk 32..128, prefetch depth 1..2, every block
+#: shape and thread tile of at least 32 columns.
+FOCUSED_TMA = ('unravel == "XYZ" && min_blocks == 1 && (zchunk == 32 || zchunk == 64 || zchunk == 128) && '
+               'depth <= 2 && block_x * tile_x >= 32')
 
 
 def tune_problem(kernel: str, precision: str, grid: tuple[int, int, int], ctx, *, strategy: str = "random",
@@ -56,7 +64,7 @@ def tune_problem(kernel: str, precision: str, grid: tuple[int, int, int], ctx, *
     if family:
         from .stencils.definitions import family_space
 
-        space = family_space(kernel, family)
+        space = family_space(kernel, family, precision)
     if restrict:
         # explore a sub-space (e.g. 'staging == "ZMARCH"'); every point is valid in the
         # full space, so the session still feeds the kernel's real wisdom file
@@ -116,6 +124,7 @@ def main(argv=None) -> int:
     ap.add_argument("--device", type=int, default=0)
     ap.add_argument("--json-out", default=None)
     ap.add_argument("--restrict", default=None, help="extra restriction expression to explore a sub-space")
+    ap.add_argument("--focused", action="store_true", help="restrict to FOCUSED_TMA (with --family TMA)")
     ap.add_argument("--family", choices=("DIRECT", "ZMARCH", "TMA"), default=None,
                     help="tune one staging family (its fixed knobs narrowed; see definitions.family_space)")
     a = ap.parse_args(argv)
@@ -123,9 +132,10 @@ def main(argv=None) -> int:
 
     ctx = open_device(a.device)
     grid = tuple(int(x) for x in a.grid.split(","))
+    restrict = FOCUSED_TMA if a.focused else a.restrict
     _, summary = tune_problem(a.kernel, a.precision, grid, ctx, strategy=a.strategy,
                               budget=Budget(a.budget_evals, a.budget_seconds), seed=a.seed, wisdom_dir=a.wisdom,
-                              session_dir=a.sessions, restrict=a.restrict, family=a.family)
+                              session_dir=a.sessions, restrict=restrict, family=a.family)
     line = json.dumps(summary, sort_keys=True)
     print(line)
     if a.json_out:

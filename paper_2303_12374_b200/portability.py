@@ -32,15 +32,19 @@ QUERIES = (192, 384, 768)
 
 
 def _tune(kernel, precision, n, ctx, wdir, evals, log):
-    from .autotune import tune_problem
+    """Per-shape optimum the way the wisdom files are made: an exhaustive
+    session over the focused TMA sub-space plus a short random DIRECT one
+    (keep-best merges them into ``wdir``)."""
+    from .autotune import FOCUSED_TMA, tune_problem
 
     sessions = []
-    for family, share in (("DIRECT", 0.3), ("TMA", 0.7)):
-        s, summary = tune_problem(kernel, precision, (n, n, n), ctx, strategy="random",
-                                  budget=Budget(max(4, int(evals * share)), 300.0), seed=n, wisdom_dir=wdir,
-                                  family=family, log=lambda *_: None)
+    for family, strategy, restrict, budget in (("TMA", "exhaustive", FOCUSED_TMA, Budget(4000, 900.0)),
+                                               ("DIRECT", "random", None, Budget(max(4, evals // 4), 300.0))):
+        s, summary = tune_problem(kernel, precision, (n, n, n), ctx, strategy=strategy, budget=budget, seed=n,
+                                  wisdom_dir=wdir, family=family, restrict=restrict, log=lambda *_: None)
         sessions.append(s)
-        log(f"  tuned {kernel} {precision} {n}^3 {family}: {summary.get('best_gbs', 0):.0f} GB/s")
+        log(f"  tuned {kernel} {precision} {n}^3 {family}: {summary.get('best_gbs', 0):.0f} GB/s "
+            f"({summary['evaluations']} evaluations)")
     return sessions
 
 
