@@ -41,7 +41,7 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 METRIC = "Gcells/s and achieved HBM GB/s (% of roofline), tuned vs default, 1/2/4/8 B200"
-WORDS = {"advec_u": 5, "diff_uvw": 10}
+from paper_2303_12374_b200.stencils.problem import BYTES_PER_CELL_WORDS as WORDS  # noqa: E402
 WORKLOADS = {
     "diff_uvw_fp32_1024": ("diff_uvw", "fp32", (1024, 1024, 1024),
                            "BASELINE config 4: diff_uvw fp32 1024^3, z-slab decomposed over N GPUs, NVLink halo exchange"),

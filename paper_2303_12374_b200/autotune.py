@@ -75,7 +75,9 @@ def tune_problem(kernel: str, precision: str, grid: tuple[int, int, int], ctx, *
                    seed=seed, device=ctx.ident, kernel_key=prob.definition.kernel_key(),
                    problem=executor.problem, on_evaluation=progress)
     cells = executor.problem[0] * executor.problem[1] * executor.problem[2]
-    words = {"advec_u": 5, "diff_uvw": 10}[kernel]
+    from .stencils.problem import BYTES_PER_CELL_WORDS
+
+    words = BYTES_PER_CELL_WORDS[kernel]
     summary = {
         "kernel": kernel, "precision": precision, "grid": list(grid), "problem": list(executor.problem),
         "evaluations": len(session.evaluations), "ok": len(session.ok_evaluations()),
@@ -112,7 +114,9 @@ def _short(cfg: dict) -> str:
 
 def main(argv=None) -> int:
     ap = argparse.ArgumentParser(prog="python -m paper_2303_12374_b200.autotune")
-    ap.add_argument("--kernel", choices=("advec_u", "diff_uvw"), required=True)
+    from .stencils.definitions import ALL_KERNELS
+
+    ap.add_argument("--kernel", choices=ALL_KERNELS, required=True)
     ap.add_argument("--precision", choices=("fp32", "fp64"), default="fp32")
     ap.add_argument("--grid", default="256,256,256")
     ap.add_argument("--strategy", choices=("random", "surrogate", "exhaustive"), default="random")

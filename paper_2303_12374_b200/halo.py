@@ -28,6 +28,7 @@ implement the same plan in Python.
 Reach per kernel (from the stencil definitions):
   advec_u : u (down 3, up 3), w (down 1, up 0), v none
   diff_uvw: evisc, u, v, w (down 1, up 1)
+  (the §8f family in HALO_REACH below, from oracle/family_oracle.py)
 """
 
 from __future__ import annotations
@@ -44,6 +45,11 @@ __all__ = [
 HALO_REACH = {
     "advec_u": {"u": (3, 3), "w": (1, 0)},
     "diff_uvw": {"evisc": (1, 1), "u": (1, 1), "v": (1, 1), "w": (1, 1)},
+    "advec_v": {"v": (3, 3), "w": (1, 0)},
+    "advec_w": {"w": (3, 3), "u": (0, 1), "v": (0, 1)},
+    "advec_s": {"s": (3, 3), "w": (1, 0)},
+    "diff_c": {"s": (1, 1), "evisc": (1, 1)},
+    "evisc_smag": {"u": (1, 1), "v": (1, 1), "w": (1, 0)},
 }
 
 

@@ -38,12 +38,15 @@ from ..space import ConfigSpace, TunableParam
 
 __all__ = [
     "KERNELS", "PRECISIONS", "stencil_space", "advec_u_definition", "diff_uvw_definition", "definition_for",
-    "assemble_source", "ARG_LAYOUT", "family_space", "FAMILY_PINS",
+    "assemble_source", "ARG_LAYOUT", "family_space", "FAMILY_PINS", "FAMILY_KERNELS", "ALL_KERNELS",
 ]
 
 _HERE = Path(__file__).resolve().parent
 PRECISIONS = {"fp32": "float", "fp64": "double"}
 KERNELS = ("advec_u", "diff_uvw")
+#: the rest of the MicroHH stencil family: DIRECT staging
+FAMILY_KERNELS = ("advec_v", "advec_w", "advec_s", "diff_c", "evisc_smag")
+ALL_KERNELS = KERNELS + FAMILY_KERNELS
 
 STAGING_VALUES = ("DIRECT", "ZMARCH", "TMA")
 DEPTH_VALUES = (0, 1, 2, 3)
@@ -61,6 +64,31 @@ ARG_LAYOUT = {
                     ("v", "input"), ("w", "input"), ("dzi", "input"), ("dzhi", "input"), ("rhoref", "input"),
                     ("rhorefh", "input")],
         "scalars": ["dxi", "dyi", "jj", "kk", "istart", "jstart", "kstart", "iend", "jend", "kend"],
+    },
+    "advec_v": {
+        "buffers": [("vt", "output"), ("u", "input"), ("v", "input"), ("w", "input"),
+                    ("rhoref", "input"), ("rhorefh", "input"), ("dzi", "input")],
+        "scalars": ["dxi", "dyi", "jj", "kk", "istart", "jstart", "kstart", "iend", "jend", "kend"],
+    },
+    "advec_w": {
+        "buffers": [("wt", "output"), ("u", "input"), ("v", "input"), ("w", "input"),
+                    ("rhoref", "input"), ("rhorefh", "input"), ("dzhi", "input")],
+        "scalars": ["dxi", "dyi", "jj", "kk", "istart", "jstart", "kstart", "iend", "jend", "kend"],
+    },
+    "advec_s": {
+        "buffers": [("st", "output"), ("s", "input"), ("u", "input"), ("v", "input"), ("w", "input"),
+                    ("rhoref", "input"), ("rhorefh", "input"), ("dzi", "input")],
+        "scalars": ["dxi", "dyi", "jj", "kk", "istart", "jstart", "kstart", "iend", "jend", "kend"],
+    },
+    "diff_c": {
+        "buffers": [("st", "output"), ("s", "input"), ("evisc", "input"), ("dzi", "input"), ("dzhi", "input"),
+                    ("rhoref", "input"), ("rhorefh", "input")],
+        "scalars": ["dxi", "dyi", "tpri", "jj", "kk", "istart", "jstart", "kstart", "iend", "jend", "kend"],
+    },
+    "evisc_smag": {
+        "buffers": [("evisc", "output"), ("u", "input"), ("v", "input"), ("w", "input"), ("dzi", "input"),
+                    ("dzhi", "input")],
+        "scalars": ["dxi", "dyi", "cs", "jj", "kk", "istart", "jstart", "kstart", "iend", "jend", "kend"],
     },
 }
 
@@ -91,7 +119,7 @@ def _inline(path: Path, depth: int = 0) -> str:
 @lru_cache(maxsize=None)
 def assemble_source(kernel: str, precision: str) -> str:
     """Self-contained NVRTC source: precision/entry prelude + inlined headers."""
-    if kernel not in KERNELS or precision not in PRECISIONS:
+    if kernel not in ALL_KERNELS or precision not in PRECISIONS:
         raise ValueError(f"unknown kernel/precision {kernel}/{precision}")
     prelude = (
         f"// {kernel} ({precision}) — B200 Kernel Launcher stencil, runtime-compiled by NVRTC\n"
@@ -134,6 +162,11 @@ def stencil_space(kernel: str = "advec_u", precision: str = "fp32") -> ConfigSpa
     (shared-memory limits depend on the element size, so the fp32 and fp64
     spaces — and their fingerprints — may differ)."""
     size = 4 if precision == "fp32" else 8
+    if kernel in FAMILY_KERNELS:
+        # DIRECT staging only: the B200 knobs are pinned, the Table-2 space is the search space
+        params = table2_params() + [TunableParam("staging", ("DIRECT",), "DIRECT"),
+                                    TunableParam("zchunk", (1,), 1), TunableParam("depth", (0,), 0)]
+        return ConfigSpace(params, [BLOCK_LIMIT_RESTRICTION])
     params = table2_params() + [
         TunableParam("staging", STAGING_VALUES, "DIRECT"),
         TunableParam("zchunk", ZCHUNK_VALUES, 1),
@@ -245,7 +278,8 @@ def _definition(kernel: str, precision: str) -> KernelDefinition:
         problem_size=(f"{p('iend')} - {p('istart')}", f"{p('jend')} - {p('jstart')}", f"{p('kend')} - {p('kstart')}"),
         block=("block_x", "block_y", "block_z"),
         grid=(grid_x, 1, 1),
-        shared_mem=(f"min(zchunk - 1, 1) * ((1 - min(depth, 1)) * {_SMEM[kernel].format(S=size)}"
+        shared_mem=("0" if kernel in FAMILY_KERNELS else
+                    f"min(zchunk - 1, 1) * ((1 - min(depth, 1)) * {_SMEM[kernel].format(S=size)}"
                     f" + min(depth, 1) * {_SMEM_TMA[kernel].format(S=size)})"),
         defines=defines,
         flags=("-std=c++17",),

@@ -27,6 +27,8 @@ FIELD_SPECS = {
     "vt": (4, -1.0, 1.0),
     "wt": (5, -1.0, 1.0),
     "evisc": (6, 0.01, 0.1),
+    "s": (7, -1.0, 1.0),
+    "st": (8, -1.0, 1.0),
 }
 _PROFILE_SEED_OFFSET = 100
 

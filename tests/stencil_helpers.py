@@ -4,10 +4,10 @@ from __future__ import annotations
 
 import numpy as np
 
-from oracle import stencil_oracle
+from oracle import family_oracle, stencil_oracle
 from oracle.synth import synth_field
 from paper_2303_12374_b200.stencils.layout import GridLayout
-from paper_2303_12374_b200.stencils.problem import KERNEL_FIELDS, StencilProblem
+from paper_2303_12374_b200.stencils.problem import CS, KERNEL_FIELDS, TPRI, StencilProblem
 from paper_2303_12374_b200.stencils.profiles import FIELD_SEED_BASE, FIELD_SPECS, make_profiles
 
 TOL = {"fp32": 1e-5, "fp64": 1e-12}
@@ -30,6 +30,21 @@ def oracle_outputs(kernel: str, layout: GridLayout, dxi=1.0, dyi=1.0, k_range=No
     if kernel == "advec_u":
         res = {"ut": stencil_oracle.advec_u(f["ut"], f["u"], f["v"], f["w"], prof.rhoref, prof.rhorefh, prof.dzi, dxi,
                                              dyi, ghost=g)}
+    elif kernel == "advec_v":
+        res = {"vt": family_oracle.advec_v(f["vt"], f["u"], f["v"], f["w"], prof.rhoref, prof.rhorefh, prof.dzi, dxi,
+                                           dyi, ghost=g)}
+    elif kernel == "advec_w":
+        res = {"wt": family_oracle.advec_w(f["wt"], f["u"], f["v"], f["w"], prof.rhoref, prof.rhorefh, prof.dzhi,
+                                           dxi, dyi, ghost=g)}
+    elif kernel == "advec_s":
+        res = {"st": family_oracle.advec_s(f["st"], f["s"], f["u"], f["v"], f["w"], prof.rhoref, prof.rhorefh,
+                                           prof.dzi, dxi, dyi, ghost=g)}
+    elif kernel == "diff_c":
+        res = {"st": family_oracle.diff_c(f["st"], f["s"], f["evisc"], prof.dzi, prof.dzhi, prof.rhoref,
+                                          prof.rhorefh, dxi, dyi, TPRI, ghost=g)}
+    elif kernel == "evisc_smag":
+        res = {"evisc": family_oracle.evisc_smag(f["evisc"], f["u"], f["v"], f["w"], prof.dzi, prof.dzhi, dxi, dyi,
+                                                 CS, ghost=g)}
     else:
         ut, vt, wt = stencil_oracle.diff_uvw(f["ut"], f["vt"], f["wt"], f["evisc"], f["u"], f["v"], f["w"], prof.dzi,
                                              prof.dzhi, prof.rhoref, prof.rhorefh, dxi, dyi, ghost=g)

@@ -1,0 +1,56 @@
+"""GPU parity of the rest of the MicroHH stencil family (SURVEY §8f row 2:
+advec_v, advec_w, advec_s, diff_c, evisc_smag) against the NumPy restatement
+(oracle/family_oracle.py), through the same NVRTC / C-ABI launch path as the
+hot-path kernels.  Bar: max|gpu - ref| / max|ref| <= 1e-5 (fp32), 1e-12 (fp64)."""
+
+import numpy as np
+import pytest
+
+from stencil_helpers import TOL, oracle_outputs, rel_error, run_config
+
+pytestmark = pytest.mark.gpu
+
+FAMILY = ["advec_v", "advec_w", "advec_s", "diff_c", "evisc_smag"]
+
+
+@pytest.fixture(scope="module")
+def compiler(gpu_ctx):
+    from paper_2303_12374_b200.cuda import NvrtcCompiler
+
+    return NvrtcCompiler(gpu_ctx)
+
+
+def _space(kernel, precision):
+    from paper_2303_12374_b200.stencils.definitions import definition_for
+
+    return definition_for(kernel, precision).space
+
+
+@pytest.mark.parametrize("kernel", FAMILY)
+@pytest.mark.parametrize("precision", ["fp32", "fp64"])
+def test_family_default_and_sampled_configs_match_oracle(gpu_ctx, compiler, kernel, precision):
+    from paper_2303_12374_b200.stencils.layout import GridLayout
+
+    lay = GridLayout(45, 23, 19, precision)
+    ref, _ = oracle_outputs(kernel, lay)
+    space = _space(kernel, precision)
+    cfgs = [space.default_config()[0]] + space.sample_random(5 if precision == "fp32" else 6, 4)
+    for cfg in cfgs:
+        got = run_config(gpu_ctx, compiler, kernel, lay, cfg)
+        for name in ref:
+            err = rel_error(got[name], ref[name], lay)
+            assert err <= TOL[precision], (cfg, name, err)
+
+
+@pytest.mark.parametrize("kernel", FAMILY)
+def test_family_k_subrange_launch(gpu_ctx, compiler, kernel):
+    from paper_2303_12374_b200.stencils.layout import GridLayout
+
+    lay = GridLayout(32, 24, 20, "fp64")
+    kr = (lay.kstart + 4, lay.kstart + 13)
+    ref, _ = oracle_outputs(kernel, lay, k_range=kr)
+    cfg = dict(_space(kernel, "fp64").default_config()[0], block_x=32, block_y=4, tile_z=2, contiguous_z=True)
+    got = run_config(gpu_ctx, compiler, kernel, lay, cfg, k_range=kr)
+    for name in ref:
+        diff = np.max(np.abs(got[name].astype(np.float64) - ref[name]))
+        assert diff <= 1e-12 * np.max(np.abs(ref[name])), (name, diff)

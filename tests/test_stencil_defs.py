@@ -16,8 +16,9 @@ def scalars(kernel, lay):
     vals = dict(dxi=1.0, dyi=1.0, jj=lay.jj, kk=lay.kk, istart=lay.istart, jstart=lay.jstart, kstart=lay.kstart,
                 iend=lay.iend, jend=lay.jend, kend=lay.kend)
     out = []
+    vals.update(tpri=3.0, cs=0.23)
     for i, n in enumerate(ARG_LAYOUT[kernel]["scalars"]):
-        out.append(ScalarArg(nb + i, "f32" if n in ("dxi", "dyi") else "i32", vals[n]))
+        out.append(ScalarArg(nb + i, "f32" if n in ("dxi", "dyi", "tpri", "cs") else "i32", vals[n]))
     return out
 
 
@@ -126,3 +127,29 @@ def test_nvrtc_compiles_column_tiles(kernel):
             reqs.append(d.render_compile_request(cfg, problem, env))
         for fut in comp.compile_many(reqs, B200):
             assert len(fut.result().cubin) > 1000
+
+
+@pytest.mark.parametrize("kernel", ["advec_v", "advec_w", "advec_s", "diff_c", "evisc_smag"])
+def test_family_kernels_compile_and_key_by_precision(kernel):
+    """The §8f family: Table-2 DIRECT space, precision in the kernel key,
+    NVRTC compiles sampled configurations for sm_100a."""
+    from paper_2303_12374_b200.cuda._abi import library_path
+    from paper_2303_12374_b200.cuda.compiler import NvrtcCompiler
+
+    keys = {definition_for(kernel, p).kernel_key() for p in PRECISIONS}
+    assert len(keys) == 2
+    if not library_path().exists():
+        pytest.skip("libklb200.so not built")
+    comp = NvrtcCompiler()
+    reqs = []
+    for precision in PRECISIONS:
+        d = definition_for(kernel, precision)
+        assert d.space.default_config()[0]["staging"] == "DIRECT"
+        lay = GridLayout(40, 24, 16, precision)
+        env = scalar_env_from_args(scalars(kernel, lay))
+        problem = d.derive_problem_size(env)
+        assert problem == (40, 24, 16)
+        for cfg in [d.space.default_config()[0]] + d.space.sample_random(2, 2):
+            reqs.append(d.render_compile_request(cfg, problem, env))
+    for fut in comp.compile_many(reqs, B200):
+        assert fut.result().lowered_name.startswith(kernel)

@@ -75,7 +75,9 @@ def main(argv=None) -> int:
         k, vs = item.split("=", 1)
         knobs.append((k, [_parse_value(v) for v in vs.split(",")]))
     cells = grid[0] * grid[1] * grid[2]
-    words = {"advec_u": 5, "diff_uvw": 10}.get(a.kernel, 10)
+    from paper_2303_12374_b200.stencils.problem import BYTES_PER_CELL_WORDS
+
+    words = BYTES_PER_CELL_WORDS[a.kernel]
     configs = []
     for combo in itertools.product(*[vs for _, vs in knobs]):
         cfg = dict(base)
