@@ -54,7 +54,30 @@ SUITE = [
     ("advec_u", "fp32", (256, 256, 256), "config 2"),
     ("advec_u", "fp64", (512, 512, 512), "config 3"),
     ("diff_uvw", "fp64", (512, 512, 512), "config 3"),
+    ("advec_u", "fp32", (512, 512, 512), "north_star 512^3"),
+    ("diff_uvw", "fp32", (512, 512, 512), "north_star 512^3"),
 ]
+#: SURVEY §8f row 2 — the rest of the MicroHH family (DIRECT kernels), 512^3
+FAMILY_SUITE = [(k, p, (512, 512, 512), "§8f family") for k in ("advec_v", "advec_w", "advec_s", "diff_c", "evisc_smag")
+                for p in ("fp32", "fp64")]
+#: SURVEY §8f row 1 — the RK3 substep fused into diff_uvw's store vs diff_uvw + a separate RK3 pass
+FUSION_SUITE = [(k, p, (512, 512, 512), "§8f fusion") for p in ("fp32", "fp64")
+                for k in ("diff_uvw", "rk3_uvw", "diff_uvw_rk3")]
+
+
+def fusion_summary(rows):
+    """Fused (diff_uvw_rk3) vs unfused (diff_uvw + rk3_uvw) per precision, tuned configs."""
+    out = []
+    by = {(r["kernel"], r["precision"]): r for r in rows if isinstance(r, dict) and "tuned" in r}
+    for p in ("fp32", "fp64"):
+        try:
+            fused = by["diff_uvw_rk3", p]["tuned"]["us"]
+            unfused = by["diff_uvw", p]["tuned"]["us"] + by["rk3_uvw", p]["tuned"]["us"]
+        except KeyError:
+            continue
+        out.append({"precision": p, "fused_us": fused, "unfused_us": round(unfused, 2),
+                    "speedup": round(unfused / fused, 3), "words_per_cell": {"fused": 13, "unfused": 22}})
+    return out
 
 
 def env_int(name, default):
@@ -379,8 +402,9 @@ def ncu_traffic(kernel_key_prefix):
     return None, None
 
 
-def suite_measure(ctx, compiler, wisdom_dir, peak):
-    """BASELINE configs 1-3 on one GPU: tuned (wisdom) vs default, L2 flushed per rep."""
+def suite_measure(ctx, compiler, wisdom_dir, peak, suite=SUITE):
+    """BASELINE configs 1-3 (+ the north_star 512^3 fp32 pair) on one GPU:
+    tuned (wisdom) vs default, L2 flushed per rep."""
     from paper_2303_12374_b200.capture import CapturePolicy
     from paper_2303_12374_b200.dispatch import WisdomKernel
     from paper_2303_12374_b200.stencils.layout import GridLayout
@@ -389,7 +413,7 @@ def suite_measure(ctx, compiler, wisdom_dir, peak):
     rows = []
     empty = ROOT / "build" / "empty_wisdom"
     empty.mkdir(parents=True, exist_ok=True)
-    for kernel, precision, grid, tag in SUITE:
+    for kernel, precision, grid, tag in suite:
         lay = GridLayout(*grid, precision)
         prob = StencilProblem(kernel, lay, ctx)
         row = {"config": tag, "kernel": kernel, "precision": precision, "grid": list(grid)}
@@ -516,6 +540,15 @@ def run_ours(args, dist):
             line["suite"] = suite_measure(ctx, compiler, wisdom_dir, peak)
         except Exception as err:
             line["suite"] = {"error": repr(err)[:300]}
+        try:
+            line["family"] = suite_measure(ctx, compiler, wisdom_dir, peak, FAMILY_SUITE)
+        except Exception as err:
+            line["family"] = {"error": repr(err)[:300]}
+        try:
+            rows = suite_measure(ctx, compiler, wisdom_dir, peak, FUSION_SUITE)
+            line["fusion"] = {"rows": rows, "summary": fusion_summary(rows)}
+        except Exception as err:
+            line["fusion"] = {"error": repr(err)[:300]}
     driver.close()
     if exchanger is not None:
         exchanger.close()

@@ -28,7 +28,7 @@ import numpy as np
 
 from .stencil_oracle import _box, _flux, interp2
 
-__all__ = ["advec_v", "advec_w", "advec_s", "diff_c", "evisc_smag", "strain2"]
+__all__ = ["advec_v", "advec_w", "advec_s", "diff_c", "evisc_smag", "strain2", "rk3_uvw", "diff_uvw_rk3"]
 
 
 def _setup(fields, ghost, interior):
@@ -160,3 +160,36 @@ def evisc_smag(evisc, u, v, w, dzi, dzhi, dxi, dyi, cs, ghost=(3, 3, 3), interio
     mlen = np.cbrt(1.0 / (dxi * dyi * _prof(dzi, gk, nk)))
     X(out)[...] = (cs * mlen) ** 2 * np.sqrt(s2)
     return out
+
+
+def rk3_uvw(ut, vt, wt, u, v, w, rk_a, rk_bdt, ghost=(3, 3, 3), interior=None):
+    """One low-storage RK3 substep on the interior: a + rk_bdt * at and
+    rk_a * at for (u, ut), (v, vt), (w, wt).  Returns (ut, vt, wt, u, v, w)."""
+    arrs, X, _ = _setup((ut, vt, wt, u, v, w), ghost, interior)
+    out = [np.array(a, copy=True) for a in arrs]
+    for t, a in ((0, 3), (1, 4), (2, 5)):
+        X(out[a])[...] += rk_bdt * X(arrs[t])
+        X(out[t])[...] = rk_a * X(arrs[t])
+    return tuple(out)
+
+
+def diff_uvw_rk3(ut, vt, wt, evisc, u, v, w, u_next, v_next, w_next, dzi, dzhi, rhoref, rhorefh, dxi, dyi, rk_a,
+                 rk_bdt, ghost=(3, 3, 3), interior=None):
+    """diff_uvw followed by one RK3 substep into the next-substep buffers
+    (SURVEY §8f row 1): T = t + diffusion; t <- rk_a T; next <- cur + rk_bdt T
+    on the interior (ghost cells of every array keep their inputs).  Returns
+    (ut, vt, wt, u_next, v_next, w_next)."""
+    from .stencil_oracle import diff_uvw
+
+    tu, tv, tw = diff_uvw(ut, vt, wt, evisc, u, v, w, dzi, dzhi, rhoref, rhorefh, dxi, dyi, ghost, interior)
+    arrs, X, _ = _setup((u, v, w, ut, vt, wt, u_next, v_next, w_next), ghost, interior)
+    res = []
+    for t_new, t_old in ((tu, arrs[3]), (tv, arrs[4]), (tw, arrs[5])):
+        out = np.array(t_old, copy=True)
+        X(out)[...] = rk_a * X(t_new)
+        res.append(out)
+    for cur, t_new, nxt in ((arrs[0], tu, arrs[6]), (arrs[1], tv, arrs[7]), (arrs[2], tw, arrs[8])):
+        out = np.array(nxt, copy=True)
+        X(out)[...] = X(cur) + rk_bdt * X(t_new)
+        res.append(out)
+    return tuple(res)

@@ -50,6 +50,8 @@ HALO_REACH = {
     "advec_s": {"s": (3, 3), "w": (1, 0)},
     "diff_c": {"s": (1, 1), "evisc": (1, 1)},
     "evisc_smag": {"u": (1, 1), "v": (1, 1), "w": (1, 0)},
+    "diff_uvw_rk3": {"evisc": (1, 1), "u": (1, 1), "v": (1, 1), "w": (1, 1)},
+    "rk3_uvw": {},
 }
 
 

@@ -45,8 +45,16 @@ _HERE = Path(__file__).resolve().parent
 PRECISIONS = {"fp32": "float", "fp64": "double"}
 KERNELS = ("advec_u", "diff_uvw")
 #: the rest of the MicroHH stencil family: DIRECT staging
-FAMILY_KERNELS = ("advec_v", "advec_w", "advec_s", "diff_c", "evisc_smag")
-ALL_KERNELS = KERNELS + FAMILY_KERNELS
+FAMILY_KERNELS = ("advec_v", "advec_w", "advec_s", "diff_c", "evisc_smag", "rk3_uvw")
+#: hot-path kernels with a fused epilogue: same space and
+#: staging families as their base kernel, compiled with a -D switch
+FUSED_KERNELS = {"diff_uvw_rk3": ("diff_uvw", "KL_RK3")}
+ALL_KERNELS = KERNELS + tuple(FUSED_KERNELS) + FAMILY_KERNELS
+
+
+def base_kernel(kernel: str) -> str:
+    """The kernel whose source, space and shared-memory layout ``kernel`` uses."""
+    return FUSED_KERNELS[kernel][0] if kernel in FUSED_KERNELS else kernel
 
 STAGING_VALUES = ("DIRECT", "ZMARCH", "TMA")
 DEPTH_VALUES = (0, 1, 2, 3)
@@ -90,6 +98,18 @@ ARG_LAYOUT = {
                     ("dzhi", "input")],
         "scalars": ["dxi", "dyi", "cs", "jj", "kk", "istart", "jstart", "kstart", "iend", "jend", "kend"],
     },
+    "diff_uvw_rk3": {
+        "buffers": [("ut", "output"), ("vt", "output"), ("wt", "output"), ("evisc", "input"), ("u", "input"),
+                    ("v", "input"), ("w", "input"), ("dzi", "input"), ("dzhi", "input"), ("rhoref", "input"),
+                    ("rhorefh", "input"), ("u_next", "output"), ("v_next", "output"), ("w_next", "output")],
+        "scalars": ["dxi", "dyi", "rk_a", "rk_bdt", "jj", "kk", "istart", "jstart", "kstart", "iend", "jend",
+                    "kend"],
+    },
+    "rk3_uvw": {
+        "buffers": [("ut", "output"), ("vt", "output"), ("wt", "output"), ("u", "output"), ("v", "output"),
+                    ("w", "output")],
+        "scalars": ["rk_a", "rk_bdt", "jj", "kk", "istart", "jstart", "kstart", "iend", "jend", "kend"],
+    },
 }
 
 
@@ -127,7 +147,9 @@ def assemble_source(kernel: str, precision: str) -> str:
         f"#define KL_ENTRY {kernel}_{precision}\n"
         "#define DIRECT 0\n#define ZMARCH 1\n#define TMA 2\n"
     )
-    return prelude + _inline(_HERE / f"{kernel}.cu")
+    if kernel in FUSED_KERNELS:
+        prelude += f"#define {FUSED_KERNELS[kernel][1]} 1\n"
+    return prelude + _inline(_HERE / f"{base_kernel(kernel)}.cu")
 
 
 #: ZMARCH shared-memory plane budget per kernel, in halo'd cells per plane
@@ -161,6 +183,7 @@ def stencil_space(kernel: str = "advec_u", precision: str = "fp32") -> ConfigSpa
     """The kernel's space: Table 2 x the B200 knobs, restricted per precision
     (shared-memory limits depend on the element size, so the fp32 and fp64
     spaces — and their fingerprints — may differ)."""
+    kernel = base_kernel(kernel)
     size = 4 if precision == "fp32" else 8
     if kernel in FAMILY_KERNELS:
         # DIRECT staging only: the B200 knobs are pinned, the Table-2 space is the search space
@@ -216,7 +239,7 @@ def family_space(kernel: str, family: str, precision: str = "fp32") -> ConfigSpa
     kernel's wisdom file (keep-best append, wisdom.py:151-178).
     """
     full = stencil_space(kernel, precision)
-    pins = dict(FAMILY_PINS[family], **_FAMILY_EXTRA.get((kernel, family), {}))
+    pins = dict(FAMILY_PINS[family], **_FAMILY_EXTRA.get((base_kernel(kernel), family), {}))
     params = [TunableParam(p.name, (pins[p.name],), pins[p.name]) if p.name in pins else p for p in full.params]
     return ConfigSpace(params, full.restrictions)
 
@@ -279,8 +302,8 @@ def _definition(kernel: str, precision: str) -> KernelDefinition:
         block=("block_x", "block_y", "block_z"),
         grid=(grid_x, 1, 1),
         shared_mem=("0" if kernel in FAMILY_KERNELS else
-                    f"min(zchunk - 1, 1) * ((1 - min(depth, 1)) * {_SMEM[kernel].format(S=size)}"
-                    f" + min(depth, 1) * {_SMEM_TMA[kernel].format(S=size)})"),
+                    f"min(zchunk - 1, 1) * ((1 - min(depth, 1)) * {_SMEM[base_kernel(kernel)].format(S=size)}"
+                    f" + min(depth, 1) * {_SMEM_TMA[base_kernel(kernel)].format(S=size)})"),
         defines=defines,
         flags=("-std=c++17",),
     )

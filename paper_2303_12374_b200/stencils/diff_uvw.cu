@@ -20,6 +20,27 @@
 #define STAGING 0
 #endif
 
+// KL_RK3 (kernel diff_uvw_rk3): the epilogue fuses the
+// MicroHH low-storage RK3 time step into the tendency store.  With the final
+// tendency T = t + d of every component,
+//     t <- rk_a * T          (the tendency carried into the next substep)
+//     next <- cur + rk_bdt * T   (u/v/w of the next substep, double-buffered:
+//                                 neighbours still read cur)
+// — 13 words per cell instead of diff_uvw (10) + a separate RK3 pass (12).
+#ifndef KL_RK3
+#define KL_RK3 0
+#endif
+#if KL_RK3
+#define KL_RK3_BUFFERS , real* __restrict__ un, real* __restrict__ vn, real* __restrict__ wn
+#define KL_RK3_SCALARS , const real rk_a, const real rk_bdt
+#else
+#define KL_RK3_BUFFERS
+#define KL_RK3_SCALARS
+#endif
+// argument positions of jj / kk (definitions.ARG_LAYOUT) for the TMA spec
+#define KL_POS_JJ (KL_RK3 ? 18 : 13)
+#define KL_POS_KK (KL_RK3 ? 19 : 14)
+
 namespace {
 
 struct ZFactors {
@@ -115,8 +136,9 @@ extern "C" __global__ void __launch_bounds__(KL_THREADS, MIN_BLOCKS)
 KL_ENTRY(real* __restrict__ ut, real* __restrict__ vt, real* __restrict__ wt, const real* __restrict__ evisc,
          const real* __restrict__ u, const real* __restrict__ v, const real* __restrict__ w,
          const real* __restrict__ dzi, const real* __restrict__ dzhi, const real* __restrict__ rhoref,
-         const real* __restrict__ rhorefh, const real dxi, const real dyi, const int jj, const int kk,
-         const int istart, const int jstart, const int kstart, const int iend, const int jend, const int kend) {
+         const real* __restrict__ rhorefh KL_RK3_BUFFERS, const real dxi, const real dyi KL_RK3_SCALARS,
+         const int jj, const int kk, const int istart, const int jstart, const int kstart, const int iend,
+         const int jend, const int kend) {
   if (jj != KL_JJ || kk != KL_KK) __trap();
   const unsigned nbx = kl::ceil_div(iend - istart, BLOCK_X * TILE_X);
   const unsigned nby = kl::ceil_div(jend - jstart, BLOCK_Y * TILE_Y);
@@ -141,9 +163,19 @@ KL_ENTRY(real* __restrict__ ut, real* __restrict__ vt, real* __restrict__ wt, co
         const GlobalAcc acc{{evisc + ijk, u + ijk, v + ijk, w + ijk}};
         real dut, dvt, dwt;
         diff_uvw_tend(acc, dxi, dyi, zf, dut, dvt, dwt);
+#if KL_RK3
+        const real tu = ut[ijk] + dut, tv = vt[ijk] + dvt, tw = wt[ijk] + dwt;
+        un[ijk] = u[ijk] + rk_bdt * tu;
+        vn[ijk] = v[ijk] + rk_bdt * tv;
+        wn[ijk] = w[ijk] + rk_bdt * tw;
+        ut[ijk] = rk_a * tu;
+        vt[ijk] = rk_a * tv;
+        wt[ijk] = rk_a * tw;
+#else
         ut[ijk] += dut;
         vt[ijk] += dvt;
         wt[ijk] += dwt;
+#endif
       }
     }
   }

@@ -422,6 +422,10 @@ struct Step<true> {
 // NVRTC has no extended device lambdas).
 struct DiffTma {
   real *ut, *vt, *wt;
+#if KL_RK3
+  real *un, *vn, *wn;  // u, v, w of the next RK3 substep
+  real rk_a, rk_bdt;
+#endif
   const real* zprof;  // [ZCHUNK][5] per-plane factors
   real* ring;
   unsigned long long* full;
@@ -503,6 +507,38 @@ struct DiffTma {
           o[1][q] += dvt[q];
           o[2][q] += dwt[q];
         }
+#if KL_RK3
+        // fused RK3 substep: next = centre + rk_bdt T (centre u/v/w of row t
+        // from the staged plane), t = rk_a T
+        real nx[3][kTX];
+#pragma unroll
+        for (int f = 0; f < 3; ++f) {
+          const real* c = pk + hof[1 + f] + (t + 1) * kBW;
+#pragma unroll
+          for (int q = 0; q < kTX; ++q) {
+            nx[f][q] = c[q] + rk_bdt * o[f][q];
+            o[f][q] *= rk_a;
+          }
+        }
+        real* const nr[3] = {un + (ur - ut), vn + (vr - vt), wn + (wr - wt)};
+        if (VA > 1 && full_x) {
+#pragma unroll
+          for (int f = 0; f < 3; ++f)
+#pragma unroll
+            for (int e = 0; e < kTX; e += VA) {
+              Pack<VA> a;
+#pragma unroll
+              for (int q = 0; q < VA; ++q) a.v[q] = nx[f][e + q];
+              *reinterpret_cast<Pack<VA>*>(nr[f] + e) = a;
+            }
+        } else {
+#pragma unroll
+          for (int f = 0; f < 3; ++f)
+#pragma unroll
+            for (int q = 0; q < kTX; ++q)
+              if (ic + q < iend) nr[f][q] = nx[f][q];
+        }
+#endif
         if (VA > 1 && full_x) {
 #pragma unroll
           for (int e = 0; e < kTX; e += VA) {
@@ -538,10 +574,15 @@ struct DiffTma {
 };
 }  // namespace
 
-// positions: ut=0 vt=1 wt=2 evisc=3 u=4 v=5 w=6, jj=13 kk=14 (definitions.ARG_LAYOUT["diff_uvw"])
+// positions: ut=0 vt=1 wt=2 evisc=3 u=4 v=5 w=6, jj / kk = KL_POS_JJ / KL_POS_KK
+// (definitions.ARG_LAYOUT["diff_uvw"] / ["diff_uvw_rk3"])
+#define KL_J KL_POS_JJ
+#define KL_K KL_POS_KK
 extern "C" __device__ const int kl_tma_spec[1 + 5 * 7] = {
-    7, 3, 13, 14, kBW, kBH, 4, 13, 14, kBW, kBH, 5, 13, 14, kBW, kBH, 6, 13, 14, kBW, kBH,
-    0, 13, 14, kTW, kTYT, 1, 13, 14, kTW, kTYT, 2, 13, 14, kTW, kTYT};
+    7, 3, KL_J, KL_K, kBW, kBH, 4, KL_J, KL_K, kBW, kBH, 5, KL_J, KL_K, kBW, kBH, 6, KL_J, KL_K, kBW, kBH,
+    0, KL_J, KL_K, kTW, kTYT, 1, KL_J, KL_K, kTW, kTYT, 2, KL_J, KL_K, kTW, kTYT};
+#undef KL_J
+#undef KL_K
 struct __align__(64) KlTmaParams {
   TmaDesc map[7];
 };
@@ -550,9 +591,9 @@ extern "C" __global__ void __launch_bounds__(KL_THREADS, MIN_BLOCKS)
 KL_ENTRY(real* __restrict__ ut, real* __restrict__ vt, real* __restrict__ wt, const real* __restrict__ evisc,
          const real* __restrict__ u, const real* __restrict__ v, const real* __restrict__ w,
          const real* __restrict__ dzi, const real* __restrict__ dzhi, const real* __restrict__ rhoref,
-         const real* __restrict__ rhorefh, const real dxi, const real dyi, const int jj, const int kk,
-         const int istart, const int jstart, const int kstart, const int iend, const int jend, const int kend,
-         const __grid_constant__ KlTmaParams tma) {
+         const real* __restrict__ rhorefh KL_RK3_BUFFERS, const real dxi, const real dyi KL_RK3_SCALARS,
+         const int jj, const int kk, const int istart, const int jstart, const int kstart, const int iend,
+         const int jend, const int kend, const __grid_constant__ KlTmaParams tma) {
   if (jj != KL_JJ || kk != KL_KK) __trap();
   extern __shared__ __align__(128) unsigned char kl_smem_raw[];
   unsigned char* base = kl_smem_raw + ((128u - (kl::smem_u32(kl_smem_raw) & 127u)) & 127u);
@@ -571,6 +612,13 @@ KL_ENTRY(real* __restrict__ ut, real* __restrict__ vt, real* __restrict__ wt, co
   m.ut = ut;
   m.vt = vt;
   m.wt = wt;
+#if KL_RK3
+  m.un = un;
+  m.vn = vn;
+  m.wn = wn;
+  m.rk_a = rk_a;
+  m.rk_bdt = rk_bdt;
+#endif
   m.ring = ring;
   m.full = full;
   m.maps = &tma.map[0];  // param-space address of the descriptors (__grid_constant__: no local copy)

@@ -37,8 +37,9 @@ extern "C" __global__ void __launch_bounds__(KL_THREADS, MIN_BLOCKS)
 KL_ENTRY(real* __restrict__ ut, real* __restrict__ vt, real* __restrict__ wt, const real* __restrict__ evisc,
          const real* __restrict__ u, const real* __restrict__ v, const real* __restrict__ w,
          const real* __restrict__ dzi, const real* __restrict__ dzhi, const real* __restrict__ rhoref,
-         const real* __restrict__ rhorefh, const real dxi, const real dyi, const int jj, const int kk,
-         const int istart, const int jstart, const int kstart, const int iend, const int jend, const int kend) {
+         const real* __restrict__ rhorefh KL_RK3_BUFFERS, const real dxi, const real dyi KL_RK3_SCALARS,
+         const int jj, const int kk, const int istart, const int jstart, const int kstart, const int iend,
+         const int jend, const int kend) {
   if (jj != KL_JJ || kk != KL_KK) __trap();
   extern __shared__ __align__(16) unsigned char kl_smem_raw[];
   real* const ring = reinterpret_cast<real*>(kl_smem_raw);  // [3 slots][4 fields][KL_SH][KL_SW]
@@ -130,9 +131,21 @@ KL_ENTRY(real* __restrict__ ut, real* __restrict__ vt, real* __restrict__ wt, co
       const int j = j0 + lj0 + t;
       if (i < iend && j < jend) {
         const long long ijk = i + static_cast<long long>(j) * KL_JJ + kofs;
+#if KL_RK3
+        // centre values of u, v, w at (row t, plane k) in the staged plane
+        const real* c = p0 + (t + 1) * KL_SW;
+        const real tu = ut[ijk] + dut, tv = vt[ijk] + dvt, tw = wt[ijk] + dwt;
+        un[ijk] = c[FS] + rk_bdt * tu;
+        vn[ijk] = c[2 * FS] + rk_bdt * tv;
+        wn[ijk] = c[3 * FS] + rk_bdt * tw;
+        ut[ijk] = rk_a * tu;
+        vt[ijk] = rk_a * tv;
+        wt[ijk] = rk_a * tw;
+#else
         ut[ijk] += dut;
         vt[ijk] += dvt;
         wt[ijk] += dwt;
+#endif
       }
     };
     diff_step<true, KL_SW>(p0, p1, FS, carry, dxi, dyi, qsx, qsy, c2x, c2y, rhorefh[k + 1], dzhi[k + 1], rhoref[k] * dzi[k],

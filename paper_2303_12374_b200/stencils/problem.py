@@ -37,16 +37,26 @@ KERNEL_FIELDS = {
     "advec_s": ("st", "s", "u", "v", "w"),
     "diff_c": ("st", "s", "evisc"),
     "evisc_smag": ("evisc", "u", "v", "w"),
+    "diff_uvw_rk3": ("ut", "vt", "wt", "evisc", "u", "v", "w", "u_next", "v_next", "w_next"),
+    "rk3_uvw": ("ut", "vt", "wt", "u", "v", "w"),
 }
 #: algorithmic HBM words per interior cell: advec_u reads u,v,w,ut
 #: and writes ut; diff_uvw reads evisc,u,v,w,ut,vt,wt and writes ut,vt,wt;
 #: advec_v/w as advec_u; advec_s reads s,u,v,w,st and writes st; diff_c reads
 #: s,evisc,st and writes st; evisc_smag reads u,v,w and writes evisc.
 BYTES_PER_CELL_WORDS = {"advec_u": 5, "diff_uvw": 10, "advec_v": 5, "advec_w": 5, "advec_s": 6, "diff_c": 4,
-                        "evisc_smag": 4}
+                        "evisc_smag": 4,
+                        # diff_uvw + RK3 epilogue: reads evisc,u,v,w,ut,vt,wt, writes ut,vt,wt,u',v',w'
+                        "diff_uvw_rk3": 13,
+                        # the separate RK3 pass: read + write u,v,w,ut,vt,wt
+                        "rk3_uvw": 12}
 #: MicroHH defaults of the model constants the family kernels take
 TPRI = 3.0  # 1 / Pr_t (Pr_t = 1/3)
 CS = 0.23   # Smagorinsky constant
+#: RK3 substep used by diff_uvw_rk3 / rk3_uvw: MicroHH's second substep of the
+#: Williamson low-storage scheme (cA = -5/9, cB = 15/16) with dt = 0.01
+RK_A = -5.0 / 9.0
+RK_BDT = 15.0 / 16.0 * 0.01
 _PROFILE_FIELDS = ("rhoref", "rhorefh", "dzi", "dzhi")
 
 
@@ -54,7 +64,7 @@ class StencilProblem:
     def __init__(self, kernel: str, layout: GridLayout, ctx: DeviceContext, *, k_offset: int = 0,
                  kcells_global: int | None = None, profiles: Profiles | None = None,
                  dxi: float = 1.0, dyi: float = 1.0, tpri: float = TPRI, cs: float = CS,
-                 stream: Stream | None = None) -> None:
+                 rk_a: float = RK_A, rk_bdt: float = RK_BDT, stream: Stream | None = None) -> None:
         if kernel not in ARG_LAYOUT:
             raise ValueError(f"unknown kernel {kernel!r}")
         self.kernel = kernel
@@ -65,6 +75,7 @@ class StencilProblem:
         self.definition = definition_for(kernel, layout.precision)
         self.dxi, self.dyi = dxi, dyi
         self.tpri, self.cs = tpri, cs
+        self.rk_a, self.rk_bdt = rk_a, rk_bdt
         self.stream = stream or ctx.stream
         glob = profiles if profiles is not None else make_profiles(self.kcells_global, layout.kgc)
         self.profiles = glob.window(k_offset, layout.kcells).as_dtype(layout.dtype)
@@ -123,7 +134,8 @@ class StencilProblem:
             "dxi": (elem, self.dxi), "dyi": (elem, self.dyi), "jj": ("i32", lay.jj), "kk": ("i32", lay.kk),
             "istart": ("i32", lay.istart), "jstart": ("i32", lay.jstart), "kstart": ("i32", lay.kstart),
             "iend": ("i32", lay.iend), "jend": ("i32", lay.jend), "kend": ("i32", lay.kend),
-            "tpri": (elem, self.tpri), "cs": (elem, self.cs),
+            "tpri": (elem, self.tpri), "cs": (elem, self.cs), "rk_a": (elem, self.rk_a),
+            "rk_bdt": (elem, self.rk_bdt),
         }
         for name in ARG_LAYOUT[self.kernel]["scalars"]:
             dtype, value = scalars[name]

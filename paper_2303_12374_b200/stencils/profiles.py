@@ -29,6 +29,9 @@ FIELD_SPECS = {
     "evisc": (6, 0.01, 0.1),
     "s": (7, -1.0, 1.0),
     "st": (8, -1.0, 1.0),
+    "u_next": (9, -1.0, 1.0),
+    "v_next": (10, -1.0, 1.0),
+    "w_next": (11, -1.0, 1.0),
 }
 _PROFILE_SEED_OFFSET = 100
 

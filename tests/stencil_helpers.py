@@ -7,7 +7,7 @@ import numpy as np
 from oracle import family_oracle, stencil_oracle
 from oracle.synth import synth_field
 from paper_2303_12374_b200.stencils.layout import GridLayout
-from paper_2303_12374_b200.stencils.problem import CS, KERNEL_FIELDS, TPRI, StencilProblem
+from paper_2303_12374_b200.stencils.problem import CS, KERNEL_FIELDS, RK_A, RK_BDT, TPRI, StencilProblem
 from paper_2303_12374_b200.stencils.profiles import FIELD_SEED_BASE, FIELD_SPECS, make_profiles
 
 TOL = {"fp32": 1e-5, "fp64": 1e-12}
@@ -42,6 +42,14 @@ def oracle_outputs(kernel: str, layout: GridLayout, dxi=1.0, dyi=1.0, k_range=No
     elif kernel == "diff_c":
         res = {"st": family_oracle.diff_c(f["st"], f["s"], f["evisc"], prof.dzi, prof.dzhi, prof.rhoref,
                                           prof.rhorefh, dxi, dyi, TPRI, ghost=g)}
+    elif kernel == "rk3_uvw":
+        res = dict(zip(("ut", "vt", "wt", "u", "v", "w"),
+                       family_oracle.rk3_uvw(f["ut"], f["vt"], f["wt"], f["u"], f["v"], f["w"], RK_A, RK_BDT, ghost=g)))
+    elif kernel == "diff_uvw_rk3":
+        res = dict(zip(("ut", "vt", "wt", "u_next", "v_next", "w_next"),
+                       family_oracle.diff_uvw_rk3(f["ut"], f["vt"], f["wt"], f["evisc"], f["u"], f["v"], f["w"],
+                                                  f["u_next"], f["v_next"], f["w_next"], prof.dzi, prof.dzhi,
+                                                  prof.rhoref, prof.rhorefh, dxi, dyi, RK_A, RK_BDT, ghost=g)))
     elif kernel == "evisc_smag":
         res = {"evisc": family_oracle.evisc_smag(f["evisc"], f["u"], f["v"], f["w"], prof.dzi, prof.dzhi, dxi, dyi,
                                                  CS, ghost=g)}

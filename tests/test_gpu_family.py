@@ -54,3 +54,39 @@ def test_family_k_subrange_launch(gpu_ctx, compiler, kernel):
     for name in ref:
         diff = np.max(np.abs(got[name].astype(np.float64) - ref[name]))
         assert diff <= 1e-12 * np.max(np.abs(ref[name])), (name, diff)
+
+
+@pytest.mark.parametrize("precision", ["fp32", "fp64"])
+def test_rk3_fused_diffusion_matches_oracle(gpu_ctx, compiler, precision):
+    """diff_uvw_rk3: the diffusion tendency with the RK3
+    substep fused into its store, in every staging family (DIRECT, ZMARCH,
+    TMA incl. packed column tiles), against the oracle diff_uvw + RK3."""
+    from paper_2303_12374_b200.stencils.definitions import FAMILY_PINS, family_space
+    from paper_2303_12374_b200.stencils.layout import GridLayout
+
+    lay = GridLayout(45, 23, 19, precision)
+    ref, _ = oracle_outputs("diff_uvw_rk3", lay)
+    space = _space("diff_uvw_rk3", precision)
+    cfgs = [space.default_config()[0]]
+    for fam in FAMILY_PINS:
+        cfgs += family_space("diff_uvw_rk3", fam, precision).sample_random(13, 2)
+    base = space.default_config()[0]
+    cfgs.append(dict(base, staging="TMA", contiguous_x=True, block_x=16, block_y=4, tile_x=4, tile_y=2, depth=1,
+                     zchunk=8, unravel="XYZ"))
+    for cfg in cfgs:
+        assert space.is_valid(cfg), cfg
+        got = run_config(gpu_ctx, compiler, "diff_uvw_rk3", lay, cfg)
+        for name in ref:
+            err = rel_error(got[name], ref[name], lay)
+            assert err <= TOL[precision], (cfg["staging"], name, err)
+
+
+def test_rk3_pass_matches_oracle(gpu_ctx, compiler):
+    from paper_2303_12374_b200.stencils.layout import GridLayout
+
+    for precision in ("fp32", "fp64"):
+        lay = GridLayout(45, 23, 19, precision)
+        ref, _ = oracle_outputs("rk3_uvw", lay)
+        got = run_config(gpu_ctx, compiler, "rk3_uvw", lay, _space("rk3_uvw", precision).default_config()[0])
+        for name in ref:
+            assert rel_error(got[name], ref[name], lay) <= TOL[precision], name

@@ -26,3 +26,14 @@ tune diff_uvw fp32 1024,1024,256 30
 tune diff_uvw fp32 1024,1024,128 30
 at --kernel diff_uvw --precision fp32 --grid 1024,1024,1 --family TMA --strategy surrogate --budget-evals 60 --budget-seconds 300
 at --kernel diff_uvw --precision fp32 --grid 1024,1024,1 --family DIRECT --strategy random --budget-evals 40 --budget-seconds 300
+# the §8f family (DIRECT kernels on the Table-2 space) at 512^3
+for k in advec_v advec_w advec_s diff_c evisc_smag; do
+  for p in fp32 fp64; do
+    at --kernel $k --precision $p --grid 512,512,512 --strategy random --budget-evals 60 --budget-seconds 300 --seed 3
+  done
+done
+# §8f row 1: the fused RK3 epilogue (same space as diff_uvw) and the separate RK3 pass it replaces
+for p in fp32 fp64; do
+  at --kernel diff_uvw_rk3 --precision $p --grid 512,512,512 --family TMA --strategy exhaustive --budget-evals 2000 --budget-seconds 1500 --restrict "$R"
+  at --kernel rk3_uvw --precision $p --grid 512,512,512 --strategy random --budget-evals 60 --budget-seconds 300 --seed 3
+done
