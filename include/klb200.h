@@ -181,6 +181,13 @@ int klb_compare_fields(uint64_t a, uint64_t b, int elem_bytes, long long base_of
                        int jj, long long kk, double* max_abs_diff, double* max_abs_ref,
                        klb_stream stream);
 
+/* zlib-compatible CRC-32 of nbytes of device memory (capture payload
+ * checksums computed where the data lives): per-chunk CRC
+ * registers on the GPU, chained on the host with the zero-append operator.
+ * Replaces zlib.crc32 over a downloaded copy in capture.py:_metadata
+ * (reference capture.py:228-256). */
+int klb_crc32_device(uint64_t dptr, size_t nbytes, klb_stream stream, uint32_t* crc_out);
+
 /* ---- multi-GPU halo exchange over NCCL (z-slab decomposition) ----------- */
 int klb_nccl_version(int* version);
 int klb_nccl_unique_id(unsigned char id_out[128]);

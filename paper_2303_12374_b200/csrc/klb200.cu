@@ -265,6 +265,88 @@ int grid_for(long long work, int threads) {
 }  // namespace
 
 // ===========================================================================
+namespace {
+
+// ---- CRC-32 (zlib polynomial) of device memory ------------------------------
+// Capture payloads are checksummed where they live: every thread computes the
+// raw (zero-initialised, unconditioned) CRC register of one chunk of CRC_CHUNK
+// bytes with slicing-by-8 tables in shared memory; the host chains the
+// chunk CRCs with the "append n zero bytes" GF(2) operator, zlib's
+// crc32_combine construction.  The result equals zlib.crc32 of the bytes.
+constexpr uint32_t CRC_POLY = 0xEDB88320u;
+constexpr long long CRC_CHUNK = 4096;
+
+__global__ void crc32_chunks_kernel(const unsigned char* __restrict__ data, long long nbytes, int aligned4,
+                                    uint32_t* __restrict__ out, long long nchunks) {
+  __shared__ uint32_t tab[8][256];
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) {
+    uint32_t c = i;
+    for (int k = 0; k < 8; ++k) c = (c >> 1) ^ (CRC_POLY & (0u - (c & 1u)));
+    tab[0][i] = c;
+  }
+  __syncthreads();
+  for (int t = 1; t < 8; ++t)
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) tab[t][i] = (tab[t - 1][i] >> 8) ^ tab[0][tab[t - 1][i] & 255];
+  __syncthreads();
+  const long long c = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (c >= nchunks) return;
+  const long long lo = c * CRC_CHUNK;
+  const long long hi = min(lo + CRC_CHUNK, nbytes);
+  uint32_t crc = 0;
+  long long p = lo;
+  if (aligned4) {
+    const uint32_t* w = reinterpret_cast<const uint32_t*>(data + lo);
+    for (; p + 8 <= hi; p += 8, w += 2) {
+      const uint32_t a = __ldg(w) ^ crc, b = __ldg(w + 1);
+      crc = tab[7][a & 255] ^ tab[6][(a >> 8) & 255] ^ tab[5][(a >> 16) & 255] ^ tab[4][a >> 24] ^
+            tab[3][b & 255] ^ tab[2][(b >> 8) & 255] ^ tab[1][(b >> 16) & 255] ^ tab[0][b >> 24];
+    }
+  }
+  for (; p < hi; ++p) crc = (crc >> 8) ^ tab[0][(crc ^ __ldg(data + p)) & 255];
+  out[c] = crc;
+}
+
+// 32x32 GF(2) matrices as 32 column words (zlib's gf2_matrix_times / square)
+uint32_t gf2_times(const uint32_t* mat, uint32_t vec) {
+  uint32_t sum = 0;
+  for (int i = 0; vec; ++i, vec >>= 1)
+    if (vec & 1) sum ^= mat[i];
+  return sum;
+}
+void gf2_square(uint32_t* sq, const uint32_t* mat) {
+  for (int n = 0; n < 32; ++n) sq[n] = gf2_times(mat, mat[n]);
+}
+// operator: CRC register after appending `len` zero bytes
+void crc_zeros_operator(long long len, uint32_t* op) {
+  uint32_t odd[32], even[32];
+  odd[0] = CRC_POLY;  // one zero bit
+  for (int n = 1; n < 32; ++n) odd[n] = 1u << (n - 1);
+  gf2_square(even, odd);  // two zero bits
+  gf2_square(odd, even);  // four zero bits
+  for (int n = 0; n < 32; ++n) op[n] = 1u << n;  // identity
+  bool first = true;
+  uint32_t res[32];
+  do {  // square to 1, 2, 4, ... zero bytes, multiplying in the set bits of len
+    gf2_square(even, odd);
+    if (len & 1) {
+      for (int n = 0; n < 32; ++n) res[n] = first ? even[n] : gf2_times(even, op[n]);
+      std::memcpy(op, res, sizeof(res));
+      first = false;
+    }
+    len >>= 1;
+    if (!len) break;
+    gf2_square(odd, even);
+    if (len & 1) {
+      for (int n = 0; n < 32; ++n) res[n] = first ? odd[n] : gf2_times(odd, op[n]);
+      std::memcpy(op, res, sizeof(res));
+      first = false;
+    }
+    len >>= 1;
+  } while (len);
+}
+
+}  // namespace
+
 extern "C" {
 
 int klb_abi_version(void) { return KLB_ABI_VERSION; }
@@ -685,6 +767,41 @@ int klb_compare_fields(uint64_t a, uint64_t b, int elem_bytes, long long base_of
   if (e != cudaSuccess) return fail(static_cast<int>(e), "compare_fields: %s", cudaGetErrorString(e));
   *max_abs_diff = host[0];
   *max_abs_ref = host[1];
+  return 0;
+}
+
+// ---- CRC-32 of device memory (capture payloads) -----------------------------------
+
+int klb_crc32_device(uint64_t dptr, size_t nbytes, klb_stream stream, uint32_t* crc_out) {
+  if (!crc_out) return fail(KLB_E_INVALID, "crc_out is null");
+  if (nbytes == 0) {
+    *crc_out = 0;
+    return 0;
+  }
+  CTX_TRY();
+  const long long nchunks = (static_cast<long long>(nbytes) + CRC_CHUNK - 1) / CRC_CHUNK;
+  uint32_t* d_out = nullptr;
+  if (cudaMalloc(&d_out, nchunks * sizeof(uint32_t)) != cudaSuccess) return fail(KLB_E_INVALID, "cudaMalloc failed");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const int threads = 256;
+  const long long blocks = (nchunks + threads - 1) / threads;
+  crc32_chunks_kernel<<<static_cast<unsigned>(blocks), threads, 0, s>>>(
+      reinterpret_cast<const unsigned char*>(dptr), static_cast<long long>(nbytes), (dptr & 3) == 0 ? 1 : 0, d_out,
+      nchunks);
+  std::vector<uint32_t> host(nchunks);
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) e = cudaMemcpyAsync(host.data(), d_out, nchunks * sizeof(uint32_t), cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  cudaFree(d_out);
+  if (e != cudaSuccess) return fail(static_cast<int>(e), "crc32_chunks: %s", cudaGetErrorString(e));
+  // chain: register <- zeros(len_c)(register) ^ raw_c, starting from the zlib preset ~0
+  uint32_t full[32], tail[32];
+  crc_zeros_operator(CRC_CHUNK, full);
+  const long long last = static_cast<long long>(nbytes) - (nchunks - 1) * CRC_CHUNK;
+  crc_zeros_operator(last, tail);
+  uint32_t reg = 0xFFFFFFFFu;
+  for (long long c = 0; c < nchunks; ++c) reg = gf2_times(c + 1 == nchunks ? tail : full, reg) ^ host[c];
+  *crc_out = reg ^ 0xFFFFFFFFu;
   return 0;
 }
 

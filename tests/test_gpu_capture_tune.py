@@ -59,3 +59,47 @@ def test_capture_tune_select_round_trip(gpu_ctx, tmp_path, monkeypatch):
     ref, _ = oracle_outputs("advec_u", lay)
     assert rel_error(prob.download("ut"), ref["ut"], lay) <= TOL["fp64"]
     prob.close()
+
+
+def test_device_crc32_matches_zlib(gpu_ctx):
+    """klb_crc32_device (per-chunk GPU CRC registers chained on the host) equals
+    zlib.crc32 for any length and alignment (chunk = 4096 B, 4-byte fast path)."""
+    import zlib
+
+    from paper_2303_12374_b200.cuda import DeviceArray
+    from paper_2303_12374_b200.cuda.capture_device import device_crc32
+
+    rng = np.random.default_rng(7)
+    data = rng.integers(0, 256, size=(6 << 20) + 64, dtype=np.uint8).tobytes()
+    arr = DeviceArray(len(data))
+    arr.upload(data, stream=gpu_ctx.stream)
+    gpu_ctx.synchronize()
+    try:
+        for n, off in ((0, 0), (1, 0), (7, 1), (8, 4), (4095, 3), (4096, 0), (4097, 4), (12288, 8), (100003, 2),
+                       ((5 << 20) + 13, 0), ((6 << 20) + 1, 63)):
+            assert device_crc32(arr.ptr + off, n) == zlib.crc32(data[off:off + n]) & 0xFFFFFFFF, (n, off)
+    finally:
+        arr.free()
+
+
+def test_device_capture_is_byte_identical_to_host_capture(gpu_ctx, tmp_path):
+    """write_capture_device (device CRCs, chunked pinned download) writes the
+    same bytes as the reference-layout host writer, and read_capture's zlib
+    check accepts them."""
+    from paper_2303_12374_b200.capture import capture_from_args, read_capture, serialize_capture
+    from paper_2303_12374_b200.cuda.capture_device import write_capture_device
+    from paper_2303_12374_b200.stencils.layout import GridLayout
+    from paper_2303_12374_b200.stencils.problem import StencilProblem
+
+    lay = GridLayout(37, 21, 9, "fp32")
+    prob = StencilProblem("diff_uvw", lay, gpu_ctx)
+    try:
+        args = prob.args()
+        host = serialize_capture(capture_from_args(prob.definition, args, "app", "t0"))
+        path = write_capture_device(prob.definition, args, tmp_path / "dev.klcap", application="app", timestamp="t0",
+                                    chunk=4096)
+        assert path.read_bytes() == host
+        cap = read_capture(path)
+        assert cap.problem == (37, 21, 9) and len(cap.buffers) == 11
+    finally:
+        prob.close()
