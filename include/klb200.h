@@ -16,6 +16,7 @@
  *   klb_time_launches              -> Executor.measure's timed reps backend.py:226-257, 442-468
  *   klb_module_global / klb_tensor_map_encode_3d -> part of ExecutableHandle.launch (TMA staging)
  *   klb_synth_field                -> synthetic capture payloads   capture.py:75-98 (BufferArg.data)
+ *   klb_crc32_device               -> zlib.crc32 of payloads       capture.py:228-256 (device capture)
  *   klb_halo_* (NCCL)              -> no reference counterpart (multi-GPU z-slabs)
  *
  * Conventions: every function returns 0 on success or a nonzero code
