@@ -3,15 +3,23 @@
 // (SURVEY.md §8f row 2).  The face velocities are the staggered components
 // themselves (u[i], u[i+1], v[j], v[j+1], w[k], w[k+1]) — no interpolation.
 //
-// DIRECT staging (the paper's kernel, every Table-2 knob; kl_direct.cuh).
+// DIRECT staging (the paper's kernel, every Table-2 knob; kl_direct.cuh) or
+// TMA staging (flux-form z-march fed by the Tensor Memory Accelerator,
+// advec_family_tma.cuh).
 // Algorithmic HBM traffic: read s, u, v, w, st; write st = 6 words per cell.
 
 #include "kl_common.cuh"
 #include "kl_direct.cuh"
 
-#if STAGING != 0
-#error "advec_s has the DIRECT staging only"
+#if STAGING == 1
+#error "advec_s: DIRECT or TMA staging (no ZMARCH variant)"
 #endif
+#define ADV_V 1
+#define ADV_W 2
+#define ADV_S 3
+#define ADV_KIND ADV_S
+
+#if STAGING == 0
 
 namespace {
 struct Plane {
@@ -42,3 +50,7 @@ KL_ENTRY(real* __restrict__ st, const real* __restrict__ s, const real* __restri
         st[ijk] -= fx * dx60 + fy * dy60 + fz * p.zfac;
       });
 }
+
+#else
+#include "advec_family_tma.cuh"
+#endif

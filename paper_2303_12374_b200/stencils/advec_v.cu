@@ -6,15 +6,23 @@
 //
 //   vt -= dxi (Fx+ - Fx-) + dyi (Fy+ - Fy-) + dzi[k]/rhoref[k] (Fz+ - Fz-)
 //
-// DIRECT staging (the paper's kernel, every Table-2 knob; kl_direct.cuh).
+// DIRECT staging (the paper's kernel, every Table-2 knob; kl_direct.cuh) or
+// TMA staging (flux-form z-march fed by the Tensor Memory Accelerator,
+// advec_family_tma.cuh).
 // Algorithmic HBM traffic: read u, v, w, vt; write vt = 5 words per cell.
 
 #include "kl_common.cuh"
 #include "kl_direct.cuh"
 
-#if STAGING != 0
-#error "advec_v has the DIRECT staging only"
+#if STAGING == 1
+#error "advec_v: DIRECT or TMA staging (no ZMARCH variant)"
 #endif
+#define ADV_V 1
+#define ADV_W 2
+#define ADV_S 3
+#define ADV_KIND ADV_V
+
+#if STAGING == 0
 
 namespace {
 struct Plane {
@@ -48,3 +56,7 @@ KL_ENTRY(real* __restrict__ vt, const real* __restrict__ u, const real* __restri
         vt[ijk] -= fx * dx120 + fy * dy120 + fz * p.zfac;
       });
 }
+
+#else
+#include "advec_family_tma.cuh"
+#endif

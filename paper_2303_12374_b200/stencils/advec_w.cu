@@ -5,15 +5,23 @@
 // divergence is divided by rhorefh[k] and scaled by dzhi[k].  Every interior
 // level is evaluated (builder decision, as for diff_uvw's wt).
 //
-// DIRECT staging (the paper's kernel, every Table-2 knob; kl_direct.cuh).
+// DIRECT staging (the paper's kernel, every Table-2 knob; kl_direct.cuh) or
+// TMA staging (flux-form z-march fed by the Tensor Memory Accelerator,
+// advec_family_tma.cuh).
 // Algorithmic HBM traffic: read u, v, w, wt; write wt = 5 words per cell.
 
 #include "kl_common.cuh"
 #include "kl_direct.cuh"
 
-#if STAGING != 0
-#error "advec_w has the DIRECT staging only"
+#if STAGING == 1
+#error "advec_w: DIRECT or TMA staging (no ZMARCH variant)"
 #endif
+#define ADV_V 1
+#define ADV_W 2
+#define ADV_S 3
+#define ADV_KIND ADV_W
+
+#if STAGING == 0
 
 namespace {
 struct Plane {
@@ -46,3 +54,7 @@ KL_ENTRY(real* __restrict__ wt, const real* __restrict__ u, const real* __restri
         wt[ijk] -= fx * dx120 + fy * dy120 + fz * p.zfac;
       });
 }
+
+#else
+#include "advec_family_tma.cuh"
+#endif

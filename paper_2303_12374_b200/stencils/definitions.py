@@ -46,6 +46,8 @@ PRECISIONS = {"fp32": "float", "fp64": "double"}
 KERNELS = ("advec_u", "diff_uvw")
 #: the rest of the MicroHH stencil family: DIRECT staging
 FAMILY_KERNELS = ("advec_v", "advec_w", "advec_s", "diff_c", "evisc_smag", "rk3_uvw")
+#: family kernels that also have a TMA-staged flux-form variant (advec_family_tma.cuh)
+ADV_FAMILY = ("advec_v", "advec_w", "advec_s")
 #: hot-path kernels with a fused epilogue: same space and
 #: staging families as their base kernel, compiled with a -D switch
 FUSED_KERNELS = {"diff_uvw_rk3": ("diff_uvw", "KL_RK3")}
@@ -185,6 +187,21 @@ def stencil_space(kernel: str = "advec_u", precision: str = "fp32") -> ConfigSpa
     spaces — and their fingerprints — may differ)."""
     kernel = base_kernel(kernel)
     size = 4 if precision == "fp32" else 8
+    if kernel in ADV_FAMILY:
+        # DIRECT (Table 2) or TMA flux-form with column pairs (tile_x in {2, 4})
+        params = table2_params() + [
+            TunableParam("staging", ("DIRECT", "TMA"), "DIRECT"),
+            TunableParam("zchunk", ZCHUNK_VALUES, 1),
+            TunableParam("depth", DEPTH_VALUES, 0),
+        ]
+        return ConfigSpace(params, [
+            BLOCK_LIMIT_RESTRICTION,
+            'staging != "DIRECT" || (zchunk == 1 && depth == 0)',
+            'staging != "TMA" || (zchunk > 1 && depth > 0 && block_z == 1 && tile_z == 1 && !unroll_x && '
+            '!unroll_y && !unroll_z && !contiguous_y && !contiguous_z && contiguous_x && tile_x >= 2 && '
+            'block_x * block_y >= 32 && block_x * tile_x <= 128 && '
+            + _adv_family_smem(kernel).format(S=size) + f" <= {SMEM_OPTIN_BYTES})",
+        ])
     if kernel in FAMILY_KERNELS:
         # DIRECT staging only: the B200 knobs are pinned, the Table-2 space is the search space
         params = table2_params() + [TunableParam("staging", ("DIRECT",), "DIRECT"),
@@ -227,6 +244,8 @@ _FAMILY_EXTRA = {
 # tile_x in {1, 2, 4} (consecutive columns)
 _FAMILY_EXTRA["advec_u", "TMA"] = {"contiguous_y": False}
 _FAMILY_EXTRA["diff_uvw", "TMA"] = {"contiguous_y": False}
+for _k in ADV_FAMILY:
+    _FAMILY_EXTRA[_k, "TMA"] = {"contiguous_y": False}
 
 
 def family_space(kernel: str, family: str, precision: str = "fp32") -> ConfigSpace:
@@ -275,6 +294,31 @@ _SMEM_TMA = {
 }
 
 
+def _adv_family_smem(kernel: str) -> str:
+    """Shared-memory bytes of the family TMA advection (advec_family_tma.cuh):
+    128 B alignment slack + 128 B of mbarriers, the phi ring (depth+4 slots of
+    the 3-halo box) and the velocity/tendency ring (depth+2 slots of boxes A
+    (u, x faces), B (w), C (v), T (tendency) by staggering), the chunk's z
+    factors."""
+    xt, r = "block_x * tile_x", "block_y * tile_y"
+
+    def width(cols):
+        return f"ceil_div(({cols}) * {{S}} + 16 - {{S}}, 16) * 16"
+
+    def box(cols, rows):
+        return f"ceil_div({width(cols)} * ({rows}), 128) * 128"
+
+    phi = box(f"{xt} + 8", f"{r} + 6")
+    a_rows = f"{r} + 1" if kernel == "advec_v" else r
+    parts = [box(f"{xt} + 1", a_rows)]
+    if kernel != "advec_w":  # B: w
+        parts.append(box(xt, f"{r} + 1" if kernel == "advec_v" else r))
+    if kernel != "advec_v":  # C: v
+        parts.append(box(xt, f"{r} + 1"))
+    parts.append(box(xt, r))  # T
+    return f"(256 + (depth + 4) * {phi} + (depth + 2) * ({' + '.join(parts)}) + 2 * zchunk * {{S}})"
+
+
 def _definition(kernel: str, precision: str) -> KernelDefinition:
     space = stencil_space(kernel, precision)
     p = lambda n: f"arg{_pos(kernel, n)}"  # noqa: E731
@@ -301,7 +345,8 @@ def _definition(kernel: str, precision: str) -> KernelDefinition:
         problem_size=(f"{p('iend')} - {p('istart')}", f"{p('jend')} - {p('jstart')}", f"{p('kend')} - {p('kstart')}"),
         block=("block_x", "block_y", "block_z"),
         grid=(grid_x, 1, 1),
-        shared_mem=("0" if kernel in FAMILY_KERNELS else
+        shared_mem=(f"min(depth, 1) * {_adv_family_smem(kernel).format(S=size)}" if kernel in ADV_FAMILY else
+                    "0" if kernel in FAMILY_KERNELS else
                     f"min(zchunk - 1, 1) * ((1 - min(depth, 1)) * {_SMEM[base_kernel(kernel)].format(S=size)}"
                     f" + min(depth, 1) * {_SMEM_TMA[base_kernel(kernel)].format(S=size)})"),
         defines=defines,

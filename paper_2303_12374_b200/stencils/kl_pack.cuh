@@ -47,6 +47,43 @@ __device__ __forceinline__ f2 flux5x60(f2 vel, f2 a, f2 b, f2 c, f2 d, f2 e, f2 
   return flux5x60_sd(vel, c + d, b + e, a + f, d - c, e - b, f - a);
 }
 
+// fp64 has no packed instructions: d2 is the same interface over two doubles
+// (two scalar instructions per operation), so pair-structured kernels serve
+// both precisions from one source.
+struct d2 {
+  double x, y;
+  __device__ __forceinline__ d2() {}
+  __device__ __forceinline__ d2(double a, double b) : x(a), y(b) {}
+  __device__ __forceinline__ explicit d2(double a) : x(a), y(a) {}
+  __device__ __forceinline__ double lo() const { return x; }
+  __device__ __forceinline__ double hi() const { return y; }
+};
+__device__ __forceinline__ d2 operator+(d2 a, d2 b) { return d2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ d2 operator-(d2 a, d2 b) { return d2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ d2 operator*(d2 a, d2 b) { return d2(a.x * b.x, a.y * b.y); }
+__device__ __forceinline__ d2 fma2(d2 a, d2 b, d2 c) { return d2(fma(a.x, b.x, c.x), fma(a.y, b.y, c.y)); }
+__device__ __forceinline__ d2 nabs2(d2 a) { return d2(-fabs(a.x), -fabs(a.y)); }
+__device__ __forceinline__ d2 flux5x60_sd(d2 vel, d2 s_cd, d2 s_be, d2 s_af, d2 d_dc, d2 d_eb, d2 d_fa) {
+  const d2 i6 = fma2(d2(37.0), s_cd, fma2(d2(-8.0), s_be, s_af));
+  const d2 i5 = fma2(d2(10.0), d_dc, fma2(d2(-5.0), d_eb, d_fa));
+  return fma2(nabs2(vel), i5, vel * i6);
+}
+__device__ __forceinline__ d2 flux5x60(d2 vel, d2 a, d2 b, d2 c, d2 d, d2 e, d2 f) {
+  return flux5x60_sd(vel, c + d, b + e, a + f, d - c, e - b, f - a);
+}
+
+// the pair type of a precision
+template <class T>
+struct pair_of;
+template <>
+struct pair_of<float> {
+  using type = f2;
+};
+template <>
+struct pair_of<double> {
+  using type = d2;
+};
+
 }  // namespace kl
 
 #endif  // KL_PACK_CUH

@@ -90,3 +90,74 @@ def test_rk3_pass_matches_oracle(gpu_ctx, compiler):
         got = run_config(gpu_ctx, compiler, "rk3_uvw", lay, _space("rk3_uvw", precision).default_config()[0])
         for name in ref:
             assert rel_error(got[name], ref[name], lay) <= TOL[precision], name
+
+
+@pytest.mark.parametrize("kernel", ["advec_v", "advec_w", "advec_s"])
+@pytest.mark.parametrize("precision", ["fp32", "fp64"])
+def test_family_tma_advection_matches_oracle(gpu_ctx, compiler, kernel, precision):
+    """TMA-staged flux-form advection of the family (advec_family_tma.cuh):
+    sampled TMA configurations plus fixed column-tile shapes on ragged grids
+    (partial thread tiles and blocks), against the oracle."""
+    from paper_2303_12374_b200.stencils.definitions import family_space
+    from paper_2303_12374_b200.stencils.layout import GridLayout
+
+    space = _space(kernel, precision)
+    base = space.default_config()[0]
+    cfgs = family_space(kernel, "TMA", precision).sample_random(17, 3)
+    cfgs += [dict(base, staging="TMA", contiguous_x=True, block_x=32, block_y=4, tile_x=2, tile_y=2, depth=2,
+                  zchunk=16, unravel="XYZ"),
+             dict(base, staging="TMA", contiguous_x=True, block_x=16, block_y=2, tile_x=4, tile_y=3, depth=1,
+                  zchunk=8)]
+    for grid in ((45, 23, 19), (130, 37, 41)):
+        lay = GridLayout(*grid, precision)
+        ref, _ = oracle_outputs(kernel, lay)
+        for cfg in cfgs:
+            assert space.is_valid(cfg), cfg
+            got = run_config(gpu_ctx, compiler, kernel, lay, cfg)
+            for name in ref:
+                err = rel_error(got[name], ref[name], lay)
+                assert err <= TOL[precision], (grid, cfg, name, err)
+
+
+@pytest.mark.parametrize("kernel", ["advec_v", "advec_w", "advec_s"])
+def test_family_tma_misaligned_fields_use_scalar_path(gpu_ctx, compiler, kernel):
+    """Pointers shifted off the 16-byte grid: the uniform scalar-access branch
+    of the family TMA kernel gives the oracle result too."""
+    from paper_2303_12374_b200.capture import scalar_env_from_args
+    from paper_2303_12374_b200.cuda import DeviceArray, DeviceBuffer
+    from paper_2303_12374_b200.cuda._abi import check, lib
+    from paper_2303_12374_b200.stencils.layout import GridLayout
+    from paper_2303_12374_b200.stencils.problem import StencilProblem
+
+    precision = "fp32"
+    lay = GridLayout(70, 29, 23, precision)
+    ref, _ = oracle_outputs(kernel, lay)
+    cfg = dict(_space(kernel, precision).default_config()[0], staging="TMA", contiguous_x=True, block_x=16,
+               block_y=4, tile_x=4, tile_y=2, depth=2, zchunk=8)
+    prob = StencilProblem(kernel, lay, gpu_ctx)
+    shifted = {}
+    try:
+        args = []
+        for a in prob.args():
+            if isinstance(a, DeviceBuffer) and a.element_count == lay.span_elems:
+                arr = DeviceArray(lay.alloc_bytes + 64)
+                dst = arr.ptr + lay.elem_bytes
+                check(lib().klb_memcpy_dtod(dst, a.ptr - lay.lead * lay.elem_bytes, lay.alloc_bytes, None))
+                shifted[a.position] = arr
+                a = DeviceBuffer(a.position, a.role, a.element_type, dst + lay.lead * lay.elem_bytes,
+                                 a.element_count, owner=arr)
+            args.append(a)
+        gpu_ctx.synchronize()
+        d = prob.definition
+        env = scalar_env_from_args(args)
+        problem = d.derive_problem_size(env)
+        exe = compiler.compile(d.render_compile_request(cfg, problem, env), gpu_ctx.ident)
+        exe.load()
+        exe.launch(d.derive_geometry(cfg, problem, env), args, timed=True)
+        name = prob.outputs()[0]
+        flat = np.frombuffer(shifted[0].download(lay.alloc_bytes, offset_bytes=lay.elem_bytes), dtype=lay.dtype)
+        assert rel_error(lay.host_view(flat), ref[name], lay) <= TOL[precision]
+    finally:
+        for arr in shifted.values():
+            arr.free()
+        prob.close()
