@@ -48,6 +48,8 @@ KERNELS = ("advec_u", "diff_uvw")
 FAMILY_KERNELS = ("advec_v", "advec_w", "advec_s", "diff_c", "evisc_smag", "rk3_uvw")
 #: family kernels that also have a TMA-staged flux-form variant (advec_family_tma.cuh)
 ADV_FAMILY = ("advec_v", "advec_w", "advec_s")
+#: family kernels with a TMA z-march over 1-halo planes (kl_plane_tma.cuh): (halo'd inputs, RMW output)
+PLANE_FAMILY = {"diff_c": (2, 1), "evisc_smag": (3, 0)}
 #: hot-path kernels with a fused epilogue: same space and
 #: staging families as their base kernel, compiled with a -D switch
 FUSED_KERNELS = {"diff_uvw_rk3": ("diff_uvw", "KL_RK3")}
@@ -202,6 +204,22 @@ def stencil_space(kernel: str = "advec_u", precision: str = "fp32") -> ConfigSpa
             'block_x * block_y >= 32 && block_x * tile_x <= 128 && '
             + _adv_family_smem(kernel).format(S=size) + f" <= {SMEM_OPTIN_BYTES})",
         ])
+    if kernel in PLANE_FAMILY:
+        # DIRECT (Table 2) or the TMA plane z-march (tile_x consecutive columns)
+        params = table2_params() + [
+            TunableParam("staging", ("DIRECT", "TMA"), "DIRECT"),
+            TunableParam("zchunk", ZCHUNK_VALUES, 1),
+            TunableParam("depth", DEPTH_VALUES, 0),
+        ]
+        return ConfigSpace(params, [
+            BLOCK_LIMIT_RESTRICTION,
+            'staging != "DIRECT" || (zchunk == 1 && depth == 0)',
+            'staging != "TMA" || (zchunk > 1 && depth > 0 && block_z == 1 && tile_z == 1 && !unroll_x && '
+            '!unroll_y && !unroll_z && !contiguous_y && !contiguous_z && '
+            '((tile_x == 1 && !contiguous_x) || (tile_x > 1 && contiguous_x)) && '
+            'block_x * block_y >= 32 && block_x * tile_x <= 128 && '
+            + _plane_family_smem(kernel).format(S=size) + f" <= {SMEM_OPTIN_BYTES})",
+        ])
     if kernel in FAMILY_KERNELS:
         # DIRECT staging only: the B200 knobs are pinned, the Table-2 space is the search space
         params = table2_params() + [TunableParam("staging", ("DIRECT",), "DIRECT"),
@@ -244,7 +262,7 @@ _FAMILY_EXTRA = {
 # tile_x in {1, 2, 4} (consecutive columns)
 _FAMILY_EXTRA["advec_u", "TMA"] = {"contiguous_y": False}
 _FAMILY_EXTRA["diff_uvw", "TMA"] = {"contiguous_y": False}
-for _k in ADV_FAMILY:
+for _k in ADV_FAMILY + tuple(PLANE_FAMILY):
     _FAMILY_EXTRA[_k, "TMA"] = {"contiguous_y": False}
 
 
@@ -319,6 +337,19 @@ def _adv_family_smem(kernel: str) -> str:
     return f"(256 + (depth + 4) * {phi} + (depth + 2) * ({' + '.join(parts)}) + 2 * zchunk * {{S}})"
 
 
+def _plane_family_smem(kernel: str) -> str:
+    """Shared-memory bytes of the TMA plane z-march (kl_plane_tma.cuh): 128 B
+    alignment slack + 128 B of mbarriers and depth+3 slots of the halo'd
+    input boxes (columns i0-1 .. i0+XT, rows j0-1 .. j0+R) plus, for a
+    read-modify-write output, its box."""
+    nh, has_t = PLANE_FAMILY[kernel]
+    xt, r = "block_x * tile_x", "block_y * tile_y"
+    halo = f"ceil_div(ceil_div(({xt} + 2) * {{S}} + 16 - {{S}}, 16) * 16 * ({r} + 2), 128) * 128"
+    tend = f"ceil_div(ceil_div({xt} * {{S}} + 16 - {{S}}, 16) * 16 * ({r}), 128) * 128"
+    slot = f"{nh} * {halo}" + (f" + {tend}" if has_t else "")
+    return f"(256 + (depth + 3) * ({slot}))"
+
+
 def _definition(kernel: str, precision: str) -> KernelDefinition:
     space = stencil_space(kernel, precision)
     p = lambda n: f"arg{_pos(kernel, n)}"  # noqa: E731
@@ -346,6 +377,7 @@ def _definition(kernel: str, precision: str) -> KernelDefinition:
         block=("block_x", "block_y", "block_z"),
         grid=(grid_x, 1, 1),
         shared_mem=(f"min(depth, 1) * {_adv_family_smem(kernel).format(S=size)}" if kernel in ADV_FAMILY else
+                    f"min(depth, 1) * {_plane_family_smem(kernel).format(S=size)}" if kernel in PLANE_FAMILY else
                     "0" if kernel in FAMILY_KERNELS else
                     f"min(zchunk - 1, 1) * ((1 - min(depth, 1)) * {_SMEM[base_kernel(kernel)].format(S=size)}"
                     f" + min(depth, 1) * {_SMEM_TMA[base_kernel(kernel)].format(S=size)})"),

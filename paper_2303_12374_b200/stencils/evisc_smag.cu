@@ -5,23 +5,68 @@
 // — the step that produces diff_uvw's evisc.  Restated on the CPU in
 // oracle/family_oracle.py:strain2 / evisc_smag.
 //
-// DIRECT staging (the paper's kernel, every Table-2 knob; kl_direct.cuh).
+// DIRECT staging (the paper's kernel, every Table-2 knob; kl_direct.cuh) or
+// TMA staging (z-march over a shared-memory ring of u / v / w planes with a
+// 1-cell halo, kl_plane_tma.cuh); one cell formula serves both.
 // Algorithmic HBM traffic: read u, v, w; write evisc = 4 words per cell.
 
 #include "kl_common.cuh"
 #include "kl_direct.cuh"
 
-#if STAGING != 0
-#error "evisc_smag has the DIRECT staging only"
+#if STAGING == 1
+#error "evisc_smag: DIRECT or TMA staging (no ZMARCH variant)"
 #endif
 
 namespace {
-struct Plane {
-  real dz, dzh, dzh1, fac;  // dzi[k], dzhi[k], dzhi[k+1], (cs mlen)^2
+__device__ __forceinline__ real sq(real a) { return a * a; }
+
+struct Smag {
+  static constexpr int NH = 3, HAS_T = 0;  // halo'd inputs: 0 = u, 1 = v, 2 = w; evisc written
+  const real *dzi, *dzhi;
+  real dxi, dyi, cs;
+  struct Plane {
+    real dz, dzh, dzh1, fac;  // dzi[k], dzhi[k], dzhi[k+1], (cs mlen)^2
+  };
+  __device__ __forceinline__ Plane plane(int k) const {
+    const real mlen = cbrt(real(1) / (dxi * dyi * dzi[k]));
+    return Plane{dzi[k], dzhi[k], dzhi[k + 1], sq(cs * mlen)};
+  }
+  template <class A>
+  __device__ __forceinline__ real cell(const A& at, const Plane& p, real) const {
+    auto U = [&](int di, int dj, int dk) { return at(0, di, dj, dk); };
+    auto V = [&](int di, int dj, int dk) { return at(1, di, dj, dk); };
+    auto W = [&](int di, int dj, int dk) { return at(2, di, dj, dk); };
+    const real diag = sq((U(1, 0, 0) - U(0, 0, 0)) * dxi) + sq((V(0, 1, 0) - V(0, 0, 0)) * dyi) +
+                      sq((W(0, 0, 1) - W(0, 0, 0)) * p.dz);
+    // du/dy + dv/dx on the four xy edges around the centre
+    const real sxy = sq((U(0, 0, 0) - U(0, -1, 0)) * dyi + (V(0, 0, 0) - V(-1, 0, 0)) * dxi) +
+                     sq((U(0, 1, 0) - U(0, 0, 0)) * dyi + (V(0, 1, 0) - V(-1, 1, 0)) * dxi) +
+                     sq((U(1, 0, 0) - U(1, -1, 0)) * dyi + (V(1, 0, 0) - V(0, 0, 0)) * dxi) +
+                     sq((U(1, 1, 0) - U(1, 0, 0)) * dyi + (V(1, 1, 0) - V(0, 1, 0)) * dxi);
+    // du/dz + dw/dx on the four xz edges
+    const real sxz = sq((U(0, 0, 0) - U(0, 0, -1)) * p.dzh + (W(0, 0, 0) - W(-1, 0, 0)) * dxi) +
+                     sq((U(0, 0, 1) - U(0, 0, 0)) * p.dzh1 + (W(0, 0, 1) - W(-1, 0, 1)) * dxi) +
+                     sq((U(1, 0, 0) - U(1, 0, -1)) * p.dzh + (W(1, 0, 0) - W(0, 0, 0)) * dxi) +
+                     sq((U(1, 0, 1) - U(1, 0, 0)) * p.dzh1 + (W(1, 0, 1) - W(0, 0, 1)) * dxi);
+    // dv/dz + dw/dy on the four yz edges
+    const real syz = sq((V(0, 0, 0) - V(0, 0, -1)) * p.dzh + (W(0, 0, 0) - W(0, -1, 0)) * dyi) +
+                     sq((V(0, 0, 1) - V(0, 0, 0)) * p.dzh1 + (W(0, 0, 1) - W(0, -1, 1)) * dyi) +
+                     sq((V(0, 1, 0) - V(0, 1, -1)) * p.dzh + (W(0, 1, 0) - W(0, 0, 0)) * dyi) +
+                     sq((V(0, 1, 1) - V(0, 1, 0)) * p.dzh1 + (W(0, 1, 1) - W(0, 0, 1)) * dyi);
+    const real strain2 = real(2) * diag + real(0.25) * (sxy + sxz + syz);
+    return p.fac * sqrt(strain2);
+  }
 };
 
-__device__ __forceinline__ real sq(real a) { return a * a; }
+struct GlobalAt {
+  const real* f[3];
+  __device__ __forceinline__ real operator()(int fi, int di, int dj, int dk) const {
+    return f[fi][di + dj * static_cast<long long>(KL_JJ) + dk * static_cast<long long>(KL_KK)];
+  }
+};
 }  // namespace
+
+#if STAGING == 0
 
 extern "C" __global__ void __launch_bounds__(KL_THREADS, MIN_BLOCKS)
 KL_ENTRY(real* __restrict__ evisc, const real* __restrict__ u, const real* __restrict__ v,
@@ -29,34 +74,31 @@ KL_ENTRY(real* __restrict__ evisc, const real* __restrict__ u, const real* __res
          const real dyi, const real cs, const int jj, const int kk, const int istart, const int jstart,
          const int kstart, const int iend, const int jend, const int kend) {
   if (jj != KL_JJ || kk != KL_KK) __trap();
-  constexpr long long I1 = 1, J1 = KL_JJ, K1 = KL_KK;
-  kl::direct_tiles(
-      istart, jstart, kstart, iend, jend, kend,
-      [&](int k) {
-        const real mlen = cbrt(real(1) / (dxi * dyi * dzi[k]));
-        return Plane{dzi[k], dzhi[k], dzhi[k + 1], sq(cs * mlen)};
-      },
-      [&](long long ijk, const Plane& p) {
-        const real* U = u + ijk;
-        const real* V = v + ijk;
-        const real* W = w + ijk;
-        const real diag = sq((U[I1] - U[0]) * dxi) + sq((V[J1] - V[0]) * dyi) + sq((W[K1] - W[0]) * p.dz);
-        // du/dy + dv/dx on the four xy edges around the centre
-        const real sxy = sq((U[0] - U[-J1]) * dyi + (V[0] - V[-I1]) * dxi) +
-                         sq((U[J1] - U[0]) * dyi + (V[J1] - V[J1 - I1]) * dxi) +
-                         sq((U[I1] - U[I1 - J1]) * dyi + (V[I1] - V[0]) * dxi) +
-                         sq((U[I1 + J1] - U[I1]) * dyi + (V[I1 + J1] - V[J1]) * dxi);
-        // du/dz + dw/dx on the four xz edges
-        const real sxz = sq((U[0] - U[-K1]) * p.dzh + (W[0] - W[-I1]) * dxi) +
-                         sq((U[K1] - U[0]) * p.dzh1 + (W[K1] - W[K1 - I1]) * dxi) +
-                         sq((U[I1] - U[I1 - K1]) * p.dzh + (W[I1] - W[0]) * dxi) +
-                         sq((U[I1 + K1] - U[I1]) * p.dzh1 + (W[I1 + K1] - W[K1]) * dxi);
-        // dv/dz + dw/dy on the four yz edges
-        const real syz = sq((V[0] - V[-K1]) * p.dzh + (W[0] - W[-J1]) * dyi) +
-                         sq((V[K1] - V[0]) * p.dzh1 + (W[K1] - W[K1 - J1]) * dyi) +
-                         sq((V[J1] - V[J1 - K1]) * p.dzh + (W[J1] - W[0]) * dyi) +
-                         sq((V[J1 + K1] - V[J1]) * p.dzh1 + (W[J1 + K1] - W[K1]) * dyi);
-        const real strain2 = real(2) * diag + real(0.25) * (sxy + sxz + syz);
-        evisc[ijk] = p.fac * sqrt(strain2);
-      });
+  const Smag tr{dzi, dzhi, dxi, dyi, cs};
+  kl::direct_tiles(istart, jstart, kstart, iend, jend, kend, [&](int k) { return tr.plane(k); },
+                   [&](long long ijk, const Smag::Plane& p) {
+                     evisc[ijk] = tr.cell(GlobalAt{{u + ijk, v + ijk, w + ijk}}, p, real(0));
+                   });
 }
+
+#else
+#include "kl_plane_tma.cuh"
+
+// positions: evisc 0, u 1, v 2, w 3, jj 9, kk 10 (definitions.ARG_LAYOUT["evisc_smag"]); maps: u, v, w
+extern "C" __device__ const int kl_tma_spec[1 + 5 * 3] = {3, 1, 9, 10, ps::kBW, ps::kBH, 2, 9, 10, ps::kBW, ps::kBH,
+                                                          3, 9, 10, ps::kBW, ps::kBH};
+struct __align__(64) KlTmaParams {
+  TmaDesc map[3];
+};
+
+extern "C" __global__ void __launch_bounds__(KL_THREADS, MIN_BLOCKS)
+KL_ENTRY(real* __restrict__ evisc, const real* __restrict__ u, const real* __restrict__ v,
+         const real* __restrict__ w, const real* __restrict__ dzi, const real* __restrict__ dzhi, const real dxi,
+         const real dyi, const real cs, const int jj, const int kk, const int istart, const int jstart,
+         const int kstart, const int iend, const int jend, const int kend, const __grid_constant__ KlTmaParams tma) {
+  if (jj != KL_JJ || kk != KL_KK) __trap();
+  const Smag tr{dzi, dzhi, dxi, dyi, cs};
+  const real* const hp[3] = {u, v, w};
+  ps::march(tr, evisc, &tma.map[0], istart, jstart, kstart, iend, jend, kend, hp);
+}
+#endif

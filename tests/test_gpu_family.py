@@ -161,3 +161,28 @@ def test_family_tma_misaligned_fields_use_scalar_path(gpu_ctx, compiler, kernel)
         for arr in shifted.values():
             arr.free()
         prob.close()
+
+
+@pytest.mark.parametrize("kernel", ["diff_c", "evisc_smag"])
+@pytest.mark.parametrize("precision", ["fp32", "fp64"])
+def test_family_tma_plane_march_matches_oracle(gpu_ctx, compiler, kernel, precision):
+    """TMA z-march over 1-halo planes (kl_plane_tma.cuh) for diff_c and
+    evisc_smag: sampled TMA configurations plus fixed tiles, ragged grids."""
+    from paper_2303_12374_b200.stencils.definitions import family_space
+    from paper_2303_12374_b200.stencils.layout import GridLayout
+
+    space = _space(kernel, precision)
+    base = space.default_config()[0]
+    cfgs = family_space(kernel, "TMA", precision).sample_random(19, 3)
+    cfgs += [dict(base, staging="TMA", block_x=32, block_y=4, tile_x=1, tile_y=2, depth=2, zchunk=16),
+             dict(base, staging="TMA", contiguous_x=True, block_x=16, block_y=2, tile_x=4, tile_y=3, depth=1,
+                  zchunk=8, unravel="XYZ")]
+    for grid in ((45, 23, 19), (130, 37, 41)):
+        lay = GridLayout(*grid, precision)
+        ref, _ = oracle_outputs(kernel, lay)
+        for cfg in cfgs:
+            assert space.is_valid(cfg), cfg
+            got = run_config(gpu_ctx, compiler, kernel, lay, cfg)
+            for name in ref:
+                err = rel_error(got[name], ref[name], lay)
+                assert err <= TOL[precision], (grid, cfg, name, err)
