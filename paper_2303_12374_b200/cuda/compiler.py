@@ -202,6 +202,7 @@ class CudaExecutable(ExecutableHandle):
         self.attrs: FuncAttrs | None = None
         self._smem_opt_in = 48 * 1024
         self._packed: dict = {}
+        self._geoms: dict = {}
         self.launch_count = 0
         self.tma_spec: list[tuple[int, int, int, int, int]] = []
 
@@ -253,6 +254,9 @@ class CudaExecutable(ExecutableHandle):
         return blob
 
     def _prepare(self, geometry: LaunchGeometry):
+        hit = self._geoms.get(geometry)
+        if hit is not None:
+            return hit
         if self.function is None:
             self.load()
         smem = geometry.shared_mem_bytes
@@ -264,7 +268,29 @@ class CudaExecutable(ExecutableHandle):
             self._smem_opt_in = smem
         grid = (C.c_uint * 3)(*geometry.grid)
         block = (C.c_uint * 3)(*geometry.block)
+        if len(self._geoms) < 1024:
+            self._geoms[geometry] = (grid, block, smem)
         return grid, block, smem
+
+    def bound(self, geometry: LaunchGeometry, args: Sequence[object], stream: Stream | None = None):
+        """A zero-argument callable enqueueing this launch: grid, block and the
+        packed parameters (TMA descriptors included) are built once, so each
+        call is one C-ABI launch — the paper's cached-launch path
+        (PAPER.md:607-625).  ``args`` must stay valid while it is used."""
+        grid, block, smem = self._prepare(geometry)
+        params, keep, staged = self._params(args, stream)
+        if staged:
+            raise LaunchError("bound launches need device-resident arguments")
+        handle = stream.handle if stream is not None else (self.ctx.stream.handle if self.ctx else None)
+        fn, launch = self.function, lib().klb_launch
+
+        def run() -> None:
+            rc = launch(fn, grid, block, smem, handle, params)
+            if rc:
+                check(rc)
+
+        run.keep = (grid, block, params, keep)  # the ctypes objects outlive the closure's callers
+        return run
 
     def _params(self, args: Sequence[object], stream: Stream | None):
         if all(isinstance(a, (ScalarArg, DeviceBuffer)) for a in args):

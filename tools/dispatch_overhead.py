@@ -70,6 +70,13 @@ def main(argv=None) -> int:
             check(lib().klb_launch(handle.function, grid, block, smem, ctx.stream.handle, params))
             bare.append(time.perf_counter() - t0)
         ctx.synchronize()
+        bound_call = wk.bind(ctx.ident, args)
+        bnd = []
+        for _ in range(a.launches):
+            t0 = time.perf_counter()
+            bound_call()
+            bnd.append(time.perf_counter() - t0)
+        ctx.synchronize()
         rep = wk.overhead_report()
         out[tag] = {
             "staging": cfg["staging"], "match_kind": first.match_kind,
@@ -78,6 +85,7 @@ def main(argv=None) -> int:
             "cached_launch_us_median": round(statistics.median(per) * 1e6, 2),
             "cached_launch_us_p90": round(sorted(per)[int(0.9 * len(per))] * 1e6, 2),
             "bare_klb_launch_us_median": round(statistics.median(bare) * 1e6, 2),
+            "bound_launch_us_median": round(statistics.median(bnd) * 1e6, 2),
             "overhead_report_subsequent_us": {k: round(v * 1e6, 2) for k, v in rep.subsequent.items()},
         }
     prob.close()

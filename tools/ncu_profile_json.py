@@ -20,9 +20,10 @@ import sys
 from pathlib import Path
 
 sys.path.insert(0, str(Path(__file__).resolve().parent))
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 from ncu_summary import summarise  # noqa: E402
 
-WORDS = {"advec_u": 5, "diff_uvw": 10}
+from paper_2303_12374_b200.stencils.problem import BYTES_PER_CELL_WORDS as WORDS  # noqa: E402
 
 
 def _num(pair):
