@@ -304,3 +304,20 @@ def test_cross_matrix_diagonal_and_gap():
     assert min(e for row in mat.entries for e in row) < 0.9
     assert fraction_of_optimum(sessions[0], sessions[0].best_config) == 1.0
     assert sum(histogram(sessions[0], 10).counts) == len(sessions[0].evaluations)
+
+
+def test_report_cuda_backend_parses_stencil_kernel_keys():
+    """``kltune report --backend cuda`` rebuilds a session's live problem from
+    its kernel key (<kernel>_<precision>-<space fingerprint>)."""
+    from types import SimpleNamespace
+
+    from paper_2303_12374_b200.cli import _CudaEvaluators
+    from paper_2303_12374_b200.report import ReportError
+
+    assert _CudaEvaluators.kernel_of(SimpleNamespace(kernel_key="diff_uvw_rk3_fp64-a27ac7eccf76")) == (
+        "diff_uvw_rk3", "fp64")
+    assert _CudaEvaluators.kernel_of(SimpleNamespace(kernel_key="advec_u_fp32-c2e327370150")) == ("advec_u", "fp32")
+    import pytest
+
+    with pytest.raises(ReportError):
+        _CudaEvaluators.kernel_of(SimpleNamespace(kernel_key="grid3d-0123456789ab"))
