@@ -140,9 +140,47 @@ def _inline(path: Path, depth: int = 0) -> str:
     return _INCLUDE.sub(repl, text)
 
 
+def _strip_comments(text: str) -> str:
+    """Remove // and /* */ comments outside string/char literals, keeping
+    every newline (line numbers of the assembled source are unchanged) and
+    dropping trailing blanks.  The assembled source is embedded in every
+    capture's metadata, which the .klcap format caps at 64 KiB
+    (reference capture.py:37); the commented sources stay in stencils/."""
+    out, i, n = [], 0, len(text)
+    quote = None
+    while i < n:
+        ch = text[i]
+        if quote:
+            out.append(ch)
+            if ch == "\\" and i + 1 < n:
+                out.append(text[i + 1])
+                i += 2
+                continue
+            if ch == quote:
+                quote = None
+            i += 1
+        elif ch in "\"'":
+            quote = ch
+            out.append(ch)
+            i += 1
+        elif text.startswith("//", i):
+            j = text.find("\n", i)
+            i = n if j < 0 else j
+        elif text.startswith("/*", i):
+            j = text.find("*/", i + 2)
+            j = n if j < 0 else j + 2
+            out.append("\n" * text.count("\n", i, j))
+            i = j
+        else:
+            out.append(ch)
+            i += 1
+    return "\n".join(line.rstrip() for line in "".join(out).split("\n"))
+
+
 @lru_cache(maxsize=None)
 def assemble_source(kernel: str, precision: str) -> str:
-    """Self-contained NVRTC source: precision/entry prelude + inlined headers."""
+    """Self-contained NVRTC source: precision/entry prelude + inlined headers
+    (comments stripped, see ``_strip_comments``)."""
     if kernel not in ALL_KERNELS or precision not in PRECISIONS:
         raise ValueError(f"unknown kernel/precision {kernel}/{precision}")
     prelude = (
@@ -153,7 +191,7 @@ def assemble_source(kernel: str, precision: str) -> str:
     )
     if kernel in FUSED_KERNELS:
         prelude += f"#define {FUSED_KERNELS[kernel][1]} 1\n"
-    return prelude + _inline(_HERE / f"{base_kernel(kernel)}.cu")
+    return prelude + _strip_comments(_inline(_HERE / f"{base_kernel(kernel)}.cu"))
 
 
 #: ZMARCH shared-memory plane budget per kernel, in halo'd cells per plane

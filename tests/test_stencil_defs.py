@@ -153,3 +153,18 @@ def test_family_kernels_compile_and_key_by_precision(kernel):
             reqs.append(d.render_compile_request(cfg, problem, env))
     for fut in comp.compile_many(reqs, B200):
         assert fut.result().lowered_name.startswith(kernel)
+
+
+@pytest.mark.parametrize("kernel", ["advec_u", "diff_uvw", "diff_uvw_rk3", "advec_v", "advec_w", "advec_s", "diff_c",
+                                    "evisc_smag", "rk3_uvw"])
+def test_capture_metadata_with_embedded_source_fits_the_format_cap(kernel):
+    """A capture embeds the definition with its source; the .klcap metadata
+    block is capped at 64 KiB (reference capture.py:37), so the assembled
+    NVRTC sources are comment-stripped."""
+    from paper_2303_12374_b200.capture import ScalarArg, metadata_block
+
+    for precision in PRECISIONS:
+        d = definition_for(kernel, precision)
+        descs = [(i, "input", "f32", 1, 4, 0) for i in range(14)]
+        blob = metadata_block(d, (1024, 1024, 1024), [ScalarArg(20, "i32", 1)] * 12, descs, "app", "t")
+        assert len(blob) < 60 * 1024, len(blob)
