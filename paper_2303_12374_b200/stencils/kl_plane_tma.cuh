@@ -135,7 +135,13 @@ __device__ __forceinline__ void march(const Traits& tr, real* __restrict__ out, 
     const typename Traits::Plane pl = tr.plane(k);
     const real* base[3] = {ring + sm * kSlot, ring + s0 * kSlot, ring + s1 * kSlot};
     const real* tend = ring + s0 * kSlot + tof;
-    const long long kofs = static_cast<long long>(k) * KL_KK;
+    // (strip row 0, column ic) of this plane in the output: rows are immediate offsets
+    real* const orow = out + ic + static_cast<long long>(j0 + lj0) * KL_JJ + static_cast<long long>(k) * KL_KK;
+    const real* pb[3][NH];
+#pragma unroll
+    for (int d = 0; d < 3; ++d)
+#pragma unroll
+      for (int f = 0; f < NH; ++f) pb[d][f] = base[d] + hof[f];
 #pragma unroll
     for (int t = 0; t < kTY; ++t) {
       const int j = j0 + lj0 + t;
@@ -146,12 +152,12 @@ __device__ __forceinline__ void march(const Traits& tr, real* __restrict__ out, 
 #pragma unroll
         for (int d = 0; d < 3; ++d)
 #pragma unroll
-          for (int f = 0; f < NH; ++f) at.p[d][f] = base[d] + hof[f] + t * kBW + c;
+          for (int f = 0; f < NH; ++f) at.p[d][f] = pb[d][f] + (t * kBW + c);
         const real t_old = Traits::HAS_T ? tend[t * kTW + c] : real(0);
         o[c] = tr.cell(at, pl, t_old);
       }
       if (j < jend) {
-        real* dst = out + ic + static_cast<long long>(j) * KL_JJ + kofs;
+        real* dst = orow + t * KL_JJ;
         if (vec && ic + kTX <= iend) {
 #pragma unroll
           for (int e = 0; e < kTX; e += kVA) {
