@@ -11,6 +11,7 @@
 
 #include "kl_common.cuh"
 #include "kl_direct.cuh"
+#include "kl_pack.cuh"
 
 #if STAGING == 1
 #error "diff_c: DIRECT or TMA staging (no ZMARCH variant)"
@@ -28,14 +29,16 @@ struct DiffC {
     const real f = h * dzi[k] / rhoref[k];
     return Plane{f * rhorefh[k + 1] * dzhi[k + 1], f * rhorefh[k] * dzhi[k]};
   }
-  // at(f, di, dj, dk): field f at the offset from the cell
-  template <class A>
-  __device__ __forceinline__ real cell(const A& at, const Plane& p, real t_old) const {
-    const real a0 = at(0, 0, 0, 0), e0 = at(1, 0, 0, 0);
+  // at(f, di, dj, dk): field f at the offset from the cell; T = real, or a
+  // pair of neighbouring cells (kl::f2 / kl::d2) under the TMA march
+  template <class T, class A>
+  __device__ __forceinline__ T cell(const A& at, const Plane& p, T t_old) const {
+    const T a0 = at(0, 0, 0, 0), e0 = at(1, 0, 0, 0);
     return t_old +
-           ((e0 + at(1, 1, 0, 0)) * (at(0, 1, 0, 0) - a0) - (at(1, -1, 0, 0) + e0) * (a0 - at(0, -1, 0, 0))) * cx +
-           ((e0 + at(1, 0, 1, 0)) * (at(0, 0, 1, 0) - a0) - (at(1, 0, -1, 0) + e0) * (a0 - at(0, 0, -1, 0))) * cy +
-           (e0 + at(1, 0, 0, 1)) * (at(0, 0, 0, 1) - a0) * p.top - (at(1, 0, 0, -1) + e0) * (a0 - at(0, 0, 0, -1)) * p.bot;
+           ((e0 + at(1, 1, 0, 0)) * (at(0, 1, 0, 0) - a0) - (at(1, -1, 0, 0) + e0) * (a0 - at(0, -1, 0, 0))) * T(cx) +
+           ((e0 + at(1, 0, 1, 0)) * (at(0, 0, 1, 0) - a0) - (at(1, 0, -1, 0) + e0) * (a0 - at(0, 0, -1, 0))) * T(cy) +
+           (e0 + at(1, 0, 0, 1)) * (at(0, 0, 0, 1) - a0) * T(p.top) -
+           (at(1, 0, 0, -1) + e0) * (a0 - at(0, 0, 0, -1)) * T(p.bot);
   }
 };
 
@@ -65,7 +68,7 @@ KL_ENTRY(real* __restrict__ st, const real* __restrict__ s, const real* __restri
   const DiffC tr = make_traits(dzi, dzhi, rhoref, rhorefh, dxi, dyi, tpri);
   kl::direct_tiles(istart, jstart, kstart, iend, jend, kend, [&](int k) { return tr.plane(k); },
                    [&](long long ijk, const DiffC::Plane& p) {
-                     st[ijk] = tr.cell(GlobalAt{{s + ijk, evisc + ijk}}, p, st[ijk]);
+                     st[ijk] = tr.cell<real>(GlobalAt{{s + ijk, evisc + ijk}}, p, st[ijk]);
                    });
 }
 

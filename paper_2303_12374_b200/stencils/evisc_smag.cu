@@ -12,13 +12,15 @@
 
 #include "kl_common.cuh"
 #include "kl_direct.cuh"
+#include "kl_pack.cuh"
 
 #if STAGING == 1
 #error "evisc_smag: DIRECT or TMA staging (no ZMARCH variant)"
 #endif
 
 namespace {
-__device__ __forceinline__ real sq(real a) { return a * a; }
+template <class T>
+__device__ __forceinline__ T sq(T a) { return a * a; }
 
 struct Smag {
   static constexpr int NH = 3, HAS_T = 0;  // halo'd inputs: 0 = u, 1 = v, 2 = w; evisc written
@@ -31,30 +33,35 @@ struct Smag {
     const real mlen = cbrt(real(1) / (dxi * dyi * dzi[k]));
     return Plane{dzi[k], dzhi[k], dzhi[k + 1], sq(cs * mlen)};
   }
-  template <class A>
-  __device__ __forceinline__ real cell(const A& at, const Plane& p, real) const {
+  // T = real, or a pair of neighbouring cells (kl::f2 / kl::d2) under the TMA march
+  template <class T, class A>
+  __device__ __forceinline__ T cell(const A& at, const Plane& pl, T) const {
     auto U = [&](int di, int dj, int dk) { return at(0, di, dj, dk); };
     auto V = [&](int di, int dj, int dk) { return at(1, di, dj, dk); };
     auto W = [&](int di, int dj, int dk) { return at(2, di, dj, dk); };
-    const real diag = sq((U(1, 0, 0) - U(0, 0, 0)) * dxi) + sq((V(0, 1, 0) - V(0, 0, 0)) * dyi) +
+    const T dxi = T(this->dxi), dyi = T(this->dyi);
+    struct {
+      T dz, dzh, dzh1;
+    } p{T(pl.dz), T(pl.dzh), T(pl.dzh1)};
+    const T diag = sq((U(1, 0, 0) - U(0, 0, 0)) * dxi) + sq((V(0, 1, 0) - V(0, 0, 0)) * dyi) +
                       sq((W(0, 0, 1) - W(0, 0, 0)) * p.dz);
     // du/dy + dv/dx on the four xy edges around the centre
-    const real sxy = sq((U(0, 0, 0) - U(0, -1, 0)) * dyi + (V(0, 0, 0) - V(-1, 0, 0)) * dxi) +
+    const T sxy = sq((U(0, 0, 0) - U(0, -1, 0)) * dyi + (V(0, 0, 0) - V(-1, 0, 0)) * dxi) +
                      sq((U(0, 1, 0) - U(0, 0, 0)) * dyi + (V(0, 1, 0) - V(-1, 1, 0)) * dxi) +
                      sq((U(1, 0, 0) - U(1, -1, 0)) * dyi + (V(1, 0, 0) - V(0, 0, 0)) * dxi) +
                      sq((U(1, 1, 0) - U(1, 0, 0)) * dyi + (V(1, 1, 0) - V(0, 1, 0)) * dxi);
     // du/dz + dw/dx on the four xz edges
-    const real sxz = sq((U(0, 0, 0) - U(0, 0, -1)) * p.dzh + (W(0, 0, 0) - W(-1, 0, 0)) * dxi) +
+    const T sxz = sq((U(0, 0, 0) - U(0, 0, -1)) * p.dzh + (W(0, 0, 0) - W(-1, 0, 0)) * dxi) +
                      sq((U(0, 0, 1) - U(0, 0, 0)) * p.dzh1 + (W(0, 0, 1) - W(-1, 0, 1)) * dxi) +
                      sq((U(1, 0, 0) - U(1, 0, -1)) * p.dzh + (W(1, 0, 0) - W(0, 0, 0)) * dxi) +
                      sq((U(1, 0, 1) - U(1, 0, 0)) * p.dzh1 + (W(1, 0, 1) - W(0, 0, 1)) * dxi);
     // dv/dz + dw/dy on the four yz edges
-    const real syz = sq((V(0, 0, 0) - V(0, 0, -1)) * p.dzh + (W(0, 0, 0) - W(0, -1, 0)) * dyi) +
+    const T syz = sq((V(0, 0, 0) - V(0, 0, -1)) * p.dzh + (W(0, 0, 0) - W(0, -1, 0)) * dyi) +
                      sq((V(0, 0, 1) - V(0, 0, 0)) * p.dzh1 + (W(0, 0, 1) - W(0, -1, 1)) * dyi) +
                      sq((V(0, 1, 0) - V(0, 1, -1)) * p.dzh + (W(0, 1, 0) - W(0, 0, 0)) * dyi) +
                      sq((V(0, 1, 1) - V(0, 1, 0)) * p.dzh1 + (W(0, 1, 1) - W(0, 0, 1)) * dyi);
-    const real strain2 = real(2) * diag + real(0.25) * (sxy + sxz + syz);
-    return p.fac * sqrt(strain2);
+    const T strain2 = T(real(2)) * diag + T(real(0.25)) * (sxy + sxz + syz);
+    return T(pl.fac) * kl::sqrt2(strain2);
   }
 };
 
@@ -77,7 +84,7 @@ KL_ENTRY(real* __restrict__ evisc, const real* __restrict__ u, const real* __res
   const Smag tr{dzi, dzhi, dxi, dyi, cs};
   kl::direct_tiles(istart, jstart, kstart, iend, jend, kend, [&](int k) { return tr.plane(k); },
                    [&](long long ijk, const Smag::Plane& p) {
-                     evisc[ijk] = tr.cell(GlobalAt{{u + ijk, v + ijk, w + ijk}}, p, real(0));
+                     evisc[ijk] = tr.cell<real>(GlobalAt{{u + ijk, v + ijk, w + ijk}}, p, real(0));
                    });
 }
 

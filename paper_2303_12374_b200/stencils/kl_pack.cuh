@@ -72,6 +72,11 @@ __device__ __forceinline__ d2 flux5x60(d2 vel, d2 a, d2 b, d2 c, d2 d, d2 e, d2 
   return flux5x60_sd(vel, c + d, b + e, a + f, d - c, e - b, f - a);
 }
 
+__device__ __forceinline__ f2 sqrt2(f2 a) { return f2(sqrtf(a.v.x), sqrtf(a.v.y)); }
+__device__ __forceinline__ d2 sqrt2(d2 a) { return d2(sqrt(a.x), sqrt(a.y)); }
+__device__ __forceinline__ float sqrt2(float a) { return sqrtf(a); }
+__device__ __forceinline__ double sqrt2(double a) { return sqrt(a); }
+
 // the pair type of a precision
 template <class T>
 struct pair_of;

@@ -29,6 +29,7 @@
 #define DEPTH 2
 #endif
 
+#include "kl_pack.cuh"
 #include "kl_tma.cuh"
 
 namespace ps {
@@ -61,11 +62,26 @@ struct At {
     return p[dk + 1][f][dj * kBW + di];
   }
 };
+// the same for two neighbouring cells (columns c, c+1) as a pair: the cell
+// formula then runs on kl::f2 (packed FADD2/FMUL2/FFMA2 in fp32) / kl::d2
+using P2 = typename kl::pair_of<real>::type;
+template <int NH, bool AL>
+struct At2 {
+  const real* p[3][NH];
+  __device__ __forceinline__ P2 operator()(int f, int di, int dj, int dk) const {
+    const real* q = p[dk + 1][f] + dj * kBW + di;
+    if (AL && (di & 1) == 0) {  // even column of an aligned layout: one 2-element shared load
+      const Pack<2> v = *reinterpret_cast<const Pack<2>*>(q);
+      return P2(v.v[0], v.v[1]);
+    }
+    return P2(q[0], q[1]);
+  }
+};
 
-template <class Traits>
-__device__ __forceinline__ void march(const Traits& tr, real* __restrict__ out, const TmaDesc* maps, int istart,
-                                      int jstart, int kstart, int iend, int jend, int kend,
-                                      const real* const (&hp)[Traits::NH]) {
+template <bool AL, class Traits>
+__device__ __forceinline__ void march_impl(const Traits& tr, real* __restrict__ out, const TmaDesc* maps, int istart,
+                                           int jstart, int kstart, int iend, int jend, int kend,
+                                           const real* const (&hp)[Traits::NH]) {
   constexpr int NH = Traits::NH;
   constexpr int kSlot = NH * kFS + (Traits::HAS_T ? kTS : 0);
   constexpr unsigned kTx = static_cast<unsigned>((NH * kBW * kBH + (Traits::HAS_T ? kTW * kTYT : 0)) * kS);
@@ -146,15 +162,27 @@ __device__ __forceinline__ void march(const Traits& tr, real* __restrict__ out, 
     for (int t = 0; t < kTY; ++t) {
       const int j = j0 + lj0 + t;
       real o[kTX];
+      if (kTX >= 2) {
 #pragma unroll
-      for (int c = 0; c < kTX; ++c) {
+        for (int c = 0; c < kTX; c += 2) {
+          At2<NH, AL> at;
+#pragma unroll
+          for (int d = 0; d < 3; ++d)
+#pragma unroll
+            for (int f = 0; f < NH; ++f) at.p[d][f] = pb[d][f] + (t * kBW + c);
+          const P2 t_old = Traits::HAS_T ? P2(tend[t * kTW + c], tend[t * kTW + c + 1]) : P2(real(0));
+          const P2 r = tr.template cell<P2>(at, pl, t_old);
+          o[c] = r.lo();
+          o[c + 1] = r.hi();
+        }
+      } else {
         At<NH> at;
 #pragma unroll
         for (int d = 0; d < 3; ++d)
 #pragma unroll
-          for (int f = 0; f < NH; ++f) at.p[d][f] = pb[d][f] + (t * kBW + c);
-        const real t_old = Traits::HAS_T ? tend[t * kTW + c] : real(0);
-        o[c] = tr.cell(at, pl, t_old);
+          for (int f = 0; f < NH; ++f) at.p[d][f] = pb[d][f] + t * kBW;
+        const real t_old = Traits::HAS_T ? tend[t * kTW] : real(0);
+        o[0] = tr.template cell<real>(at, pl, t_old);
       }
       if (j < jend) {
         real* dst = orow + t * KL_JJ;
@@ -179,6 +207,24 @@ __device__ __forceinline__ void march(const Traits& tr, real* __restrict__ out, 
     s1 = s1 + 1 == kNS ? 0 : s1 + 1;
     ph1 ^= s1 == 0 ? 1u : 0u;
   }
+}
+
+// Aligned layouts (column i0 16-byte aligned in every field — always, for
+// GridLayout) read even-column operand pairs with one shared load; any other
+// alignment takes the scalar-pair instantiation (uniform branch per launch).
+template <class Traits>
+__device__ __forceinline__ void march(const Traits& tr, real* __restrict__ out, const TmaDesc* maps, int istart,
+                                      int jstart, int kstart, int iend, int jend, int kend,
+                                      const real* const (&hp)[Traits::NH]) {
+  bool al = kl::tma_xoff(out) == 0;
+#pragma unroll
+  for (int f = 0; f < Traits::NH; ++f) al = al && kl::tma_xoff(hp[f]) == 0;
+  const int i0 = istart;  // block starts are multiples of kXT from istart
+  al = al && (i0 & (kE - 1)) == 0;
+  if (kTX >= 2 && al)
+    march_impl<true>(tr, out, maps, istart, jstart, kstart, iend, jend, kend, hp);
+  else
+    march_impl<false>(tr, out, maps, istart, jstart, kstart, iend, jend, kend, hp);
 }
 }  // namespace ps
 
