@@ -63,6 +63,11 @@ def test_virtual_ranks_match_single_grid(gpu_ctx, tmp_path, kernel, staging):
     gpu_ctx.synchronize()
     for drv in ranks:
         assert set(drv.ranges) <= {"interior", "lower", "upper"}
+        if staging == "TMA":
+            # resolve() pre-compiles every sub-range and switches step() to
+            # bound launches (one C-ABI call each)
+            drv.resolve()
+            assert set(drv._bound) == set(drv.ranges)
         drv.step()
     gpu_ctx.synchronize()
     g = lay.kgc
