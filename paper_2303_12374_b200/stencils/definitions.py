@@ -48,8 +48,9 @@ KERNELS = ("advec_u", "diff_uvw")
 FAMILY_KERNELS = ("advec_v", "advec_w", "advec_s", "diff_c", "evisc_smag", "rk3_uvw")
 #: family kernels that also have a TMA-staged flux-form variant (advec_family_tma.cuh)
 ADV_FAMILY = ("advec_v", "advec_w", "advec_s")
-#: family kernels with a TMA z-march over 1-halo planes (kl_plane_tma.cuh): (halo'd inputs, RMW output)
-PLANE_FAMILY = {"diff_c": (2, 1), "evisc_smag": (3, 0)}
+#: family kernels with a TMA z-march over 1-halo planes: (halo'd inputs, RMW output, ring slots - depth)
+#: — diff_c: kl_plane_tma.cuh (planes k-1..k+1 per step); evisc_smag: evisc_smag_tma.cuh (planes k, k+1)
+PLANE_FAMILY = {"diff_c": (2, 1, 3), "evisc_smag": (3, 0, 2)}
 #: hot-path kernels with a fused epilogue: same space and
 #: staging families as their base kernel, compiled with a -D switch
 FUSED_KERNELS = {"diff_uvw_rk3": ("diff_uvw", "KL_RK3")}
@@ -376,16 +377,16 @@ def _adv_family_smem(kernel: str) -> str:
 
 
 def _plane_family_smem(kernel: str) -> str:
-    """Shared-memory bytes of the TMA plane z-march (kl_plane_tma.cuh): 128 B
-    alignment slack + 128 B of mbarriers and depth+3 slots of the halo'd
-    input boxes (columns i0-1 .. i0+XT, rows j0-1 .. j0+R) plus, for a
-    read-modify-write output, its box."""
-    nh, has_t = PLANE_FAMILY[kernel]
+    """Shared-memory bytes of the TMA plane z-marches (kl_plane_tma.cuh,
+    evisc_smag_tma.cuh): 128 B alignment slack + 128 B of mbarriers and
+    depth+3 (depth+2) slots of the halo'd input boxes (columns i0-1 ..
+    i0+XT, rows j0-1 .. j0+R) plus, for a read-modify-write output, its box."""
+    nh, has_t, extra = PLANE_FAMILY[kernel]
     xt, r = "block_x * tile_x", "block_y * tile_y"
     halo = f"ceil_div(ceil_div(({xt} + 2) * {{S}} + 16 - {{S}}, 16) * 16 * ({r} + 2), 128) * 128"
     tend = f"ceil_div(ceil_div({xt} * {{S}} + 16 - {{S}}, 16) * 16 * ({r}), 128) * 128"
     slot = f"{nh} * {halo}" + (f" + {tend}" if has_t else "")
-    return f"(256 + (depth + 3) * ({slot}))"
+    return f"(256 + (depth + {extra}) * ({slot}))"
 
 
 def _definition(kernel: str, precision: str) -> KernelDefinition:

@@ -6,8 +6,8 @@
 // oracle/family_oracle.py:strain2 / evisc_smag.
 //
 // DIRECT staging (the paper's kernel, every Table-2 knob; kl_direct.cuh) or
-// TMA staging (z-march over a shared-memory ring of u / v / w planes with a
-// 1-cell halo, kl_plane_tma.cuh); one cell formula serves both.
+// TMA staging (edge-reusing z-march over a shared-memory ring of u / v / w
+// planes with a 1-cell halo, evisc_smag_tma.cuh).
 // Algorithmic HBM traffic: read u, v, w; write evisc = 4 words per cell.
 
 #include "kl_common.cuh"
@@ -89,23 +89,5 @@ KL_ENTRY(real* __restrict__ evisc, const real* __restrict__ u, const real* __res
 }
 
 #else
-#include "kl_plane_tma.cuh"
-
-// positions: evisc 0, u 1, v 2, w 3, jj 9, kk 10 (definitions.ARG_LAYOUT["evisc_smag"]); maps: u, v, w
-extern "C" __device__ const int kl_tma_spec[1 + 5 * 3] = {3, 1, 9, 10, ps::kBW, ps::kBH, 2, 9, 10, ps::kBW, ps::kBH,
-                                                          3, 9, 10, ps::kBW, ps::kBH};
-struct __align__(64) KlTmaParams {
-  TmaDesc map[3];
-};
-
-extern "C" __global__ void __launch_bounds__(KL_THREADS, MIN_BLOCKS)
-KL_ENTRY(real* __restrict__ evisc, const real* __restrict__ u, const real* __restrict__ v,
-         const real* __restrict__ w, const real* __restrict__ dzi, const real* __restrict__ dzhi, const real dxi,
-         const real dyi, const real cs, const int jj, const int kk, const int istart, const int jstart,
-         const int kstart, const int iend, const int jend, const int kend, const __grid_constant__ KlTmaParams tma) {
-  if (jj != KL_JJ || kk != KL_KK) __trap();
-  const Smag tr{dzi, dzhi, dxi, dyi, cs};
-  const real* const hp[3] = {u, v, w};
-  ps::march(tr, evisc, &tma.map[0], istart, jstart, kstart, iend, jend, kend, hp);
-}
+#include "evisc_smag_tma.cuh"
 #endif

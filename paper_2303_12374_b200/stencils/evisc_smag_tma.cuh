@@ -1,0 +1,247 @@
+// evisc_smag_tma.cuh — STAGING == TMA variant of evisc_smag (included by
+// evisc_smag.cu): an edge-reusing z-march.  The strain rate sums, per cell,
+// the squared shear of its 12 surrounding edges (4 xy, 4 xz, 4 yz) — each
+// edge shared by four cells.  Here every edge is evaluated once per thread
+// tile and carried:
+//   * xy edges of plane k at the (TILE_X+1) x (TILE_Y+1) corners of the tile,
+//     summed in x pairs and shared by the rows above/below;
+//   * xz / yz edges on the top face k+1/2 of the tile, summed in x / y pairs
+//     and carried up the march as the next plane's bottom-face sums.
+// u, v, w planes with a 1-cell x/y halo are fetched by TMA DEPTH planes ahead
+// into a (DEPTH+2)-slot ring (step k reads planes k and k+1; a prologue
+// evaluates the bottom faces of the chunk from planes k0-1, k0), so the
+// compute warps issue no global loads, only the evisc stores.  ~3x fewer
+// floating-point operations per cell than the per-cell formula.
+
+#if BLOCK_Z != 1 || TILE_Z != 1
+#error "evisc_smag TMA requires BLOCK_Z == TILE_Z == 1"
+#endif
+#if TILE_X > 1 && !CONTIG_X
+#error "evisc_smag TMA: TILE_X > 1 needs consecutive columns (CONTIG_X)"
+#endif
+#ifndef DEPTH
+#define DEPTH 2
+#endif
+
+#include "kl_tma.cuh"
+
+namespace {
+constexpr int kS = static_cast<int>(sizeof(real));
+constexpr int kE = 16 / kS;
+constexpr int kTX = TILE_X, kTY = TILE_Y;
+constexpr int kXT = BLOCK_X * kTX;
+constexpr int kTYT = BLOCK_Y * kTY;
+__host__ __device__ constexpr int rup(int a, int b) { return (a + b - 1) / b * b; }
+constexpr int kBW = rup(kXT + 2 + kE - 1, kE);  // columns i0-1 .. i0+kXT (start rounded down to 16 B)
+constexpr int kBH = kTYT + 2;                    // rows j0-1 .. j0+kTYT
+constexpr int kFS = rup(kBW * kBH * kS, 128) / kS;
+constexpr int kSlot = 3 * kFS;                   // u, v, w
+constexpr int kNS = DEPTH + 2;
+constexpr unsigned kTx = static_cast<unsigned>(3 * kBW * kBH * kS);
+static_assert(kBW <= 256 && kBH <= 256, "TMA box extents are limited to 256");
+
+template <int N>
+struct __align__(N * sizeof(real)) Pack {
+  real v[N];
+};
+
+// Top-face (k+1/2) edge pair sums of a tile: xz summed over the two x-edges of
+// each cell, yz over the two y-edges.  Carried to the next plane.
+struct Faces {
+  real xz[kTY][kTX], yz[kTY][kTX];
+};
+
+struct EviscTma {
+  real* evisc;
+  const real *dzi, *dzhi;
+  real* ring;
+  unsigned long long* bars;
+  const TmaDesc* maps;
+  real dxi, dyi, cs;
+  int j0, k0, k1, tid, iend, jend, ic, lj0;
+  int xh[3], hof[3];  // per-field box starts / (strip row 0, column ic) offsets in a slot
+
+  __device__ __forceinline__ void issue(int slot, int p) const {
+    unsigned long long* bar = bars + slot;
+    real* dst = ring + slot * kSlot;
+    kl::mbar_expect_tx(bar, kTx);
+#pragma unroll
+    for (int f = 0; f < 3; ++f) kl::tma_load_3d(dst + f * kFS, maps + f, bar, xh[f], j0 - 1, p);
+  }
+
+  // Top-face edge pair sums from planes k (lo) and k+1 (hi) of u, v, w:
+  //   xz edge (i-1/2+a, k+1/2): (u[i+a,k+1]-u[i+a,k]) dzh1 + (w[i+a,k+1]-w[i+a-1,k+1]) dxi
+  //   yz edge (j-1/2+b, k+1/2): (v[j+b,k+1]-v[j+b,k]) dzh1 + (w[j+b,k+1]-w[j+b-1,k+1]) dyi
+  __device__ __forceinline__ void top_faces(const real* lo, const real* hi, real dzh1, Faces& out) const {
+    const real *ul = lo + hof[0], *uh = hi + hof[0], *vl = lo + hof[1], *vh = hi + hof[1], *wh = hi + hof[2];
+#pragma unroll
+    for (int t = 0; t < kTY; ++t) {
+      real ex[kTX + 1];
+#pragma unroll
+      for (int a = 0; a <= kTX; ++a) {
+        const int o = t * kBW + a;
+        const real s = (uh[o] - ul[o]) * dzh1 + (wh[o] - wh[o - 1]) * dxi;
+        ex[a] = s * s;
+      }
+#pragma unroll
+      for (int c = 0; c < kTX; ++c) out.xz[t][c] = ex[c] + ex[c + 1];
+    }
+    real ey[kTY + 1][kTX];
+#pragma unroll
+    for (int b = 0; b <= kTY; ++b)
+#pragma unroll
+      for (int c = 0; c < kTX; ++c) {
+        const int o = b * kBW + c;
+        const real s = (vh[o] - vl[o]) * dzh1 + (wh[o] - wh[o - kBW]) * dyi;
+        ey[b][c] = s * s;
+      }
+#pragma unroll
+    for (int t = 0; t < kTY; ++t)
+#pragma unroll
+      for (int c = 0; c < kTX; ++c) out.yz[t][c] = ey[t][c] + ey[t + 1][c];
+  }
+
+  template <bool VEC>
+  __device__ __forceinline__ void march() const {
+    Faces bot;
+    kl::mbar_wait(bars + 0, 0);  // plane k0-1
+    kl::mbar_wait(bars + 1, 0);  // plane k0
+    top_faces(ring, ring + kSlot, dzhi[k0], bot);  // the bottom faces k0-1/2 of the chunk
+
+    int sprev = 0, sk = 1, sk1 = 2 % kNS;  // slots of planes k-1, k, k+1
+    unsigned ph1 = 0;
+    for (int k = k0; k < k1; ++k) {
+      __syncthreads();  // every thread is done with plane k-1's slot
+      if (tid == 0) {
+        const int p = k - 1 + kNS;
+        if (p <= k1) {
+          kl::fence_proxy_async_smem();
+          issue(sprev, p);
+        }
+      }
+      kl::mbar_wait(bars + sk1, ph1);
+      const real* pk = ring + sk * kSlot;
+      const real* pk1 = ring + sk1 * kSlot;
+      const real dz = dzi[k], dzh1 = dzhi[k + 1];
+      const real mlen = cbrt(real(1) / (dxi * dyi * dz));
+      const real fac = (cs * mlen) * (cs * mlen);
+      Faces top;
+      top_faces(pk, pk1, dzh1, top);
+
+      const real *u = pk + hof[0], *v = pk + hof[1], *w = pk + hof[2], *w1 = pk1 + hof[2];
+      // xy edges at the tile's corners (rows t = 0..kTY, columns a = 0..kTX), x-pair sums
+      //   edge (i-1/2+a, j-1/2+t): (u[i+a,j+t]-u[i+a,j+t-1]) dyi + (v[i+a,j+t]-v[i+a-1,j+t]) dxi
+      real pxy[kTY + 1][kTX];
+#pragma unroll
+      for (int t = 0; t <= kTY; ++t) {
+        real e[kTX + 1];
+#pragma unroll
+        for (int a = 0; a <= kTX; ++a) {
+          const int o = t * kBW + a;
+          const real s = (u[o] - u[o - kBW]) * dyi + (v[o] - v[o - 1]) * dxi;
+          e[a] = s * s;
+        }
+#pragma unroll
+        for (int c = 0; c < kTX; ++c) pxy[t][c] = e[c] + e[c + 1];
+      }
+      real* const orow = evisc + ic + static_cast<long long>(j0 + lj0) * KL_JJ + static_cast<long long>(k) * KL_KK;
+#pragma unroll
+      for (int t = 0; t < kTY; ++t) {
+        real out[kTX];
+#pragma unroll
+        for (int c = 0; c < kTX; ++c) {
+          const int o = t * kBW + c;
+          const real dx = (u[o + 1] - u[o]) * dxi, dy = (v[o + kBW] - v[o]) * dyi, dzz = (w1[o] - w[o]) * dz;
+          const real diag = dx * dx + dy * dy + dzz * dzz;
+          const real off = (pxy[t][c] + pxy[t + 1][c]) + (bot.xz[t][c] + top.xz[t][c]) + (bot.yz[t][c] + top.yz[t][c]);
+          out[c] = fac * sqrt(real(2) * diag + real(0.25) * off);
+        }
+        if (j0 + lj0 + t < jend) {
+          real* dst = orow + t * KL_JJ;
+          if (VEC && ic + kTX <= iend) {
+            constexpr int VA = kTX < kE ? kTX : kE;
+#pragma unroll
+            for (int e = 0; e < kTX; e += VA) {
+              Pack<VA> pk;
+#pragma unroll
+              for (int q = 0; q < VA; ++q) pk.v[q] = out[e + q];
+              *reinterpret_cast<Pack<VA>*>(dst + e) = pk;
+            }
+          } else {
+#pragma unroll
+            for (int c = 0; c < kTX; ++c)
+              if (ic + c < iend) dst[c] = out[c];
+          }
+        }
+      }
+      bot = top;
+      sprev = sk;
+      sk = sk1;
+      sk1 = sk1 + 1 == kNS ? 0 : sk1 + 1;
+      ph1 ^= sk1 == 0 ? 1u : 0u;
+    }
+  }
+};
+}  // namespace
+
+// positions: evisc 0, u 1, v 2, w 3, jj 9, kk 10 (definitions.ARG_LAYOUT["evisc_smag"]); maps: u, v, w
+extern "C" __device__ const int kl_tma_spec[1 + 5 * 3] = {3, 1, 9, 10, kBW, kBH, 2, 9, 10, kBW, kBH,
+                                                          3, 9, 10, kBW, kBH};
+struct __align__(64) KlTmaParams {
+  TmaDesc map[3];
+};
+
+extern "C" __global__ void __launch_bounds__(KL_THREADS, MIN_BLOCKS)
+KL_ENTRY(real* __restrict__ evisc, const real* __restrict__ u, const real* __restrict__ v,
+         const real* __restrict__ w, const real* __restrict__ dzi, const real* __restrict__ dzhi, const real dxi,
+         const real dyi, const real cs, const int jj, const int kk, const int istart, const int jstart,
+         const int kstart, const int iend, const int jend, const int kend, const __grid_constant__ KlTmaParams tma) {
+  if (jj != KL_JJ || kk != KL_KK) __trap();
+  extern __shared__ __align__(128) unsigned char kl_smem_raw[];
+  unsigned char* sbase = kl_smem_raw + ((128u - (kl::smem_u32(kl_smem_raw) & 127u)) & 127u);
+
+  const unsigned nbx = kl::ceil_div(iend - istart, kXT);
+  const unsigned nby = kl::ceil_div(jend - jstart, kTYT);
+  const unsigned nbz = kl::ceil_div(kend - kstart, ZCHUNK);
+  int bx, by, bz;
+  kl::unravel(blockIdx.x, nbx, nby, nbz, bx, by, bz);
+  const int i0 = istart + bx * kXT;
+
+  EviscTma m;
+  m.evisc = evisc;
+  m.dzi = dzi;
+  m.dzhi = dzhi;
+  m.bars = reinterpret_cast<unsigned long long*>(sbase);
+  m.ring = reinterpret_cast<real*>(sbase + 128);
+  m.maps = &tma.map[0];
+  m.dxi = dxi;
+  m.dyi = dyi;
+  m.cs = cs;
+  m.j0 = jstart + by * kTYT;
+  m.k0 = kstart + bz * ZCHUNK;
+  m.k1 = min(m.k0 + ZCHUNK, kend);
+  m.tid = threadIdx.x + threadIdx.y * BLOCK_X;
+  m.iend = iend;
+  m.jend = jend;
+  m.lj0 = threadIdx.y * kTY;
+  const int cx = kTX * static_cast<int>(threadIdx.x);
+  m.ic = i0 + cx;
+  const real* const hp[3] = {u, v, w};
+#pragma unroll
+  for (int f = 0; f < 3; ++f) {
+    const int x = i0 - 1 + kl::tma_xoff(hp[f]);
+    m.xh[f] = x & ~(kE - 1);
+    m.hof[f] = f * kFS + (m.lj0 + 1) * kBW + (x - m.xh[f]) + 1 + cx;  // (strip row 0, column ic)
+  }
+  if (m.tid == 0) {
+    for (int q = 0; q < kNS; ++q) kl::mbar_init(m.bars + q, 1);
+    kl::mbar_init_fence();
+  }
+  __syncthreads();
+  if (m.tid == 0)
+    for (int p = m.k0 - 1; p <= min(m.k0 - 1 + kNS - 1, m.k1); ++p) m.issue(p - (m.k0 - 1), p);
+  if (kTX > 1 && kl::tma_xoff(evisc) == 0 && (i0 & (kE - 1)) == 0)
+    m.march<true>();
+  else
+    m.march<false>();
+}
