@@ -23,6 +23,7 @@
 #define DEPTH 2
 #endif
 
+#include "kl_pack.cuh"
 #include "kl_tma.cuh"
 
 namespace {
@@ -50,6 +51,34 @@ struct __align__(N * sizeof(real)) Pack {
 struct Faces {
   real xz[kTY][kTX], yz[kTY][kTX];
 };
+
+// Column pairs (TILE_X >= 2): the same quantities of cells (c, c+1) in
+// kl::f2 (packed FADD2/FMUL2/FFMA2, fp32) / kl::d2 (fp64).  Operands of
+// even columns are aligned register pairs (one shared load on aligned
+// layouts); x-face operands one column to the left, and the x-pair sums of
+// edge values, straddle the pairs and stay scalar.
+using P2 = typename kl::pair_of<real>::type;
+constexpr int kP = kTX / 2 > 0 ? kTX / 2 : 1;
+struct Faces2 {
+  P2 xz[kTY][kP], yz[kTY][kP];
+};
+template <bool AL>
+__device__ __forceinline__ P2 ld2(const real* q) {
+  if (AL) {
+    const Pack<2> v = *reinterpret_cast<const Pack<2>*>(q);
+    return P2(v.v[0], v.v[1]);
+  }
+  return P2(q[0], q[1]);
+}
+// x-pair sums s[c] = e[c] + e[c+1] (c = 0..kTX-1) of kTX+1 edge values held
+// as kP pairs + the last one, returned as pairs
+__device__ __forceinline__ void xpair_sums(const P2 (&e)[kP], real last, P2 (&s)[kP]) {
+#pragma unroll
+  for (int p = 0; p < kP; ++p) {
+    const real next = p + 1 < kP ? e[p + 1].lo() : last;
+    s[p] = P2(e[p].lo() + e[p].hi(), e[p].hi() + next);
+  }
+}
 
 struct EviscTma {
   real* evisc;
@@ -99,6 +128,123 @@ struct EviscTma {
     for (int t = 0; t < kTY; ++t)
 #pragma unroll
       for (int c = 0; c < kTX; ++c) out.yz[t][c] = ey[t][c] + ey[t + 1][c];
+  }
+
+  template <bool AL>
+  __device__ __forceinline__ void top_faces2(const real* lo, const real* hi, real dzh1_, Faces2& out) const {
+    const real *ul = lo + hof[0], *uh = hi + hof[0], *vl = lo + hof[1], *vh = hi + hof[1], *wh = hi + hof[2];
+    const P2 dzh1(dzh1_), dx(dxi), dy(dyi);
+#pragma unroll
+    for (int t = 0; t < kTY; ++t) {
+      const int o = t * kBW;
+      P2 ex[kP];
+#pragma unroll
+      for (int p = 0; p < kP; ++p) {
+        const int a = o + 2 * p;
+        const P2 s = kl::fma2(ld2<AL>(uh + a) - ld2<AL>(ul + a), dzh1, (ld2<AL>(wh + a) - ld2<false>(wh + a - 1)) * dx);
+        ex[p] = s * s;
+      }
+      const real sl = (uh[o + kTX] - ul[o + kTX]) * dzh1_ + (wh[o + kTX] - wh[o + kTX - 1]) * dxi;
+      xpair_sums(ex, sl * sl, out.xz[t]);
+    }
+    P2 ey[kTY + 1][kP];
+#pragma unroll
+    for (int b = 0; b <= kTY; ++b)
+#pragma unroll
+      for (int p = 0; p < kP; ++p) {
+        const int o = b * kBW + 2 * p;
+        const P2 s = kl::fma2(ld2<AL>(vh + o) - ld2<AL>(vl + o), dzh1, (ld2<AL>(wh + o) - ld2<AL>(wh + o - kBW)) * dy);
+        ey[b][p] = s * s;
+      }
+#pragma unroll
+    for (int t = 0; t < kTY; ++t)
+#pragma unroll
+      for (int p = 0; p < kP; ++p) out.yz[t][p] = ey[t][p] + ey[t + 1][p];
+  }
+
+  template <bool VEC>
+  __device__ __forceinline__ void march2() const {
+    Faces2 bot;
+    kl::mbar_wait(bars + 0, 0);  // plane k0-1
+    kl::mbar_wait(bars + 1, 0);  // plane k0
+    top_faces2<VEC>(ring, ring + kSlot, dzhi[k0], bot);
+    const P2 dx(dxi), dy(dyi), two(real(2)), quarter(real(0.25));
+
+    int sprev = 0, sk = 1, sk1 = 2 % kNS;  // slots of planes k-1, k, k+1
+    unsigned ph1 = 0;
+    for (int k = k0; k < k1; ++k) {
+      __syncthreads();  // every thread is done with plane k-1's slot
+      if (tid == 0) {
+        const int p = k - 1 + kNS;
+        if (p <= k1) {
+          kl::fence_proxy_async_smem();
+          issue(sprev, p);
+        }
+      }
+      kl::mbar_wait(bars + sk1, ph1);
+      const real* pk = ring + sk * kSlot;
+      const real* pk1 = ring + sk1 * kSlot;
+      const real dz_ = dzi[k];
+      const real mlen = cbrt(real(1) / (dxi * dyi * dz_));
+      const P2 fac((cs * mlen) * (cs * mlen)), dz(dz_);
+      Faces2 top;
+      top_faces2<VEC>(pk, pk1, dzhi[k + 1], top);
+
+      const real *u = pk + hof[0], *v = pk + hof[1], *w = pk + hof[2], *w1 = pk1 + hof[2];
+      P2 pxy[kTY + 1][kP];
+#pragma unroll
+      for (int t = 0; t <= kTY; ++t) {
+        const int o = t * kBW;
+        P2 e[kP];
+#pragma unroll
+        for (int p = 0; p < kP; ++p) {
+          const int a = o + 2 * p;
+          const P2 s = kl::fma2(ld2<VEC>(u + a) - ld2<VEC>(u + a - kBW), dy, (ld2<VEC>(v + a) - ld2<false>(v + a - 1)) * dx);
+          e[p] = s * s;
+        }
+        const real sl = (u[o + kTX] - u[o + kTX - kBW]) * dyi + (v[o + kTX] - v[o + kTX - 1]) * dxi;
+        xpair_sums(e, sl * sl, pxy[t]);
+      }
+      real* const orow = evisc + ic + static_cast<long long>(j0 + lj0) * KL_JJ + static_cast<long long>(k) * KL_KK;
+#pragma unroll
+      for (int t = 0; t < kTY; ++t) {
+        real out[kTX];
+#pragma unroll
+        for (int p = 0; p < kP; ++p) {
+          const int o = t * kBW + 2 * p;
+          const P2 ddx = (ld2<false>(u + o + 1) - ld2<VEC>(u + o)) * dx;
+          const P2 ddy = (ld2<VEC>(v + o + kBW) - ld2<VEC>(v + o)) * dy;
+          const P2 ddz = (ld2<VEC>(w1 + o) - ld2<VEC>(w + o)) * dz;
+          const P2 diag = kl::fma2(ddx, ddx, kl::fma2(ddy, ddy, ddz * ddz));
+          const P2 off = (pxy[t][p] + pxy[t + 1][p]) + (bot.xz[t][p] + top.xz[t][p]) + (bot.yz[t][p] + top.yz[t][p]);
+          const P2 r = fac * kl::sqrt2(kl::fma2(two, diag, quarter * off));
+          out[2 * p] = r.lo();
+          out[2 * p + 1] = r.hi();
+        }
+        if (j0 + lj0 + t < jend) {
+          real* dst = orow + t * KL_JJ;
+          if (VEC && ic + kTX <= iend) {
+            constexpr int VA = kTX < kE ? kTX : kE;
+#pragma unroll
+            for (int e = 0; e < kTX; e += VA) {
+              Pack<VA> pk;
+#pragma unroll
+              for (int q = 0; q < VA; ++q) pk.v[q] = out[e + q];
+              *reinterpret_cast<Pack<VA>*>(dst + e) = pk;
+            }
+          } else {
+#pragma unroll
+            for (int c = 0; c < kTX; ++c)
+              if (ic + c < iend) dst[c] = out[c];
+          }
+        }
+      }
+      bot = top;
+      sprev = sk;
+      sk = sk1;
+      sk1 = sk1 + 1 == kNS ? 0 : sk1 + 1;
+      ph1 ^= sk1 == 0 ? 1u : 0u;
+    }
   }
 
   template <bool VEC>
@@ -154,7 +300,7 @@ struct EviscTma {
           const real dx = (u[o + 1] - u[o]) * dxi, dy = (v[o + kBW] - v[o]) * dyi, dzz = (w1[o] - w[o]) * dz;
           const real diag = dx * dx + dy * dy + dzz * dzz;
           const real off = (pxy[t][c] + pxy[t + 1][c]) + (bot.xz[t][c] + top.xz[t][c]) + (bot.yz[t][c] + top.yz[t][c]);
-          out[c] = fac * sqrt(real(2) * diag + real(0.25) * off);
+          out[c] = fac * kl::sqrt_fast(real(2) * diag + real(0.25) * off);
         }
         if (j0 + lj0 + t < jend) {
           real* dst = orow + t * KL_JJ;
@@ -181,6 +327,17 @@ struct EviscTma {
       ph1 ^= sk1 == 0 ? 1u : 0u;
     }
   }
+};
+// selects the pair march for TILE_X >= 2 without instantiating it otherwise
+template <bool kPairs>
+struct Marcher {
+  template <bool VEC>
+  static __device__ __forceinline__ void run(const EviscTma& m) { m.march<VEC>(); }
+};
+template <>
+struct Marcher<true> {
+  template <bool VEC>
+  static __device__ __forceinline__ void run(const EviscTma& m) { m.march2<VEC>(); }
 };
 }  // namespace
 
@@ -240,8 +397,11 @@ KL_ENTRY(real* __restrict__ evisc, const real* __restrict__ u, const real* __res
   __syncthreads();
   if (m.tid == 0)
     for (int p = m.k0 - 1; p <= min(m.k0 - 1 + kNS - 1, m.k1); ++p) m.issue(p - (m.k0 - 1), p);
-  if (kTX > 1 && kl::tma_xoff(evisc) == 0 && (i0 & (kE - 1)) == 0)
-    m.march<true>();
+  bool aligned = kl::tma_xoff(evisc) == 0 && (i0 & (kE - 1)) == 0;
+#pragma unroll
+  for (int f = 0; f < 3; ++f) aligned = aligned && kl::tma_xoff(hp[f]) == 0;
+  if (kTX > 1 && aligned)
+    Marcher<(kTX >= 2)>::template run<true>(m);
   else
-    m.march<false>();
+    Marcher<(kTX >= 2)>::template run<false>(m);
 }

@@ -72,9 +72,18 @@ __device__ __forceinline__ d2 flux5x60(d2 vel, d2 a, d2 b, d2 c, d2 d, d2 e, d2 
   return flux5x60_sd(vel, c + d, b + e, a + f, d - c, e - b, f - a);
 }
 
-__device__ __forceinline__ f2 sqrt2(f2 a) { return f2(sqrtf(a.v.x), sqrtf(a.v.y)); }
+// square roots: fp32 uses the hardware approximation (sqrt.approx, max
+// relative error 2^-23 — far inside the 1e-5 parity bar, and one MUFU instead
+// of the IEEE-rounded sequence with its special-case branch); fp64 stays exact
+__device__ __forceinline__ float sqrt_fast(float a) {
+  float r;
+  asm("sqrt.approx.f32 %0, %1;" : "=f"(r) : "f"(a));
+  return r;
+}
+__device__ __forceinline__ double sqrt_fast(double a) { return sqrt(a); }
+__device__ __forceinline__ f2 sqrt2(f2 a) { return f2(sqrt_fast(a.v.x), sqrt_fast(a.v.y)); }
 __device__ __forceinline__ d2 sqrt2(d2 a) { return d2(sqrt(a.x), sqrt(a.y)); }
-__device__ __forceinline__ float sqrt2(float a) { return sqrtf(a); }
+__device__ __forceinline__ float sqrt2(float a) { return sqrt_fast(a); }
 __device__ __forceinline__ double sqrt2(double a) { return sqrt(a); }
 
 // the pair type of a precision
