@@ -2,6 +2,6 @@
 set -x
 OUT=${OUT:-gpurun_out/final}
 mkdir -p $OUT
-/usr/bin/time -v python __graft_entry__.py smoke > $OUT/smoke.txt 2> $OUT/smoke.err; echo "smoke rc=$?"; tail -3 $OUT/smoke.txt; grep Elapsed $OUT/smoke.err
-/usr/bin/time -v python bench.py > $OUT/bench.json 2> $OUT/bench.err; echo "bench rc=$?"; grep Elapsed $OUT/bench.err; head -c 300 $OUT/bench.json
-/usr/bin/time -v python bench.py --impl reference --steps 5 --warmup 3 > $OUT/bench_ref.json 2> $OUT/bench_ref.err; echo "ref rc=$?"; grep Elapsed $OUT/bench_ref.err; cat $OUT/bench_ref.json
+t0=$(date +%s); python __graft_entry__.py smoke > $OUT/smoke.txt 2> $OUT/smoke.err; echo "smoke rc=$? $(( $(date +%s) - t0 )) s"; tail -3 $OUT/smoke.txt
+t0=$(date +%s); python bench.py > $OUT/bench.json 2> $OUT/bench.err; echo "bench rc=$? $(( $(date +%s) - t0 )) s"; tail -2 $OUT/bench.err; head -c 300 $OUT/bench.json
+t0=$(date +%s); python bench.py --impl reference --steps 5 --warmup 3 > $OUT/bench_ref.json 2> $OUT/bench_ref.err; echo "ref rc=$? $(( $(date +%s) - t0 )) s"; tail -2 $OUT/bench_ref.err; cat $OUT/bench_ref.json
