@@ -48,6 +48,9 @@ WORKLOADS = {
     "advec_u_fp32_256": ("advec_u", "fp32", (256, 256, 256), "BASELINE config 2: advec_u fp32 256^3, wisdom-selected"),
     "advec_u_fp64_512": ("advec_u", "fp64", (512, 512, 512), "BASELINE config 3: advec_u fp64 512^3"),
     "diff_uvw_fp64_512": ("diff_uvw", "fp64", (512, 512, 512), "BASELINE config 3: diff_uvw fp64 512^3"),
+    # small grids for the multi-process plumbing test (not a BASELINE configuration)
+    "diff_uvw_fp32_256": ("diff_uvw", "fp32", (256, 256, 256), "diff_uvw fp32 256^3 (multi-process plumbing test)"),
+    "advec_u_fp32_256x256x96": ("advec_u", "fp32", (256, 256, 96), "advec_u fp32 256x256x96 (multi-process plumbing test)"),
 }
 SUITE = [
     ("diff_uvw", "fp64", (64, 64, 64), "config 1"),
@@ -435,14 +438,19 @@ def suite_measure(ctx, compiler, wisdom_dir, peak, suite=SUITE):
 
 def run_ours(args, dist):
     from paper_2303_12374_b200.cuda import NvrtcCompiler, open_device
-    from paper_2303_12374_b200.halo import NcclExchanger
+    from paper_2303_12374_b200.halo import NcclExchanger, StagedExchanger
     from paper_2303_12374_b200.slab import SlabDriver
 
     kernel, precision, grid, label = WORKLOADS[args.workload]
-    ctx = open_device(dist.local if args.gpus > 1 or dist.world > 1 else 0)
+    # KL_DEVICE_ORDINAL pins every rank to one device (the single-GPU
+    # multi-process test of the N > 1 path, tests/test_gpu_multiproc.py)
+    forced = os.environ.get("KL_DEVICE_ORDINAL")
+    ctx = open_device(int(forced) if forced is not None else (dist.local if args.gpus > 1 or dist.world > 1 else 0))
     peak, peak_src = peaks()
     exchanger = None
-    if dist.world > 1:
+    if dist.world > 1 and os.environ.get("KL_HALO_TRANSPORT", "nccl") == "staged":
+        exchanger = StagedExchanger(dist.rank, dist.world)  # host relay over gloo (testing on one GPU)
+    elif dist.world > 1:
         uid = dist.broadcast_bytes(NcclExchanger.unique_id() if dist.rank == 0 else None)
         exchanger = NcclExchanger(dist.rank, dist.world, uid)
     compiler = NvrtcCompiler(ctx)
@@ -458,7 +466,7 @@ def run_ours(args, dist):
         chosen = driver.resolve()
         for _ in range(args.warmup):
             driver.step()
-        with ClockSampler(range(dist.world) if dist.world > 1 else [ctx.ordinal]) as clocks:
+        with ClockSampler([ctx.ordinal] if forced is not None or dist.world == 1 else range(dist.world)) as clocks:
             step_s, kern_s, launches = timed_steps(driver, dist, args.steps)
         cells_total = grid[0] * grid[1] * grid[2]
         interior_cells = dist.sum(driver.cells_in("interior") if "interior" in driver.ranges else 0)

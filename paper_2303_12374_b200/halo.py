@@ -38,7 +38,7 @@ from dataclasses import dataclass
 
 __all__ = [
     "HALO_REACH", "SlabDecomposition", "halo_plan", "NcclExchanger", "CopyExchanger", "HostExchanger",
-    "SlabRank",
+    "StagedExchanger", "SlabRank",
 ]
 
 #: kernel -> {field: (down, up)}
@@ -192,6 +192,53 @@ class HostExchanger:
             req.wait()
         for arr, first, count, buf in sinks:
             arr[first:first + count] = buf.numpy()
+
+
+class StagedExchanger:
+    """The same exchange as ``NcclExchanger`` with the planes relayed through
+    pinned host memory over torch.distributed (any backend; gloo here).
+
+    Not a performance transport: it serialises on the host.  It exists so the
+    whole multi-rank path (decomposition, sub-range launches, exchange
+    ordering, max-over-ranks timing, bench output at N > 1) can run as several
+    processes on ONE GPU — NCCL refuses two ranks on one device — which is
+    what ``tests/test_gpu_multiproc.py`` does (selected in ``bench.py`` by
+    ``KL_HALO_TRANSPORT=staged``).  Same signature as ``NcclExchanger.exchange``.
+    """
+
+    def __init__(self, rank: int, nranks: int) -> None:
+        self.rank, self.nranks = rank, nranks
+
+    def exchange(self, stream, ptrs, elem_bytes: int, kk: int, kstart: int, kend: int, down: int, up: int,
+                 below: int, above: int) -> None:
+        import numpy as np
+        import torch
+        import torch.distributed as dist
+
+        from .cuda._abi import check, lib
+
+        plane = kk * elem_bytes
+        stream.synchronize()  # the planes to send are final (the comm stream waited on compute)
+        reqs, sinks = [], []
+        for ptr in ptrs:
+            for op, peer, first, count in halo_plan(kstart, kend, down, up, below, above):
+                buf = np.empty(count * plane, dtype=np.uint8)
+                if op == "send":
+                    check(lib().klb_memcpy_dtoh(buf.ctypes.data, ptr + first * plane, count * plane, stream.handle))
+                    stream.synchronize()
+                    reqs.append(dist.isend(torch.from_numpy(buf), peer))
+                else:
+                    t = torch.from_numpy(buf)
+                    reqs.append(dist.irecv(t, peer))
+                    sinks.append((ptr + first * plane, buf))
+        for req in reqs:
+            req.wait()
+        for dst, buf in sinks:
+            check(lib().klb_memcpy_htod(dst, buf.ctypes.data, buf.nbytes, stream.handle))
+        stream.synchronize()
+
+    def close(self) -> None:
+        pass
 
 
 @dataclass
