@@ -6,6 +6,7 @@ prints one valid JSON line (rank 0) for both arms."""
 
 import json
 import os
+import re
 import socket
 import subprocess
 import sys
@@ -35,8 +36,9 @@ def _torchrun(nproc, *args, timeout=900):
 def test_ranks_match_oracle(kernel, precision, grid, nproc):
     out = _torchrun(nproc, "tests/multiproc_slab_check.py", kernel, precision, grid)
     assert out.returncode == 0, out.stdout[-2000:] + out.stderr[-2000:]
-    oks = [line for line in out.stdout.splitlines() if " ok " in line]
-    assert len(oks) == nproc, out.stdout
+    # torchrun multiplexes the ranks' stdout (lines may run together)
+    assert len(re.findall(r"rank \d+ ok ", out.stdout)) == nproc, out.stdout
+    assert "FAIL" not in out.stdout
 
 
 def test_bench_two_ranks_prints_one_line_per_arm():
