@@ -3,27 +3,33 @@
 Each kernel is defined once per precision so the precision reaches the
 wisdom key (the reference ``kernel_key`` hashes only the space,
 so the name must carry it): ``advec_u_fp32``, ``advec_u_fp64``,
-``diff_uvw_fp32``, ``diff_uvw_fp64``.
+``diff_uvw_fp32`` … for the hot path (``KERNELS``), the fused
+``diff_uvw_rk3`` (``FUSED_KERNELS``: the base kernel's source compiled with a
+-D switch, same space) and the §8f family (``FAMILY_KERNELS``).
 
 Space = the paper's Table 2 (presets.table2_params, 7,776,000 raw points) plus
-two B200 knobs:
+three B200 knobs:
 
 ``staging``  "DIRECT" (the paper's kernel) | "ZMARCH" (register/shared-memory
-             z-marching column, SURVEY §7 step 7);
-``zchunk``   planes marched per block for ZMARCH (8..128); 1 under DIRECT,
-             so ``block_z * tile_z * zchunk`` is the z extent of a block in
-             both variants and one grid formula serves the whole space.
+             z-marching column) | "TMA" (z-march fed by cp.async.bulk.tensor
+             into an mbarrier ring; column tiles; packed fp32 pairs);
+``zchunk``   planes marched per block (8..128); 1 under DIRECT, so
+             ``block_z * tile_z * zchunk`` is the z extent of a block in every
+             family and one grid formula serves the whole space;
+``depth``    TMA prefetch depth (planes in flight beyond the ones read).
 
-Restrictions: ``block_x*block_y*block_z <= 1024`` (Table 2 limit) and, so the
-tuner never measures two names for one binary, the z-knobs are pinned to
-their defaults where they have no meaning (``zchunk`` under DIRECT;
-``block_z``/``tile_z``/``unroll_z``/``contiguous_z`` under ZMARCH).
+Restrictions: ``block_x*block_y*block_z <= 1024`` (Table 2 limit); knobs
+without meaning in a family pinned (no duplicate binaries); the TMA rings fit
+the 227 KB opt-in shared memory for the precision (exact byte expressions,
+so fp32 and fp64 spaces differ) and TMA boxes stay <= 256 elements.  The
+advection family (advec_v/w/s) and diff_c / evisc_smag have DIRECT + TMA
+spaces of the same shape; rk3_uvw is DIRECT only.
 
 Launch geometry: a 1-D list of blocks (the paper's "thread blocks are launched
 as a one-dimensional list ... each thread unravels its 1D block identifier",
 PAPER.md:425-431) of ``nbx*nby*nbz`` blocks; shared memory is derived per
-configuration for ZMARCH.  ``KL_JJ``/``KL_KK`` specialise the row/plane pitch
-from the launch's scalar arguments.
+configuration.  ``KL_JJ``/``KL_KK`` specialise the row/plane pitch from the
+launch's scalar arguments.
 """
 
 from __future__ import annotations
