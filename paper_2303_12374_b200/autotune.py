@@ -39,16 +39,30 @@ def tune_problem(kernel: str, precision: str, grid: tuple[int, int, int], ctx, *
                  budget: Budget | None = None, seed: int = 0, wisdom_dir: str | Path | None = "wisdom",
                  session_dir: str | Path | None = None, k_range: tuple[int, int] | None = None,
                  repetitions: int = 7, warmup: int = 3, restrict: str | None = None, family: str | None = None,
-                 log=print):
+                 isolate: bool = False, log=print):
     from .cuda.executor import CudaReplayExecutor
     from .stencils.layout import GridLayout
     from .stencils.problem import StencilProblem
 
     layout = GridLayout(*grid, precision)
-    prob = StencilProblem(kernel, layout, ctx)
-    args = prob.args(k_range)
-    executor = CudaReplayExecutor(None, ctx, definition=prob.definition, args=args, repetitions=repetitions,
-                                  warmup=warmup, flush_l2=True, verify=True, output_layout=layout)
+    if isolate:
+        # measurements in a worker process that is replaced after a sticky CUDA error (cuda/isolated.py)
+        from .cuda.isolated import IsolatedReplayExecutor
+        from .stencils.definitions import definition_for
+
+        if k_range is not None:
+            raise ValueError("isolated tuning of k sub-ranges is not supported")
+        prob = None
+        executor = IsolatedReplayExecutor({"kernel": kernel, "precision": precision, "grid": list(grid),
+                                           "device": ctx.ordinal}, repetitions=repetitions, warmup=warmup,
+                                          flush_l2=True, verify=True)
+        definition = definition_for(kernel, precision)
+    else:
+        prob = StencilProblem(kernel, layout, ctx)
+        args = prob.args(k_range)
+        executor = CudaReplayExecutor(None, ctx, definition=prob.definition, args=args, repetitions=repetitions,
+                                      warmup=warmup, flush_l2=True, verify=True, output_layout=layout)
+        definition = prob.definition
     t0 = time.time()
     count = [0]
 
@@ -58,9 +72,9 @@ def tune_problem(kernel: str, precision: str, grid: tuple[int, int, int], ctx, *
         if m.status == STATUS_OK and (count[0] % 10 == 0 or count[0] < 4):
             log(f"  [{count[0]}] {m.objective * 1e6:9.1f} us  {_short(rec.config)}")
 
-    default_cfg = prob.definition.space.default_config()[0]
+    default_cfg = definition.space.default_config()[0]
     default_m = executor.measure(default_cfg)
-    space = prob.definition.space
+    space = definition.space
     if family:
         from .stencils.definitions import family_space
 
@@ -72,7 +86,7 @@ def tune_problem(kernel: str, precision: str, grid: tuple[int, int, int], ctx, *
 
         space = ConfigSpace(space.params, list(space.restrictions) + [restrict])
     session = tune(space, executor, strategy=strategy, budget=budget or Budget(max_evaluations=50),
-                   seed=seed, device=ctx.ident, kernel_key=prob.definition.kernel_key(),
+                   seed=seed, device=ctx.ident, kernel_key=definition.kernel_key(),
                    problem=executor.problem, on_evaluation=progress)
     cells = executor.problem[0] * executor.problem[1] * executor.problem[2]
     from .stencils.problem import BYTES_PER_CELL_WORDS
@@ -103,7 +117,8 @@ def tune_problem(kernel: str, precision: str, grid: tuple[int, int, int], ctx, *
         append_result(wfile, session)
         wfile.save(wisdom_path(wisdom_dir, session.kernel_key))
     executor.close()
-    prob.close()
+    if prob is not None:
+        prob.close()
     return session, summary
 
 
@@ -129,6 +144,8 @@ def main(argv=None) -> int:
     ap.add_argument("--json-out", default=None)
     ap.add_argument("--restrict", default=None, help="extra restriction expression to explore a sub-space")
     ap.add_argument("--focused", action="store_true", help="restrict to FOCUSED_TMA (with --family TMA)")
+    ap.add_argument("--isolate", action="store_true",
+                    help="measure in a worker process replaced after a sticky CUDA error (cuda/isolated.py)")
     ap.add_argument("--family", choices=("DIRECT", "ZMARCH", "TMA"), default=None,
                     help="tune one staging family (its fixed knobs narrowed; see definitions.family_space)")
     a = ap.parse_args(argv)
@@ -139,7 +156,7 @@ def main(argv=None) -> int:
     restrict = FOCUSED_TMA if a.focused else a.restrict
     _, summary = tune_problem(a.kernel, a.precision, grid, ctx, strategy=a.strategy,
                               budget=Budget(a.budget_evals, a.budget_seconds), seed=a.seed, wisdom_dir=a.wisdom,
-                              session_dir=a.sessions, restrict=restrict, family=a.family)
+                              session_dir=a.sessions, restrict=restrict, family=a.family, isolate=a.isolate)
     line = json.dumps(summary, sort_keys=True)
     print(line)
     if a.json_out:

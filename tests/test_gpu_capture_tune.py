@@ -103,3 +103,36 @@ def test_device_capture_is_byte_identical_to_host_capture(gpu_ctx, tmp_path):
         assert cap.problem == (37, 21, 9) and len(cap.buffers) == 11
     finally:
         prob.close()
+
+
+def test_isolated_executor_survives_a_sticky_error(gpu_ctx, tmp_path):
+    """A configuration that traps poisons a CUDA context; the isolated executor
+    reports it launch_failed and measures the next configuration in a fresh
+    worker (the reference tuner never aborts on a failing configuration)."""
+    from paper_2303_12374_b200.backend import STATUS_LAUNCH_FAILED, STATUS_OK
+    from paper_2303_12374_b200.capture import BufferArg, Capture, ScalarArg, write_capture
+    from paper_2303_12374_b200.cuda.isolated import IsolatedReplayExecutor
+    from paper_2303_12374_b200.kerneldef import KernelDefinition
+    from paper_2303_12374_b200.space import ConfigSpace, TunableParam
+
+    src = ('extern "C" __global__ void trapk(float* x, int n) {\\n'
+           '  const int i = blockIdx.x * blockDim.x + threadIdx.x;\\n'
+           '  if (TRAP) __trap();\\n'
+           '  if (i < n) x[i] += 1.0f;\\n}\\n')
+    space = ConfigSpace([TunableParam("block", (32, 64), 32), TunableParam("trap", (0, 1), 0)])
+    d = KernelDefinition("trapk", space, source_text=src, problem_size=("arg1",), block=("block", 1, 1),
+                         grid=("ceil_div(problem_x, block)", 1, 1), defines=[("TRAP", "trap")])
+    n = 4096
+    cap = Capture(d, (n,), scalars=[ScalarArg(1, "i32", n)],
+                  buffers=[BufferArg(0, "output", "f32", np.zeros(n, np.float32).tobytes())])
+    path = tmp_path / "trapk.klcap"
+    write_capture(cap, path)
+    ex = IsolatedReplayExecutor({"capture": str(path)}, repetitions=3, warmup=1, timeout=120)
+    try:
+        assert ex.measure({"block": 64, "trap": 0}).status == STATUS_OK
+        assert ex.measure({"block": 32, "trap": 1}).status == STATUS_LAUNCH_FAILED
+        m = ex.measure({"block": 32, "trap": 0})
+        assert m.status == STATUS_OK and ex.restarts == 1
+        assert ex.describe()["isolated"] and ex.problem == (n,)
+    finally:
+        ex.close()
