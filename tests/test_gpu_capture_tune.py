@@ -115,10 +115,12 @@ def test_isolated_executor_survives_a_sticky_error(gpu_ctx, tmp_path):
     from paper_2303_12374_b200.kerneldef import KernelDefinition
     from paper_2303_12374_b200.space import ConfigSpace, TunableParam
 
-    src = ('extern "C" __global__ void trapk(float* x, int n) {\\n'
-           '  const int i = blockIdx.x * blockDim.x + threadIdx.x;\\n'
-           '  if (TRAP) __trap();\\n'
-           '  if (i < n) x[i] += 1.0f;\\n}\\n')
+    src = """extern "C" __global__ void trapk(float* x, int n) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (TRAP) __trap();
+  if (i < n) x[i] += 1.0f;
+}
+"""
     space = ConfigSpace([TunableParam("block", (32, 64), 32), TunableParam("trap", (0, 1), 0)])
     d = KernelDefinition("trapk", space, source_text=src, problem_size=("arg1",), block=("block", 1, 1),
                          grid=("ceil_div(problem_x, block)", 1, 1), defines=[("TRAP", "trap")])
