@@ -31,6 +31,15 @@ ANCHORS = (128, 256, 512, 1024)
 QUERIES = (192, 384, 768)
 
 
+def _shape(q) -> tuple[int, int, int]:
+    """A query/anchor: an int n (the cube n^3) or an (nx, ny, nz) tuple."""
+    return (q, q, q) if isinstance(q, int) else tuple(q)
+
+
+def _label(q) -> str:
+    return f"{q}^3" if isinstance(q, int) else "x".join(map(str, q))
+
+
 def _tune(kernel, precision, n, ctx, wdir, evals, log):
     """Per-shape optimum the way the wisdom files are made: an exhaustive
     session over the focused TMA sub-space plus a short random DIRECT one
@@ -40,10 +49,11 @@ def _tune(kernel, precision, n, ctx, wdir, evals, log):
     sessions = []
     for family, strategy, restrict, budget in (("TMA", "exhaustive", FOCUSED_TMA, Budget(4000, 900.0)),
                                                ("DIRECT", "random", None, Budget(max(4, evals // 4), 300.0))):
-        s, summary = tune_problem(kernel, precision, (n, n, n), ctx, strategy=strategy, budget=budget, seed=n,
+        s, summary = tune_problem(kernel, precision, _shape(n), ctx, strategy=strategy, budget=budget,
+                                  seed=_shape(n)[0],
                                   wisdom_dir=wdir, family=family, restrict=restrict, log=lambda *_: None)
         sessions.append(s)
-        log(f"  tuned {kernel} {precision} {n}^3 {family}: {summary.get('best_gbs', 0):.0f} GB/s "
+        log(f"  tuned {kernel} {precision} {_label(n)} {family}: {summary.get('best_gbs', 0):.0f} GB/s "
             f"({summary['evaluations']} evaluations)")
     return sessions
 
@@ -53,7 +63,7 @@ def _measure(kernel, precision, n, ctx, configs):
     from .stencils.layout import GridLayout
     from .stencils.problem import StencilProblem
 
-    lay = GridLayout(n, n, n, precision)
+    lay = GridLayout(*_shape(n), precision)
     prob = StencilProblem(kernel, lay, ctx)
     ex = CudaReplayExecutor(None, ctx, definition=prob.definition, args=prob.args(), output_layout=lay, verify=False)
     out = [ex.measure(c) for c in configs]
@@ -63,28 +73,36 @@ def _measure(kernel, precision, n, ctx, configs):
 
 
 def sweep(ctx, kernels=("advec_u", "diff_uvw"), precisions=("fp32", "fp64"), anchors=ANCHORS, queries=QUERIES,
-          evals=60, log=print) -> dict:
+          evals=60, log=print, anchor_wisdom: str | Path | None = None) -> dict:
+    """Selection from anchor wisdom vs the per-shape tuned optimum.  With
+    ``anchor_wisdom`` the anchors are the records of an existing wisdom
+    directory (e.g. the committed ``wisdom/``) instead of fresh sessions."""
     from .stencils.definitions import definition_for
 
-    results = {"anchors": list(anchors), "queries": list(queries), "rows": []}
+    results = {"anchors": "wisdom:" + str(anchor_wisdom) if anchor_wisdom else [_label(a) for a in anchors],
+               "queries": [_label(q) for q in queries], "rows": []}
     with tempfile.TemporaryDirectory() as tmp:
         for precision in precisions:
             for kernel in kernels:
                 d = definition_for(kernel, precision)
-                wdir = Path(tmp) / f"{kernel}_{precision}"
-                wdir.mkdir()
-                for n in anchors:
-                    _tune(kernel, precision, n, ctx, wdir, evals, log)
-                wfile = WisdomFile.load(wisdom_path(wdir, d.kernel_key()))
+                if anchor_wisdom:
+                    wfile = WisdomFile.load(wisdom_path(anchor_wisdom, d.kernel_key()))
+                else:
+                    wdir = Path(tmp) / f"{kernel}_{precision}"
+                    wdir.mkdir()
+                    for n in anchors:
+                        _tune(kernel, precision, n, ctx, wdir, evals, log)
+                    wfile = WisdomFile.load(wisdom_path(wdir, d.kernel_key()))
                 default = d.space.default_config()[0]
                 for q in queries:
-                    qdir = Path(tmp) / f"q_{kernel}_{precision}_{q}"
+                    qdir = Path(tmp) / f"q_{kernel}_{precision}_{_label(q)}"
                     qdir.mkdir()
                     sessions = _tune(kernel, precision, q, ctx, qdir, evals, log)
                     best = min((s for s in sessions if s.best is not None), key=lambda s: s.best_objective)
-                    choice = select(wfile, ctx.ident, (q, q, q), default)
+                    choice = select(wfile, ctx.ident, _shape(q), default)
                     m_sel, m_def = _measure(kernel, precision, q, ctx, [choice.config, default])
-                    row = {"kernel": kernel, "precision": precision, "query": q, "match_kind": choice.match_kind,
+                    row = {"kernel": kernel, "precision": precision, "query": q if isinstance(q, int) else list(q),
+                           "match_kind": choice.match_kind,
                            "selected_from": list(choice.record.problem) if choice.record else None,
                            "optimum_us": best.best_objective * 1e6}
                     for tag, m, cfg in (("selected", m_sel, choice.config), ("default", m_def, default)):
@@ -92,7 +110,7 @@ def sweep(ctx, kernels=("advec_u", "diff_uvw"), precisions=("fp32", "fp64"), anc
                             row[f"{tag}_us"] = m.objective * 1e6
                             row[f"{tag}_fraction"] = fraction_of_optimum(best, cfg, lambda c, m=m: m)
                     results["rows"].append(row)
-                    log(f"{kernel} {precision} {q}^3: selected {row.get('selected_fraction', 0):.3f} of optimum "
+                    log(f"{kernel} {precision} {_label(q)}: selected {row.get('selected_fraction', 0):.3f} of optimum "
                         f"(from {row['selected_from']}), default {row.get('default_fraction', 0):.3f}")
     for tag in ("selected", "default"):
         effs = [r.get(f"{tag}_fraction") for r in results["rows"]]
@@ -107,14 +125,23 @@ def main(argv=None) -> int:
     ap.add_argument("--evals", type=int, default=60)
     ap.add_argument("--device", type=int, default=0)
     ap.add_argument("--anchors", default=",".join(map(str, ANCHORS)))
-    ap.add_argument("--queries", default=",".join(map(str, QUERIES)))
+    ap.add_argument("--queries", default=",".join(map(str, QUERIES)),
+                    help="comma-separated; n for n^3 or NXxNYxNZ")
+    ap.add_argument("--anchor-wisdom", default=None, help="use this wisdom directory's records as the anchors")
     a = ap.parse_args(argv)
     from .cuda import open_device
 
     ctx = open_device(a.device)
     t0 = time.time()
-    res = sweep(ctx, anchors=tuple(int(x) for x in a.anchors.split(",")),
-                queries=tuple(int(x) for x in a.queries.split(",")), evals=a.evals)
+    def parse(text):
+        out = []
+        for tok in text.split(","):
+            dims = [int(x) for x in tok.lower().split("x")]
+            out.append(dims[0] if len(dims) == 1 else tuple(dims))
+        return tuple(out)
+
+    res = sweep(ctx, anchors=parse(a.anchors), queries=parse(a.queries), evals=a.evals,
+                anchor_wisdom=a.anchor_wisdom)
     res["seconds"] = round(time.time() - t0, 1)
     res["device"] = ctx.ident.to_json_obj()
     Path(a.out).write_text(json.dumps(res, indent=1, sort_keys=True))
