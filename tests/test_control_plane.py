@@ -321,3 +321,10 @@ def test_report_cuda_backend_parses_stencil_kernel_keys():
 
     with pytest.raises(ReportError):
         _CudaEvaluators.kernel_of(SimpleNamespace(kernel_key="grid3d-0123456789ab"))
+
+
+def test_portability_shapes_accept_cubes_and_boxes():
+    from paper_2303_12374_b200 import portability as p
+
+    assert p._shape(192) == (192, 192, 192) and p._shape((640, 640, 320)) == (640, 640, 320)
+    assert p._label(384) == "384^3" and p._label((1024, 512, 256)) == "1024x512x256"
