@@ -38,7 +38,7 @@ from ..backend import (
     LaunchError,
     Measurement,
 )
-from ..capture import ELEMENT_SIZES, BufferArg, Capture, ScalarArg, scalar_env_from_args
+from ..capture import ELEMENT_SIZES, Capture, scalar_env_from_args
 from ..expr import EvalError
 from ..kerneldef import DefinitionError, KernelDefinition
 from ..space import Configuration

@@ -16,8 +16,6 @@ its neighbours' interior planes, and the halo exchange keeps them so.
 
 from __future__ import annotations
 
-import ctypes as C
-
 import numpy as np
 
 from ..capture import ScalarArg

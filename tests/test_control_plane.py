@@ -12,7 +12,7 @@ import pytest
 from hypothesis import given, settings, strategies as st
 
 import kltune
-from kltune.backend import MockCompiler, SimCostModel, SimulatedExecutor, STATUS_OK
+from kltune.backend import MockCompiler, SimCostModel, SimulatedExecutor
 from kltune.capture import (BufferArg, CaptureFormatError, CapturePolicy, CaptureSession, ScalarArg,
                             capture_from_args, read_capture, serialize_capture, write_capture, write_capture_stream)
 from kltune.dispatch import WisdomKernel
