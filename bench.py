@@ -436,6 +436,62 @@ def suite_measure(ctx, compiler, wisdom_dir, peak, suite=SUITE):
     return rows
 
 
+GRAPH_SUITE = [("diff_uvw", "fp64", (64, 64, 64), "config 1"), ("advec_u", "fp32", (128, 128, 128), "128^3")]
+
+
+def graph_measure(ctx, compiler, wisdom_dir, n=200):
+    """Launch-bound small problems: n back-to-back applications of the tuned
+    kernel (L2 warm, no flush between them) enqueued one bound launch at a
+    time vs replayed as one captured CUDA graph (WisdomKernel.graph); device
+    time per application from events on the launching stream, plus the host
+    enqueue cost per application."""
+    from paper_2303_12374_b200.capture import CapturePolicy
+    from paper_2303_12374_b200.cuda import Event, Stream
+    from paper_2303_12374_b200.dispatch import WisdomKernel
+    from paper_2303_12374_b200.stencils.layout import GridLayout
+    from paper_2303_12374_b200.stencils.problem import StencilProblem
+
+    rows = []
+    stream = Stream.create()
+    try:
+        for kernel, precision, grid, tag in GRAPH_SUITE:
+            lay = GridLayout(*grid, precision)
+            prob = StencilProblem(kernel, lay, ctx)
+            wk = WisdomKernel(prob.definition, compiler, wisdom_dir=wisdom_dir, capture_policy=CapturePolicy())
+            run = wk.bind(ctx.ident, prob.args(), stream=stream)
+            g = wk.graph(ctx.ident, prob.args(), stream, repeat=n)
+            row = {"config": tag, "kernel": kernel, "precision": precision, "grid": list(grid), "applications": n}
+            for variant in ("eager", "graph"):
+                best = None
+                for _ in range(3):
+                    (run() if variant == "eager" else g.launch(stream))  # warm
+                    stream.synchronize()
+                    e0, e1 = Event(), Event()
+                    e0.record(stream)
+                    t0 = time.perf_counter()
+                    if variant == "eager":
+                        for _ in range(n):
+                            run()
+                    else:
+                        g.launch(stream)
+                    host = time.perf_counter() - t0
+                    e1.record(stream)
+                    e1.synchronize()
+                    dev = e0.elapsed_ms(e1) * 1e-3
+                    if best is None or dev < best[0]:
+                        best = (dev, host)
+                row[variant] = {"us_per_application": round(best[0] / n * 1e6, 3),
+                                "host_enqueue_us_per_application": round(best[1] / n * 1e6, 3),
+                                "gcells": round(lay.cells * n / best[0] / 1e9, 2)}
+            row["graph_speedup"] = round(row["eager"]["us_per_application"] / row["graph"]["us_per_application"], 3)
+            g.close()
+            prob.close()
+            rows.append(row)
+    finally:
+        stream.close()
+    return rows
+
+
 def run_ours(args, dist):
     from paper_2303_12374_b200.cuda import NvrtcCompiler, open_device
     from paper_2303_12374_b200.halo import NcclExchanger, StagedExchanger
@@ -557,6 +613,10 @@ def run_ours(args, dist):
             line["fusion"] = {"rows": rows, "summary": fusion_summary(rows)}
         except Exception as err:
             line["fusion"] = {"error": repr(err)[:300]}
+        try:
+            line["graph"] = graph_measure(ctx, compiler, wisdom_dir)
+        except Exception as err:
+            line["graph"] = {"error": repr(err)[:300]}
     driver.close()
     if exchanger is not None:
         exchanger.close()

@@ -49,6 +49,7 @@ typedef void* klb_event;
 typedef void* klb_module;
 typedef void* klb_function;
 typedef void* klb_comm;
+typedef void* klb_graph; /* an instantiated (executable) CUDA graph */
 
 typedef struct klb_device_info {
   char name[256];
@@ -148,6 +149,18 @@ int klb_event_destroy(klb_event event);
 int klb_event_record(klb_event event, klb_stream stream);
 int klb_event_synchronize(klb_event event);
 int klb_event_elapsed_ms(klb_event start, klb_event stop, float* ms);
+
+/* ---- CUDA graphs ----------------------------------------------------------
+ * No reference counterpart (the reference launches one kernel per call,
+ * dispatch.py:184-187): a sequence of klb_launch calls on a created stream,
+ * bracketed by begin/end capture, becomes one executable graph replayed by
+ * klb_graph_launch — the launch-bound small problems (BASELINE config 1) and
+ * multi-kernel time steps pay one launch instead of one per kernel.
+ * klb_stream_end_capture always ends the capture, also on failure. */
+int klb_stream_begin_capture(klb_stream stream);
+int klb_stream_end_capture(klb_stream stream, klb_graph* graph);
+int klb_graph_launch(klb_graph graph, klb_stream stream);
+int klb_graph_destroy(klb_graph graph);
 
 /* ---- module globals / TMA descriptors ------------------------------------
  * A runtime-compiled kernel may request TMA tensor maps for some of its

@@ -42,7 +42,7 @@ int g_default_ordinal = -1;
 // CUDA driver API, resolved at runtime through cudaGetDriverEntryPoint so the
 // library has no link-time dependency on libcuda.so.1: it loads (and reports
 // a clean error from klb_init) on hosts without an NVIDIA driver.
-#define KLB_DRIVER_API(X) X(cuCtxGetCurrent) X(cuCtxSetCurrent) X(cuCtxSynchronize) X(cuDeviceGet) X(cuDeviceGetAttribute) X(cuDeviceGetCount) X(cuDeviceGetName) X(cuDeviceGetUuid) X(cuDevicePrimaryCtxRetain) X(cuDeviceTotalMem) X(cuDriverGetVersion) X(cuEventCreate) X(cuEventDestroy) X(cuEventElapsedTime) X(cuEventRecord) X(cuEventSynchronize) X(cuFuncGetAttribute) X(cuFuncSetAttribute) X(cuGetErrorName) X(cuGetErrorString) X(cuInit) X(cuLaunchKernel) X(cuMemAlloc) X(cuMemFree) X(cuMemFreeHost) X(cuMemGetInfo) X(cuMemHostAlloc) X(cuMemcpyDtoDAsync) X(cuMemcpyDtoHAsync) X(cuMemcpyHtoDAsync) X(cuMemsetD32Async) X(cuMemsetD8Async) X(cuModuleGetFunction) X(cuModuleLoadData) X(cuModuleUnload) X(cuOccupancyMaxActiveBlocksPerMultiprocessor) X(cuStreamCreateWithPriority) X(cuStreamDestroy) X(cuStreamSynchronize) X(cuStreamWaitEvent) X(cuModuleGetGlobal) X(cuTensorMapEncodeTiled)
+#define KLB_DRIVER_API(X) X(cuCtxGetCurrent) X(cuCtxSetCurrent) X(cuCtxSynchronize) X(cuDeviceGet) X(cuDeviceGetAttribute) X(cuDeviceGetCount) X(cuDeviceGetName) X(cuDeviceGetUuid) X(cuDevicePrimaryCtxRetain) X(cuDeviceTotalMem) X(cuDriverGetVersion) X(cuEventCreate) X(cuEventDestroy) X(cuEventElapsedTime) X(cuEventRecord) X(cuEventSynchronize) X(cuFuncGetAttribute) X(cuFuncSetAttribute) X(cuGetErrorName) X(cuGetErrorString) X(cuInit) X(cuLaunchKernel) X(cuMemAlloc) X(cuMemFree) X(cuMemFreeHost) X(cuMemGetInfo) X(cuMemHostAlloc) X(cuMemcpyDtoDAsync) X(cuMemcpyDtoHAsync) X(cuMemcpyHtoDAsync) X(cuMemsetD32Async) X(cuMemsetD8Async) X(cuModuleGetFunction) X(cuModuleLoadData) X(cuModuleUnload) X(cuOccupancyMaxActiveBlocksPerMultiprocessor) X(cuStreamCreateWithPriority) X(cuStreamDestroy) X(cuStreamSynchronize) X(cuStreamWaitEvent) X(cuModuleGetGlobal) X(cuTensorMapEncodeTiled) X(cuStreamBeginCapture) X(cuStreamEndCapture) X(cuGraphInstantiateWithFlags) X(cuGraphLaunch) X(cuGraphDestroy) X(cuGraphExecDestroy)
 
 struct DriverApi {
 #define KLB_DECL(name) decltype(&::name) name = nullptr;
@@ -682,6 +682,47 @@ int klb_event_synchronize(klb_event event) {
 int klb_event_elapsed_ms(klb_event start, klb_event stop, float* ms) {
   CTX_TRY();
   CU_TRY(drv.cuEventElapsedTime(ms, reinterpret_cast<CUevent>(start), reinterpret_cast<CUevent>(stop)));
+  return 0;
+}
+
+// ---- CUDA graphs -------------------------------------------------------------------
+// A launch sequence recorded by stream capture and replayed with one
+// cuGraphLaunch: the kernel parameters (TMA descriptors included) are copied
+// into the graph at capture time.  Thread-local capture mode, so another host
+// thread's unrelated CUDA calls do not invalidate the capture.
+
+int klb_stream_begin_capture(klb_stream stream) {
+  CTX_TRY();
+  if (!stream) return fail(KLB_E_INVALID, "graph capture needs a created (non-default) stream");
+  CU_TRY(drv.cuStreamBeginCapture(as_stream(stream), CU_STREAM_CAPTURE_MODE_THREAD_LOCAL));
+  return 0;
+}
+
+int klb_stream_end_capture(klb_stream stream, klb_graph* graph) {
+  if (!graph) return fail(KLB_E_INVALID, "graph output pointer is null");
+  *graph = nullptr;
+  CTX_TRY();
+  CUgraph g = nullptr;
+  // always ends the capture (a failed capture leaves the stream usable again)
+  CU_TRY(drv.cuStreamEndCapture(as_stream(stream), &g));
+  if (!g) return fail(KLB_E_INVALID, "stream capture produced no graph");
+  CUgraphExec exec = nullptr;
+  CUresult r = drv.cuGraphInstantiateWithFlags(&exec, g, 0);
+  drv.cuGraphDestroy(g);
+  if (r != CUDA_SUCCESS) return cu_fail(r, "cuGraphInstantiateWithFlags");
+  *graph = exec;
+  return 0;
+}
+
+int klb_graph_launch(klb_graph graph, klb_stream stream) {
+  CTX_TRY();
+  CU_TRY(drv.cuGraphLaunch(reinterpret_cast<CUgraphExec>(graph), as_stream(stream)));
+  return 0;
+}
+
+int klb_graph_destroy(klb_graph graph) {
+  CTX_TRY();
+  CU_TRY(drv.cuGraphExecDestroy(reinterpret_cast<CUgraphExec>(graph)));
   return 0;
 }
 

@@ -8,11 +8,11 @@ them reach the GPU only through the C ABI in ``libklb200.so``
 
 from ._abi import KlbError, library_path
 from .compiler import CompiledImage, CudaExecutable, NvrtcCompiler
-from .device import DeviceArray, DeviceBuffer, DeviceContext, Event, HostPinned, Stream, open_device
+from .device import DeviceArray, DeviceBuffer, DeviceContext, Event, Graph, HostPinned, Stream, open_device
 
 __all__ = [
     "KlbError", "library_path", "CompiledImage", "CudaExecutable", "NvrtcCompiler", "DeviceArray", "DeviceBuffer",
-    "DeviceContext", "Event", "HostPinned", "Stream", "open_device", "CudaReplayExecutor",
+    "DeviceContext", "Event", "Graph", "HostPinned", "Stream", "open_device", "CudaReplayExecutor",
 ]
 
 

@@ -109,6 +109,10 @@ EXPORTS: dict[str, list] = {
     "klb_event_record": [_vp, _vp],
     "klb_event_synchronize": [_vp],
     "klb_event_elapsed_ms": [_vp, _vp, C.POINTER(C.c_float)],
+    "klb_stream_begin_capture": [_vp],
+    "klb_stream_end_capture": [_vp, _pvp],
+    "klb_graph_launch": [_vp, _vp],
+    "klb_graph_destroy": [_vp],
     "klb_module_global": [_vp, C.c_char_p, C.POINTER(_u64), C.POINTER(_sz)],
     "klb_tensor_map_encode_3d": [_vp, _i, _u64, C.POINTER(_u64), C.POINTER(_u64), C.POINTER(C.c_uint)],
     "klb_synth_field": [_u64, _i, _ll, _i, _i, _i, _i, _ll, _i, _i, _i, _i, _u64, _d, _d, _i, _vp],

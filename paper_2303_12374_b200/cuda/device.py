@@ -16,6 +16,8 @@ from __future__ import annotations
 
 import ctypes as C
 import threading
+from collections.abc import Iterator
+from contextlib import contextmanager
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -67,6 +69,49 @@ class Stream:
         if self._owned and self.handle:
             check(lib().klb_stream_destroy(self.handle))
             self.handle, self._owned = None, False
+
+
+class Graph:
+    """An executable CUDA graph: the launches enqueued on a stream between
+    ``capture`` entry and exit, replayed by one ``launch`` (klb_graph_*).
+    Kernel parameters are copied in at capture time; the buffers they point
+    to must stay allocated while the graph is used."""
+
+    def __init__(self) -> None:
+        self.handle = None
+
+    @classmethod
+    @contextmanager
+    def capture(cls, stream: Stream) -> Iterator["Graph"]:
+        if stream is None or not stream.handle:
+            raise ValueError("graph capture needs a created (non-default) stream")
+        g = cls()
+        check(lib().klb_stream_begin_capture(stream.handle))
+        h = C.c_void_p()
+        try:
+            yield g
+        except BaseException:
+            if lib().klb_stream_end_capture(stream.handle, C.byref(h)) == 0 and h.value:
+                lib().klb_graph_destroy(h.value)
+            raise
+        check(lib().klb_stream_end_capture(stream.handle, C.byref(h)))
+        g.handle = h.value
+
+    def launch(self, stream: Stream) -> None:
+        if self.handle is None:
+            raise ValueError("graph was not captured (or is closed)")
+        check(lib().klb_graph_launch(self.handle, stream.handle))
+
+    def close(self) -> None:
+        if self.handle:
+            check(lib().klb_graph_destroy(self.handle))
+            self.handle = None
+
+    def __del__(self) -> None:
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 class Event:

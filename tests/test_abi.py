@@ -63,3 +63,23 @@ def test_nvrtc_compiles_sm100a_without_gpu():
     with pytest.raises(CompileError) as err:
         comp.compile_image(CompileRequest("__global__ void k() { syntax error }", "k", (), ()), dev)
     assert "error" in err.value.diagnostics
+
+
+def test_graph_capture_without_a_device_fails_cleanly():
+    """CUDA-graph capture refuses the legacy default stream before any driver
+    call, and the C ABI reports a clean error (not a crash) without a GPU."""
+    from paper_2303_12374_b200.cuda import Graph, Stream
+    from paper_2303_12374_b200.cuda._abi import KlbError, check, lib, library_path
+
+    with pytest.raises(ValueError):
+        with Graph.capture(Stream()):
+            pass
+    if not library_path().exists():
+        pytest.skip("libklb200.so not built")
+    n = ctypes.c_int(-1)
+    if lib().klb_device_count(ctypes.byref(n)) == 0 and n.value > 0:
+        pytest.skip("a GPU is visible here")
+    g = ctypes.c_void_p()
+    with pytest.raises(KlbError):
+        check(lib().klb_stream_end_capture(None, ctypes.byref(g)))
+    assert g.value is None

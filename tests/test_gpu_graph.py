@@ -1,0 +1,93 @@
+"""CUDA-graph replay of bound launches (klb_stream_*_capture / klb_graph_*).
+
+``WisdomKernel.graph`` captures ``repeat`` launches of the wisdom-selected
+configuration on a stream; replaying the graph must leave exactly the bytes
+the same launches leave when enqueued one by one (the kernel parameters — TMA
+descriptors included — are copied into the graph at capture), and one
+captured application must match the oracle.
+"""
+
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from stencil_helpers import TOL, oracle_outputs, rel_error
+
+pytestmark = pytest.mark.gpu
+
+WISDOM = Path(__file__).resolve().parent.parent / "wisdom"
+
+
+@pytest.mark.parametrize("kernel,precision,grid", [("diff_uvw", "fp64", (64, 64, 64)),
+                                                   ("advec_u", "fp32", (96, 40, 70)),
+                                                   ("diff_uvw_rk3", "fp32", (72, 40, 33))])
+def test_graph_replay_matches_eager_launches(gpu_ctx, kernel, precision, grid):
+    from paper_2303_12374_b200.cuda import NvrtcCompiler, Stream
+    from paper_2303_12374_b200.dispatch import WisdomKernel
+    from paper_2303_12374_b200.stencils.layout import GridLayout
+    from paper_2303_12374_b200.stencils.problem import StencilProblem
+
+    lay = GridLayout(*grid, precision)
+    prob = StencilProblem(kernel, lay, gpu_ctx)
+    stream = Stream.create()
+    try:
+        wk = WisdomKernel(prob.definition, NvrtcCompiler(gpu_ctx), wisdom_dir=WISDOM)
+        n = 4
+        run = wk.bind(gpu_ctx.ident, prob.args(), stream=stream)
+        for _ in range(n):
+            run()
+        stream.synchronize()
+        eager = {name: prob.download(name).copy() for name in prob.outputs()}
+
+        prob.regenerate()
+        before = {name: prob.download(name).copy() for name in prob.outputs()}
+        g = wk.graph(gpu_ctx.ident, prob.args(), stream, repeat=n)
+        stream.synchronize()
+        for name in before:  # capturing records the launches, it does not run them
+            assert np.array_equal(prob.download(name), before[name]), name
+        g.launch(stream)
+        stream.synchronize()
+        for name in eager:
+            assert np.array_equal(prob.download(name), eager[name]), name
+        g.close()
+
+        prob.regenerate()
+        one = wk.graph(gpu_ctx.ident, prob.args(), stream, repeat=1)
+        one.launch(stream)
+        stream.synchronize()
+        ref, _ = oracle_outputs(kernel, lay)
+        for name in ref:
+            assert rel_error(prob.download(name), ref[name], lay) <= TOL[precision], name
+        one.close()
+    finally:
+        prob.close()
+        stream.close()
+
+
+def test_failed_capture_leaves_the_stream_usable(gpu_ctx):
+    from paper_2303_12374_b200.cuda import Graph, NvrtcCompiler, Stream
+    from paper_2303_12374_b200.dispatch import WisdomKernel
+    from paper_2303_12374_b200.stencils.layout import GridLayout
+    from paper_2303_12374_b200.stencils.problem import StencilProblem
+
+    lay = GridLayout(40, 24, 12, "fp64")
+    prob = StencilProblem("advec_u", lay, gpu_ctx)
+    stream = Stream.create()
+    try:
+        wk = WisdomKernel(prob.definition, NvrtcCompiler(gpu_ctx), wisdom_dir=WISDOM)
+        run = wk.bind(gpu_ctx.ident, prob.args(), stream=stream)
+        with pytest.raises(RuntimeError, match="abandon"):
+            with Graph.capture(stream):
+                run()
+                raise RuntimeError("abandon the capture")
+        with pytest.raises(ValueError):
+            Graph.capture(Stream()).__enter__()  # the legacy default stream cannot be captured
+        prob.regenerate()
+        run()  # the stream left capture mode: eager launches work again
+        stream.synchronize()
+        ref, _ = oracle_outputs("advec_u", lay)
+        assert rel_error(prob.download("ut"), ref["ut"], lay) <= TOL["fp64"]
+    finally:
+        prob.close()
+        stream.close()
