@@ -78,6 +78,7 @@ class StencilProblem:
         glob = profiles if profiles is not None else make_profiles(self.kcells_global, layout.kgc)
         self.profiles = glob.window(k_offset, layout.kcells).as_dtype(layout.dtype)
         self.fields: dict[str, DeviceArray] = {}
+        self._borrowed: set[str] = set()  # fields aliased from another problem (share_fields)
         for name in KERNEL_FIELDS[kernel]:
             arr = DeviceArray(layout.alloc_bytes)
             arr.zero(self.stream)
@@ -153,6 +154,23 @@ class StencilProblem:
         out[pos_ke] = ScalarArg(pos_ke, "i32", ke)
         return out
 
+    def share_fields(self, other: "StencilProblem", names) -> None:
+        """Use ``other``'s device buffers for ``names`` — kernels chained in one
+        time step (evisc_smag's evisc feeding diff_uvw, the tendencies the
+        advection and diffusion kernels accumulate into) read and write the
+        same fields instead of copies.  The borrowed buffers stay owned by
+        ``other``; ``regenerate`` refills them like this problem's own."""
+        if other.layout != self.layout:
+            raise ValueError("shared fields need identical layouts")
+        for name in names:
+            if name not in self.fields or name not in other.fields:
+                raise KeyError(f"{name!r} is not a field of both {self.kernel} and {other.kernel}")
+            if name not in self._borrowed:
+                self.fields[name].free()
+            self.fields[name] = other.fields[name]
+            self._borrowed.add(name)
+        self._args = self._build_args()
+
     def scalar_env(self) -> dict[str, int]:
         from ..capture import scalar_env_from_args
 
@@ -163,7 +181,8 @@ class StencilProblem:
         return BYTES_PER_CELL_WORDS[self.kernel] * self.layout.elem_bytes * self.layout.cells
 
     def close(self) -> None:
-        for arr in list(self.fields.values()) + list(self.profile_arrays.values()):
+        own = [a for n, a in self.fields.items() if n not in self._borrowed]
+        for arr in own + list(self.profile_arrays.values()):
             arr.free()
         self.fields.clear()
         self.profile_arrays.clear()

@@ -91,3 +91,65 @@ def test_failed_capture_leaves_the_stream_usable(gpu_ctx):
     finally:
         prob.close()
         stream.close()
+
+
+def test_chained_step_graph_matches_the_oracle_chain(gpu_ctx):
+    """A time-step fragment as one graph: evisc_smag (u, v, w -> evisc) then the
+    fused diff_uvw + RK3 substep reading that evisc and the same u, v, w
+    (StencilProblem.share_fields).  Graph replay == eager launches bit for bit,
+    and both match the oracle chain (evisc_smag -> diff_uvw_rk3 on its output)."""
+    from oracle import family_oracle
+    from paper_2303_12374_b200.cuda import Graph, NvrtcCompiler, Stream
+    from paper_2303_12374_b200.dispatch import WisdomKernel
+    from paper_2303_12374_b200.stencils.layout import GridLayout
+    from paper_2303_12374_b200.stencils.problem import CS, RK_A, RK_BDT, StencilProblem
+    from paper_2303_12374_b200.stencils.profiles import make_profiles
+    from stencil_helpers import host_fields
+
+    lay = GridLayout(70, 38, 29, "fp64")
+    pe = StencilProblem("evisc_smag", lay, gpu_ctx)
+    pd = StencilProblem("diff_uvw_rk3", lay, gpu_ctx)
+    stream = Stream.create()
+    try:
+        pd.share_fields(pe, ("evisc", "u", "v", "w"))
+        comp = NvrtcCompiler(gpu_ctx)
+        run_e = WisdomKernel(pe.definition, comp, wisdom_dir=WISDOM).bind(gpu_ctx.ident, pe.args(), stream=stream)
+        run_d = WisdomKernel(pd.definition, comp, wisdom_dir=WISDOM).bind(gpu_ctx.ident, pd.args(), stream=stream)
+        outs = ("evisc", "ut", "vt", "wt", "u_next", "v_next", "w_next")
+
+        def fetch():
+            return {n: (pe if n == "evisc" else pd).download(n).copy() for n in outs}
+
+        run_e()
+        run_d()
+        stream.synchronize()
+        eager = fetch()
+
+        pe.regenerate()
+        pd.regenerate()
+        with Graph.capture(stream) as g:
+            run_e()
+            run_d()
+        g.launch(stream)
+        stream.synchronize()
+        got = fetch()
+        for n in outs:
+            assert np.array_equal(got[n], eager[n]), n
+        g.close()
+
+        f = host_fields(lay, ("evisc", "u", "v", "w", "ut", "vt", "wt", "u_next", "v_next", "w_next"))
+        prof = make_profiles(lay.kcells, lay.kgc).as_dtype(lay.dtype)
+        gh = (lay.igc, lay.jgc, lay.kgc)
+        evisc = family_oracle.evisc_smag(f["evisc"], f["u"], f["v"], f["w"], prof.dzi, prof.dzhi, 1.0, 1.0, CS,
+                                         ghost=gh)
+        ref = dict(zip(("ut", "vt", "wt", "u_next", "v_next", "w_next"),
+                       family_oracle.diff_uvw_rk3(f["ut"], f["vt"], f["wt"], evisc, f["u"], f["v"], f["w"],
+                                                  f["u_next"], f["v_next"], f["w_next"], prof.dzi, prof.dzhi,
+                                                  prof.rhoref, prof.rhorefh, 1.0, 1.0, RK_A, RK_BDT, ghost=gh)))
+        ref["evisc"] = evisc
+        for n in outs:
+            assert rel_error(got[n], ref[n], lay) <= TOL["fp64"], n
+    finally:
+        pd.close()
+        pe.close()
+        stream.close()
