@@ -100,7 +100,7 @@ int klb_nvrtc_version(int* major, int* minor);
  * the reference CompileRequest.entry ("name" or "name<args>"); it is passed to
  * nvrtcAddNameExpression and the lowered (mangled) name is returned.
  * options: NVRTC option strings (e.g. "--gpu-architecture=sm_100a",
- * "-D TILE_X=2", "-std=c++17").  On success *image/*image_size hold the CUBIN
+ * "-D TILE_X=2", "-std=c++17").  On success *image and *image_size hold the CUBIN
  * and *lowered_name the symbol; on failure (KLB_E_COMPILE) *log holds the
  * compiler log.  Free all returned buffers with klb_free. */
 int klb_compile(const char* source, const char* program_name, const char* entry,
