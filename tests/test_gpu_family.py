@@ -119,7 +119,7 @@ def test_family_tma_advection_matches_oracle(gpu_ctx, compiler, kernel, precisio
                 assert err <= TOL[precision], (grid, cfg, name, err)
 
 
-@pytest.mark.parametrize("kernel", ["advec_v", "advec_w", "advec_s"])
+@pytest.mark.parametrize("kernel", ["advec_v", "advec_w", "advec_s", "diff_c", "evisc_smag"])
 def test_family_tma_misaligned_fields_use_scalar_path(gpu_ctx, compiler, kernel):
     """Pointers shifted off the 16-byte grid: the uniform scalar-access branch
     of the family TMA kernel gives the oracle result too."""
@@ -176,7 +176,11 @@ def test_family_tma_plane_march_matches_oracle(gpu_ctx, compiler, kernel, precis
     cfgs = family_space(kernel, "TMA", precision).sample_random(19, 3)
     cfgs += [dict(base, staging="TMA", block_x=32, block_y=4, tile_x=1, tile_y=2, depth=2, zchunk=16),
              dict(base, staging="TMA", contiguous_x=True, block_x=16, block_y=2, tile_x=4, tile_y=3, depth=1,
-                  zchunk=8, unravel="XYZ")]
+                  zchunk=8, unravel="XYZ"),
+             dict(base, staging="TMA", contiguous_x=True, block_x=32, block_y=2, tile_x=4, tile_y=4, depth=2,
+                  zchunk=16, unravel="XYZ"),
+             dict(base, staging="TMA", contiguous_x=True, block_x=64, block_y=1, tile_x=2, tile_y=1, depth=3,
+                  zchunk=32, unravel="XYZ")]
     for grid in ((45, 23, 19), (130, 37, 41)):
         lay = GridLayout(*grid, precision)
         ref, _ = oracle_outputs(kernel, lay)
