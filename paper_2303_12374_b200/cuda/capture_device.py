@@ -28,7 +28,7 @@ import zlib
 from pathlib import Path
 from typing import Sequence
 
-from ..capture import BufferArg, ScalarArg, header_block, metadata_block, scalar_env_from_args, _round_up
+from ..capture import ADDRESS_ALIGN, BufferArg, ScalarArg, header_block, metadata_block, scalar_env_from_args, _round_up
 from ..kerneldef import KernelDefinition
 from ._abi import check, lib
 from .device import DeviceBuffer, Event, HostPinned, Stream
@@ -54,12 +54,12 @@ def write_capture_device(definition: KernelDefinition, args: Sequence[object], p
     for b in buffers:
         if isinstance(b, DeviceBuffer):
             descs.append((b.position, b.role, b.element_type, b.element_count, b.nbytes,
-                          device_crc32(b.ptr, b.nbytes, stream)))
+                          device_crc32(b.ptr, b.nbytes, stream), b.ptr % ADDRESS_ALIGN))
         else:
             descs.append((b.position, b.role, b.element_type, b.element_count, len(b.data),
-                          zlib.crc32(b.data) & 0xFFFFFFFF))
-    meta = metadata_block(definition, problem, scalars, descs, application, timestamp)
+                          zlib.crc32(b.data) & 0xFFFFFFFF, b.address_mod))
     target = Path(path)
+    meta = metadata_block(definition, problem, scalars, descs, application, timestamp, target=target)
     target.parent.mkdir(parents=True, exist_ok=True)
     fd, scratch = tempfile.mkstemp(prefix=target.name + ".", suffix=".tmp", dir=str(target.parent))
     staging = [HostPinned(chunk), HostPinned(chunk)]
@@ -87,12 +87,12 @@ def write_capture_device(definition: KernelDefinition, args: Sequence[object], p
                     if pending is not None:
                         pk, psize = pending
                         events[pk].synchronize()
-                        out.write(C.string_at(staging[pk].ptr, psize))
+                        out.write((C.c_char * psize).from_address(staging[pk].ptr))
                     pending = (k, size)
                 if pending is not None:
                     pk, psize = pending
                     events[pk].synchronize()
-                    out.write(C.string_at(staging[pk].ptr, psize))
+                    out.write((C.c_char * psize).from_address(staging[pk].ptr))
                 cursor += gap + n
         os.replace(scratch, target)
     except BaseException:

@@ -23,7 +23,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from ..backend import DeviceIdent
-from ..capture import ELEMENT_SIZES, BufferArg
+from ..capture import ADDRESS_ALIGN, ELEMENT_SIZES, BufferArg
 from ._abi import DeviceInfo, check, lib
 
 __all__ = [
@@ -254,7 +254,8 @@ class DeviceBuffer:
         out = C.create_string_buffer(max(self.nbytes, 1))
         check(lib().klb_memcpy_dtoh(out, self.ptr, self.nbytes, None))
         check(lib().klb_device_synchronize())
-        return BufferArg(self.position, self.role, self.element_type, out.raw[: self.nbytes])
+        return BufferArg(self.position, self.role, self.element_type, out.raw[: self.nbytes],
+                         address_mod=self.ptr % ADDRESS_ALIGN)
 
 
 class DeviceContext:

@@ -24,6 +24,7 @@ backend.py:462 — SURVEY Appendix B.4), the captured buffers ARE replayed.
 
 from __future__ import annotations
 
+import ctypes as C
 import statistics
 import time
 from typing import Sequence
@@ -38,7 +39,7 @@ from ..backend import (
     LaunchError,
     Measurement,
 )
-from ..capture import ELEMENT_SIZES, Capture, scalar_env_from_args
+from ..capture import ADDRESS_ALIGN, ELEMENT_SIZES, Capture, CaptureFile, scalar_env_from_args
 from ..expr import EvalError
 from ..kerneldef import DefinitionError, KernelDefinition
 from ..space import Configuration
@@ -55,12 +56,15 @@ _STICKY = {700, 701, 702, 709, 710, 714, 715, 716, 717, 718, 719, 720}
 class CudaReplayExecutor(Executor):
     reentrant = False
 
-    def __init__(self, capture: Capture | None, ctx: DeviceContext, *, definition: KernelDefinition | None = None,
+    def __init__(self, capture: Capture | CaptureFile | None, ctx: DeviceContext, *,
+                 definition: KernelDefinition | None = None,
                  args: Sequence[object] | None = None, problem=None, compiler: NvrtcCompiler | None = None,
                  warmup: int = 3, repetitions: int = 7, flush_l2: bool = True, verify: bool = True,
-                 output_layout=None) -> None:
-        """Either ``capture`` (buffers uploaded here) or ``definition`` + device
-        ``args`` (+ ``problem``) of an already resident launch."""
+                 output_layout=None, chunk: int = 64 << 20) -> None:
+        """Either ``capture`` (a loaded ``Capture``, or a ``CaptureFile`` whose
+        payloads are streamed from disk to the device in ``chunk``-byte
+        pieces — see ``from_file``) or ``definition`` + device ``args``
+        (+ ``problem``) of an already resident launch."""
         self.ctx = ctx
         self.compiler = compiler or NvrtcCompiler(ctx)
         self.warmup = warmup
@@ -70,7 +74,11 @@ class CudaReplayExecutor(Executor):
         self.output_layout = output_layout
         self.broken: str | None = None
         self._owned: list[DeviceArray] = []
-        if capture is not None:
+        if isinstance(capture, CaptureFile):
+            self.definition = capture.definition
+            self.problem = tuple(capture.problem)
+            self.args = self._upload_file(capture, chunk)
+        elif capture is not None:
             self.definition = capture.definition
             self.problem = tuple(capture.problem)
             self.args = self._upload_capture(capture)
@@ -100,14 +108,77 @@ class CudaReplayExecutor(Executor):
 
         check(lib().klb_memcpy_dtod(dst, src, nbytes, self.ctx.stream.handle))
 
+    @classmethod
+    def from_file(cls, path, ctx: DeviceContext, **kwargs) -> "CudaReplayExecutor":
+        """Replay a ``.klcap`` without loading it into host memory: each
+        payload is read in chunks into two pinned staging buffers, CRC-checked
+        on the way, and uploaded asynchronously (the read of chunk i+1
+        overlaps the H2D copy of chunk i).  Host memory: two chunks."""
+        return cls(CaptureFile.open(path), ctx, **kwargs)
+
+    def _placed(self, nbytes: int, address_mod: int | None) -> tuple[DeviceArray, int]:
+        """A device allocation and the address inside it that reproduces the
+        captured argument's alignment (``address_mod`` = original address mod
+        ``ADDRESS_ALIGN``): the application's fields put every interior row
+        on a 128-byte boundary, which the TMA kernels' vector path needs, so
+        the replay must not time the misaligned fallback instead."""
+        if address_mod is None:
+            arr = DeviceArray(nbytes)
+            return arr, arr.ptr
+        arr = DeviceArray(nbytes + ADDRESS_ALIGN)
+        return arr, arr.ptr + (address_mod - arr.ptr) % ADDRESS_ALIGN
+
     def _upload_capture(self, cap: Capture) -> list:
+        from ._abi import check, lib
+
         args: list = list(cap.scalars)
         for b in cap.buffers:
-            arr = DeviceArray(len(b.data))
+            arr, ptr = self._placed(len(b.data), b.address_mod)
             if b.data:
-                arr.upload(b.data, stream=self.ctx.stream)
+                check(lib().klb_memcpy_htod(ptr, b.data, len(b.data), self.ctx.stream.handle))
+                self.ctx.stream.synchronize()
             self._owned.append(arr)
-            args.append(DeviceBuffer(b.position, b.role, b.element_type, arr.ptr, b.element_count, owner=arr))
+            args.append(DeviceBuffer(b.position, b.role, b.element_type, ptr, b.element_count, owner=arr))
+        return args
+
+    def _upload_file(self, capfile: CaptureFile, chunk: int) -> list:
+        from ._abi import check, lib
+        from .device import Event, HostPinned
+
+        stream = self.ctx.stream
+        args: list = list(capfile.scalars)
+        entries = capfile.buffers
+        longest = max((e["byte_length"] for e in entries), default=0)
+        chunk = max(ELEMENT_SIZES["f64"], min(chunk, longest))
+        staging = [HostPinned(chunk), HostPinned(chunk)]
+        events = [Event(), Event()]
+        pending = [False, False]
+        self.host_staging_bytes = 2 * chunk
+        try:
+            views = [(C.c_char * chunk).from_address(h.ptr) for h in staging]
+            for index, e in enumerate(entries):
+                arr, ptr = self._placed(e["byte_length"], e.get("address_mod128"))
+                self._owned.append(arr)
+
+                def consume(slot, offset, size, ptr=ptr):
+                    check(lib().klb_memcpy_htod(ptr + offset, staging[slot].ptr, size, stream.handle))
+                    events[slot].record(stream)
+                    pending[slot] = True
+
+                def ready(slot):
+                    if pending[slot]:
+                        events[slot].synchronize()
+                        pending[slot] = False
+
+                consume.ready = ready
+                capfile.read_into(index, views, consume)
+                count = e["byte_length"] // ELEMENT_SIZES[e["element_type"]]
+                args.append(DeviceBuffer(e["position"], e["role"], e["element_type"], ptr, count, owner=arr))
+            stream.synchronize()
+        finally:
+            stream.synchronize()
+            for h in staging:
+                h.free()
         return args
 
     def restore_outputs(self) -> None:
@@ -126,6 +197,7 @@ class CudaReplayExecutor(Executor):
             self._expected.append(ref)
         self.ctx.stream.synchronize()
         self.restore_outputs()
+        exe.close()
 
     # -- compilation -------------------------------------------------------------------
     def _key(self, config: Configuration) -> tuple:
@@ -192,6 +264,7 @@ class CudaReplayExecutor(Executor):
         except (CompileError, EvalError):
             return Measurement(STATUS_COMPILE_FAILED, stage_timings=stages)
         stages["compile_wait"] = time.perf_counter() - t0
+        exe = None
         try:
             t0 = time.perf_counter()
             exe = CudaExecutable(req, image, self.ctx)
@@ -212,13 +285,20 @@ class CudaReplayExecutor(Executor):
             samples = exe.time_launches(geom, self.args, self.warmup, self.repetitions, flush=flush)
             if self.verify:
                 self.restore_outputs()
-            exe.close()
         except (LaunchError, KlbError, EvalError, DefinitionError) as err:
             code = getattr(err, "code", None)
             text = str(err)
             if code in _STICKY or any(f"[klb {c}]" in text for c in _STICKY):
                 self.broken = text
             return Measurement(STATUS_LAUNCH_FAILED, stage_timings=stages)
+        finally:
+            # every exit (invalid geometry, failed verification, launch error)
+            # unloads the module; a poisoned context cannot unload, so skip it
+            if exe is not None and not self.broken:
+                try:
+                    exe.close()
+                except (KlbError, LaunchError):
+                    pass
         objective = statistics.median(samples)
         stages["launch"] = objective
         stages["launch_min"] = min(samples)

@@ -29,14 +29,13 @@ __all__ = ["IsolatedReplayExecutor"]
 
 
 def _worker(conn, spec: dict, kwargs: dict) -> None:
-    from ..capture import read_capture
     from .device import open_device
     from .executor import CudaReplayExecutor
 
     ctx = open_device(int(spec.get("device", 0)))
     prob = None
     if "capture" in spec:
-        ex = CudaReplayExecutor(read_capture(spec["capture"]), ctx, **kwargs)
+        ex = CudaReplayExecutor.from_file(spec["capture"], ctx, **kwargs)
     else:
         from ..stencils.layout import GridLayout
         from ..stencils.problem import StencilProblem

@@ -58,7 +58,7 @@ HALO_REACH = {
 def kernel_reach(kernel: str) -> tuple[int, int]:
     """(max down, max up) over the kernel's exchanged fields."""
     reach = HALO_REACH[kernel].values()
-    return max(d for d, _ in reach), max(u for _, u in reach)
+    return max((d for d, _ in reach), default=0), max((u for _, u in reach), default=0)
 
 
 @dataclass(frozen=True)

@@ -26,6 +26,52 @@ def oracle_outputs(kernel: str, layout: GridLayout, dxi=1.0, dyi=1.0, k_range=No
     """Oracle result for the full interior (or local planes ``k_range``)."""
     f = host_fields(layout, KERNEL_FIELDS[kernel])
     prof = make_profiles(layout.kcells, layout.kgc).as_dtype(layout.dtype)
+    res = _oracle_compute(kernel, f, prof, layout, dxi, dyi)
+    if k_range is not None:
+        kb, ke = k_range
+        for name, arr in res.items():
+            orig = f[name].astype(np.float64)
+            arr[:kb] = orig[:kb]
+            arr[ke:] = orig[ke:]
+    return res, f
+
+
+def oracle_window(kernel: str, layout: GridLayout, kb: int, ke: int, k_offset: int = 0,
+                  kcells_global: int | None = None, dxi=1.0, dyi=1.0):
+    """Oracle outputs on local planes ``[kb, ke)`` of a grid ``layout`` whose
+    local plane 0 is global ghost-padded plane ``k_offset`` (a z-slab; 0 for
+    a whole grid) — only planes ``kb - kgc .. ke + kgc`` are generated, so the
+    check is bounded however large the grid.  Returns ``{output: (ke-kb,
+    jtot, itot) float64}`` (interior i/j)."""
+    g = layout.kgc
+    sub = GridLayout(layout.itot, layout.jtot, ke - kb, layout.precision, layout.igc, layout.jgc, g)
+    f = host_fields(sub, KERNEL_FIELDS[kernel], k_offset=k_offset + kb - g)
+    kcg = kcells_global if kcells_global is not None else layout.kcells
+    prof = make_profiles(kcg, g).window(k_offset + kb - g, sub.kcells).as_dtype(layout.dtype)
+    res = _oracle_compute(kernel, f, prof, sub, dxi, dyi)
+    return {n: sub.interior(a) for n, a in res.items()}
+
+
+def download_planes(prob: StencilProblem, name: str, kb: int, ke: int) -> np.ndarray:
+    """Interior i/j of local planes ``[kb, ke)`` of a device field, (ke-kb, jtot, itot)."""
+    lay = prob.layout
+    e = lay.elem_bytes
+    raw = prob.fields[name].download((ke - kb) * lay.kk * e, (lay.lead + kb * lay.kk) * e)
+    arr = np.frombuffer(raw, dtype=lay.dtype).reshape(ke - kb, lay.jcells, lay.jj)
+    return arr[:, lay.jstart:lay.jend, lay.istart:lay.iend]
+
+
+def window_error(prob: StencilProblem, kernel: str, kb: int, ke: int) -> dict:
+    """max|gpu - ref| / max|ref| per output over local planes [kb, ke)."""
+    ref = oracle_window(kernel, prob.layout, kb, ke, prob.k_offset, prob.kcells_global, prob.dxi, prob.dyi)
+    out = {}
+    for name, r in ref.items():
+        got = download_planes(prob, name, kb, ke).astype(np.float64)
+        out[name] = float(np.max(np.abs(got - r)) / np.max(np.abs(r)))
+    return out
+
+
+def _oracle_compute(kernel, f, prof, layout, dxi, dyi):
     g = (layout.igc, layout.jgc, layout.kgc)
     if kernel == "advec_u":
         res = {"ut": stencil_oracle.advec_u(f["ut"], f["u"], f["v"], f["w"], prof.rhoref, prof.rhorefh, prof.dzi, dxi,
@@ -57,13 +103,7 @@ def oracle_outputs(kernel: str, layout: GridLayout, dxi=1.0, dyi=1.0, k_range=No
         ut, vt, wt = stencil_oracle.diff_uvw(f["ut"], f["vt"], f["wt"], f["evisc"], f["u"], f["v"], f["w"], prof.dzi,
                                              prof.dzhi, prof.rhoref, prof.rhorefh, dxi, dyi, ghost=g)
         res = {"ut": ut, "vt": vt, "wt": wt}
-    if k_range is not None:
-        kb, ke = k_range
-        for name, arr in res.items():
-            orig = f[name].astype(np.float64)
-            arr[:kb] = orig[:kb]
-            arr[ke:] = orig[ke:]
-    return res, f
+    return res
 
 
 def rel_error(got: np.ndarray, ref: np.ndarray, layout: GridLayout) -> float:

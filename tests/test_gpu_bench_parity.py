@@ -1,0 +1,126 @@
+"""Oracle parity of the kernels the benchmark times, at the shapes it times them.
+
+Every launch goes through the application path the bench uses —
+``WisdomKernel`` over the committed ``wisdom/`` (select -> NVRTC -> load ->
+launch) — and is compared with the float64 oracle (``oracle/``, SURVEY
+Appendix A; parity UNPINNED against upstream MicroHH) on
+the same synthetic inputs.  Grids too large for a whole-grid oracle are
+checked on three 8-plane windows (bottom, middle, top): the oracle generates
+only the window's planes plus their ghost reach (``oracle_window``), so the
+host cost is bounded whatever the grid.
+
+Bar (BASELINE.json north_star): max|gpu - ref| / max|ref| <= 1e-5 (fp32),
+<= 1e-12 (fp64) per output array.
+
+Cases = BASELINE configs 1-4 (+ the north-star 512^3 fp32 pair and the fused
+RK3 kernel), and config 4's N = 2/4/8 z-slab ranks: the 1024^2 x {511, 254,
+126}-plane interior sub-ranges and single-plane boundary sub-ranges, each
+selected from wisdom for its own shape, exactly as ``bench.py --gpus N``
+launches them on every rank.
+"""
+
+from __future__ import annotations
+
+import json
+import os
+from pathlib import Path
+
+import pytest
+
+from stencil_helpers import TOL, window_error
+
+pytestmark = pytest.mark.gpu
+
+ROOT = Path(__file__).resolve().parent.parent
+WISDOM = ROOT / "wisdom"
+RESULTS = os.environ.get("KL_PARITY_LOG")  # optional JSON-lines record of every case
+
+CASES = [
+    # (tag, kernel, precision, grid, match kind the committed wisdom must give)
+    ("config 1", "diff_uvw", "fp64", (64, 64, 64), "exact"),
+    ("config 2", "advec_u", "fp32", (256, 256, 256), "exact"),
+    ("config 3", "advec_u", "fp64", (512, 512, 512), "exact"),
+    ("config 3", "diff_uvw", "fp64", (512, 512, 512), "exact"),
+    ("config 4", "diff_uvw", "fp32", (1024, 1024, 1024), "exact"),
+    ("north_star", "advec_u", "fp32", (512, 512, 512), "exact"),
+    ("north_star", "diff_uvw", "fp32", (512, 512, 512), "exact"),
+    ("§8f fusion", "diff_uvw_rk3", "fp32", (512, 512, 512), "exact"),
+    ("§8f fusion", "diff_uvw_rk3", "fp64", (512, 512, 512), "exact"),
+]
+
+
+def _windows(lay, n=8):
+    if lay.ktot <= 64:
+        return [(lay.kstart, lay.kend)]
+    mid = lay.kstart + lay.ktot // 2
+    return [(lay.kstart, lay.kstart + n), (mid - n // 2, mid + n // 2), (lay.kend - n, lay.kend)]
+
+
+def _record(entry: dict) -> None:
+    print(json.dumps(entry))
+    if RESULTS:
+        with open(RESULTS, "a", encoding="utf-8") as fh:
+            fh.write(json.dumps(entry) + "\n")
+
+
+@pytest.fixture(scope="module")
+def compiler(gpu_ctx):
+    from paper_2303_12374_b200.cuda import NvrtcCompiler
+
+    return NvrtcCompiler(gpu_ctx)
+
+
+@pytest.mark.parametrize("tag,kernel,precision,grid,kind", CASES,
+                         ids=[f"{k}_{p}_{g[0]}x{g[1]}x{g[2]}" for _, k, p, g, _ in CASES])
+def test_wisdom_selected_kernel_matches_oracle(gpu_ctx, compiler, tag, kernel, precision, grid, kind):
+    from paper_2303_12374_b200.capture import CapturePolicy
+    from paper_2303_12374_b200.dispatch import WisdomKernel
+    from paper_2303_12374_b200.stencils.layout import GridLayout
+    from paper_2303_12374_b200.stencils.problem import StencilProblem
+
+    lay = GridLayout(*grid, precision)
+    prob = StencilProblem(kernel, lay, gpu_ctx)
+    try:
+        wk = WisdomKernel(prob.definition, compiler, wisdom_dir=WISDOM, capture_policy=CapturePolicy())
+        report = wk.launch(gpu_ctx.ident, prob.args())
+        gpu_ctx.synchronize()
+        errors = {f"{kb}:{ke}": window_error(prob, kernel, kb, ke) for kb, ke in _windows(lay)}
+    finally:
+        prob.close()
+    worst = max(e for w in errors.values() for e in w.values())
+    _record({"case": tag, "kernel": kernel, "precision": precision, "grid": list(grid),
+             "match_kind": report.match_kind, "config": report.configuration, "worst_rel_err": worst,
+             "tolerance": TOL[precision], "windows": errors})
+    assert report.match_kind == kind, report.match_kind
+    assert worst <= TOL[precision], errors
+
+
+@pytest.mark.parametrize("nranks", [2, 4, 8])
+def test_slab_rank_subranges_match_oracle(gpu_ctx, compiler, nranks):
+    """Config 4 at N ranks: rank 1's slab (interior sub-range + its boundary
+    planes, each wisdom-selected for its own shape) as SlabDriver launches
+    them.  The slab's ghost planes hold the neighbours' planes (the device
+    generator indexes by global plane — what the halo exchange maintains), so
+    the result must equal the whole-grid oracle on the rank's planes."""
+    from paper_2303_12374_b200.slab import SlabDriver
+
+    drv = SlabDriver("diff_uvw", "fp32", (1024, 1024, 1024), gpu_ctx, rank=1, nranks=nranks, exchanger=None,
+                     compiler=compiler, wisdom_dir=WISDOM)
+    try:
+        chosen = drv.resolve()
+        drv.step()
+        gpu_ctx.synchronize()
+        lay = drv.layout
+        shapes = {name: ke - kb for name, (kb, ke) in drv.ranges.items()}
+        windows = [(lay.kstart, lay.kstart + 4), (lay.kstart + lay.ktot // 2 - 2, lay.kstart + lay.ktot // 2 + 2),
+                   (lay.kend - 4, lay.kend)]
+        errors = {f"{kb}:{ke}": window_error(drv.problem, "diff_uvw", kb, ke) for kb, ke in windows}
+    finally:
+        drv.close()
+    worst = max(e for w in errors.values() for e in w.values())
+    _record({"case": f"config 4 slab rank 1 of {nranks}", "subrange_planes": shapes,
+             "selection": {n: {"match_kind": k, "config": c} for n, (c, k) in chosen.items()},
+             "worst_rel_err": worst, "windows": errors})
+    interior = {2: 511, 4: 254, 8: 126}[nranks]
+    assert shapes["interior"] == interior and shapes.get("lower", shapes.get("upper")) == 1
+    assert worst <= TOL["fp32"], errors

@@ -127,3 +127,26 @@ def test_c_restatement_matches_numpy_oracle(kernel):
                       prof.rhoref, prof.rhorefh, 1.0, 1.0, threads=2)
     for name in ref:
         assert np.max(np.abs(got[name] - ref[name])) <= 1e-12 * np.max(np.abs(ref[name]))
+
+
+@pytest.mark.parametrize("kernel", ["advec_u", "diff_uvw", "diff_uvw_rk3", "evisc_smag"])
+def test_oracle_window_equals_whole_grid(kernel):
+    """The bounded-window oracle the large-shape GPU parity tests use
+    (tests/test_gpu_bench_parity.py) equals the whole-grid oracle, for a grid
+    and for a z-slab of it (global plane offset)."""
+    import sys
+    from pathlib import Path
+
+    sys.path.insert(0, str(Path(__file__).resolve().parent))
+    from stencil_helpers import oracle_outputs, oracle_window
+    from paper_2303_12374_b200.stencils.layout import GridLayout
+
+    lay = GridLayout(20, 12, 16, "fp32")
+    full, _ = oracle_outputs(kernel, lay)
+    win = oracle_window(kernel, lay, 5, 11)
+    for name, arr in win.items():
+        assert np.array_equal(arr, lay.interior(full[name])[2:8])
+    slab = GridLayout(20, 12, 8, "fp32")  # global interior planes 4..12 = padded offset 4
+    win = oracle_window(kernel, slab, 3, 11, k_offset=4, kcells_global=lay.kcells)
+    for name, arr in win.items():
+        assert np.array_equal(arr, lay.interior(full[name])[4:12])
