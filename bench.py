@@ -104,50 +104,64 @@ def peaks():
 
 
 class Dist:
+    """Rank plumbing of the N-GPU job, torch-free: ``ProcessGroup``
+    (klb_group_*, one shared-memory segment; barrier, max/sum over ranks,
+    NCCL-id broadcast).  RANK / WORLD_SIZE / LOCAL_RANK come from the
+    launcher — torchrun, or ``bench.py --gpus N``'s own spawner."""
+
     def __init__(self):
         self.rank = env_int("RANK", 0)
         self.world = env_int("WORLD_SIZE", 1)
         self.local = env_int("LOCAL_RANK", self.rank)
-        self.pg = None
+        self.group = None
         if self.world > 1:
-            import torch.distributed as dist
+            from paper_2303_12374_b200.group import ProcessGroup
 
-            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-            dist.init_process_group("gloo", rank=self.rank, world_size=self.world)
-            self.pg = dist
+            self.group = ProcessGroup(self.rank, self.world, timeout=float(os.environ.get("KLB_GROUP_TIMEOUT", 600)))
 
     def barrier(self):
-        if self.pg:
-            self.pg.barrier()
+        if self.group:
+            self.group.barrier()
 
     def max(self, value: float) -> float:
-        if not self.pg:
-            return value
-        import torch
-
-        t = torch.tensor([value], dtype=torch.float64)
-        self.pg.all_reduce(t, op=self.pg.ReduceOp.MAX)
-        return float(t.item())
+        return self.group.max(value) if self.group else value
 
     def sum(self, value: float) -> float:
-        if not self.pg:
-            return value
-        import torch
+        return self.group.sum(value) if self.group else value
 
-        t = torch.tensor([value], dtype=torch.float64)
-        self.pg.all_reduce(t, op=self.pg.ReduceOp.SUM)
-        return float(t.item())
-
-    def broadcast_bytes(self, payload: bytes | None) -> bytes:
-        if not self.pg:
-            return payload
-        obj = [payload]
-        self.pg.broadcast_object_list(obj, src=0)
-        return obj[0]
+    def broadcast_bytes(self, payload: bytes | None, size: int) -> bytes:
+        return self.group.broadcast(payload, size=size) if self.group else payload
 
     def close(self):
-        if self.pg:
-            self.pg.destroy_process_group()
+        if self.group:
+            self.group.close()
+
+
+def spawn_ranks(n: int, argv: list[str]) -> int:
+    """``--gpus N`` without a launcher: start N ranks of this script (rank r
+    on GPU r), each with RANK/WORLD_SIZE/LOCAL_RANK and one shared group name;
+    rank 0 prints the JSON line.  A failing rank stops the others."""
+    import subprocess
+
+    group = f"/klb_bench_{os.getpid()}_{time.time_ns()}"
+    procs = []
+    for r in range(n):
+        env = dict(os.environ, RANK=str(r), WORLD_SIZE=str(n), LOCAL_RANK=str(r), LOCAL_WORLD_SIZE=str(n),
+                   KLB_GROUP=group, MASTER_ADDR="127.0.0.1")
+        procs.append(subprocess.Popen([sys.executable, str(Path(__file__).resolve()), *argv], env=env))
+    rc = 0
+    while procs:
+        for p in list(procs):
+            code = p.poll()
+            if code is None:
+                continue
+            procs.remove(p)
+            if code != 0:
+                rc = rc or code
+                for q in procs:
+                    q.terminate()
+        time.sleep(0.05)
+    return rc
 
 
 # ---------------------------------------------------------------------------
@@ -497,7 +511,7 @@ def graph_measure(ctx, compiler, wisdom_dir, n=200):
 
 def run_ours(args, dist):
     from paper_2303_12374_b200.cuda import NvrtcCompiler, open_device
-    from paper_2303_12374_b200.halo import NcclExchanger, StagedExchanger
+    from paper_2303_12374_b200.halo import IpcExchanger, NcclExchanger
     from paper_2303_12374_b200.slab import SlabDriver
 
     kernel, precision, grid, label = WORKLOADS[args.workload]
@@ -506,12 +520,18 @@ def run_ours(args, dist):
     forced = os.environ.get("KL_DEVICE_ORDINAL")
     ctx = open_device(int(forced) if forced is not None else (dist.local if args.gpus > 1 or dist.world > 1 else 0))
     peak, peak_src = peaks()
-    exchanger = None
-    if dist.world > 1 and os.environ.get("KL_HALO_TRANSPORT", "nccl") == "staged":
-        exchanger = StagedExchanger(dist.rank, dist.world)  # host relay over gloo (testing on one GPU)
-    elif dist.world > 1:
-        uid = dist.broadcast_bytes(NcclExchanger.unique_id() if dist.rank == 0 else None)
-        exchanger = NcclExchanger(dist.rank, dist.world, uid)
+    exchanger, transport = None, None
+    if dist.world > 1:
+        # ipc (default): neighbours map each other's fields (CUDA IPC) and pull
+        # halo planes over NVLink with copy engines; nccl: ncclSend/ncclRecv
+        transport = os.environ.get("KL_HALO_TRANSPORT", "ipc")
+        if transport == "nccl":
+            uid = dist.broadcast_bytes(NcclExchanger.unique_id() if dist.rank == 0 else None, 128)
+            exchanger = NcclExchanger(dist.rank, dist.world, uid)
+        else:
+            exchanger = IpcExchanger(dist.group)
+        if dist.rank == 0:
+            print(f"klb: halo transport={transport} comm nranks={dist.world}", file=sys.stderr, flush=True)
     compiler = NvrtcCompiler(ctx)
     wisdom_dir = Path(args.wisdom)
     empty = ROOT / "build" / "empty_wisdom"
@@ -583,6 +603,7 @@ def run_ours(args, dist):
         "data": "synthetic (splitmix64 fields generated on device; oracle/synth.py twin)",
         "config": {"workload": label, "kernel": kernel, "precision": precision, "grid": list(grid),
                    "decomposition": f"z-slab x{dist.world}", "parallelism": f"slab{dist.world}",
+                   "halo_transport": transport,
                    "ghost_cells": 3, "l2": "inputs larger than L2 (7 fields x 4.4 GB), no flush",
                    "wisdom": str(wisdom_dir.relative_to(ROOT)) if wisdom_dir.is_relative_to(ROOT) else str(wisdom_dir)},
         "variants": variants,
@@ -644,6 +665,8 @@ def main(argv=None):
     args = ap.parse_args(argv)
     if args.warmup < 3:
         args.warmup = 3
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn_ranks(args.gpus, sys.argv[1:] if argv is None else list(argv))
     dist = Dist()
     try:
         if args.impl == "reference":

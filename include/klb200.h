@@ -17,7 +17,8 @@
  *   klb_module_global / klb_tensor_map_encode_3d -> part of ExecutableHandle.launch (TMA staging)
  *   klb_synth_field                -> synthetic capture payloads   capture.py:75-98 (BufferArg.data)
  *   klb_crc32_device               -> zlib.crc32 of payloads       capture.py:228-256 (device capture)
- *   klb_halo_* (NCCL)              -> no reference counterpart (multi-GPU z-slabs)
+ *   klb_halo_* (NCCL / CUDA IPC)   -> no reference counterpart (multi-GPU z-slabs)
+ *   klb_group_*                    -> no reference counterpart (single-node rank rendezvous)
  *
  * Conventions: every function returns 0 on success or a nonzero code
  * (a CUresult, nvrtcResult + 10000, ncclResult_t + 20000, or KLB_E_* below);
@@ -43,6 +44,7 @@ extern "C" {
 #define KLB_E_COMPILE 30003   /* NVRTC compile failed (log returned) */
 #define KLB_E_NOT_INIT 30004  /* klb_init not called on this process */
 #define KLB_E_NO_DRIVER 30005 /* no usable CUDA driver (libcuda) on this host */
+#define KLB_E_TIMEOUT 30006   /* a process-group peer did not arrive in time */
 
 typedef void* klb_stream;
 typedef void* klb_event;
@@ -220,6 +222,49 @@ int klb_nccl_comm_destroy(klb_comm comm);
 int klb_halo_exchange_z(klb_comm comm, klb_stream stream, int nfields, const uint64_t* fields,
                         int elem_bytes, long long kk, int kstart, int kend,
                         int n_down, int n_up, int rank_below, int rank_above);
+
+/* ---- single-node process group (rendezvous without torch or sockets) ----
+ * One POSIX shared-memory segment per job (`name` = "/identifier", the same
+ * on every rank, unique per job); process-shared atomics implement a barrier
+ * and a fixed-slot allgather.  Every call blocks at most `timeout_s` seconds
+ * waiting for peers (KLB_E_TIMEOUT), so a dead peer cannot hang the job.
+ * Replaces the torch.distributed/gloo plumbing of the multi-rank bench
+ * (VERDICT r1 "N>1 harness depends on torch").  No reference counterpart. */
+#define KLB_GROUP_SLOT 4096
+#define KLB_GROUP_MAX_RANKS 64
+typedef void* klb_group;
+int klb_group_open(const char* name, int rank, int nranks, double timeout_s, klb_group* group);
+int klb_group_barrier(klb_group group);
+/* Every rank contributes `bytes` (<= KLB_GROUP_SLOT) from `in`; `out`
+ * receives nranks * bytes, rank r's contribution at offset r * bytes. */
+int klb_group_allgather(klb_group group, const void* in, size_t bytes, void* out);
+int klb_group_close(klb_group group);
+
+/* ---- CUDA IPC: the peer-memory (P2P) halo transport ----------------------
+ * Neighbour ranks map each other's field allocations (cuIpcOpenMemHandle
+ * with lazy peer access: NVLink loads/stores between GPUs, or another
+ * process's allocation on the same GPU) and order their copies with
+ * interprocess events.  SURVEY §8e "P2P cuMemcpyPeerAsync" alternative to
+ * NCCL send/recv; no reference counterpart. */
+#define KLB_IPC_HANDLE_BYTES 64
+/* Handle of the allocation containing `dptr`; *offset = dptr - allocation base. */
+int klb_ipc_mem_handle(uint64_t dptr, unsigned char handle_out[KLB_IPC_HANDLE_BYTES], uint64_t* offset);
+/* Map a peer's allocation; *dptr is its base in this process. */
+int klb_ipc_mem_open(const unsigned char handle[KLB_IPC_HANDLE_BYTES], uint64_t* dptr);
+int klb_ipc_mem_close(uint64_t dptr);
+/* An interprocess event (no timing) and its handle; destroy with klb_event_destroy. */
+int klb_ipc_event_create(klb_event* event, unsigned char handle_out[KLB_IPC_HANDLE_BYTES]);
+int klb_ipc_event_open(const unsigned char handle[KLB_IPC_HANDLE_BYTES], klb_event* event);
+/* Pull halo planes from the neighbours' (mapped) fields into this rank's
+ * ghost planes, on `stream` (copy engines; the SMs stay with the interior
+ * launch).  Same plan as klb_halo_exchange_z, receiver side only:
+ *   planes [kstart-n_up, kstart)  <- below's [below_kend-n_up, below_kend)
+ *   planes [kend, kend+n_down)    <- above's [above_kstart, above_kstart+n_down)
+ * `below_fields` / `above_fields` NULL = no neighbour on that side; all
+ * pointers are element (0,0,0) of the respective slab. */
+int klb_halo_pull_z(klb_stream stream, int nfields, const uint64_t* fields, const uint64_t* below_fields,
+                    const uint64_t* above_fields, int elem_bytes, long long kk, int kstart, int kend,
+                    int n_down, int n_up, int below_kend, int above_kstart);
 
 #ifdef __cplusplus
 }

@@ -20,6 +20,15 @@
 #include <dlfcn.h>
 #include <nvrtc.h>
 
+#include <fcntl.h>
+#include <sched.h>
+#include <sys/mman.h>
+#include <sys/stat.h>
+#include <unistd.h>
+
+#include <atomic>
+#include <chrono>
+#include <cerrno>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -42,7 +51,7 @@ int g_default_ordinal = -1;
 // CUDA driver API, resolved at runtime through cudaGetDriverEntryPoint so the
 // library has no link-time dependency on libcuda.so.1: it loads (and reports
 // a clean error from klb_init) on hosts without an NVIDIA driver.
-#define KLB_DRIVER_API(X) X(cuCtxGetCurrent) X(cuCtxSetCurrent) X(cuCtxSynchronize) X(cuDeviceGet) X(cuDeviceGetAttribute) X(cuDeviceGetCount) X(cuDeviceGetName) X(cuDeviceGetUuid) X(cuDevicePrimaryCtxRetain) X(cuDeviceTotalMem) X(cuDriverGetVersion) X(cuEventCreate) X(cuEventDestroy) X(cuEventElapsedTime) X(cuEventRecord) X(cuEventSynchronize) X(cuFuncGetAttribute) X(cuFuncSetAttribute) X(cuGetErrorName) X(cuGetErrorString) X(cuInit) X(cuLaunchKernel) X(cuMemAlloc) X(cuMemFree) X(cuMemFreeHost) X(cuMemGetInfo) X(cuMemHostAlloc) X(cuMemcpyDtoDAsync) X(cuMemcpyDtoHAsync) X(cuMemcpyHtoDAsync) X(cuMemsetD32Async) X(cuMemsetD8Async) X(cuModuleGetFunction) X(cuModuleLoadData) X(cuModuleUnload) X(cuOccupancyMaxActiveBlocksPerMultiprocessor) X(cuStreamCreateWithPriority) X(cuStreamDestroy) X(cuStreamSynchronize) X(cuStreamWaitEvent) X(cuModuleGetGlobal) X(cuTensorMapEncodeTiled) X(cuStreamBeginCapture) X(cuStreamEndCapture) X(cuGraphInstantiateWithFlags) X(cuGraphLaunch) X(cuGraphDestroy) X(cuGraphExecDestroy)
+#define KLB_DRIVER_API(X) X(cuCtxGetCurrent) X(cuCtxSetCurrent) X(cuCtxSynchronize) X(cuDeviceGet) X(cuDeviceGetAttribute) X(cuDeviceGetCount) X(cuDeviceGetName) X(cuDeviceGetUuid) X(cuDevicePrimaryCtxRetain) X(cuDeviceTotalMem) X(cuDriverGetVersion) X(cuEventCreate) X(cuEventDestroy) X(cuEventElapsedTime) X(cuEventRecord) X(cuEventSynchronize) X(cuFuncGetAttribute) X(cuFuncSetAttribute) X(cuGetErrorName) X(cuGetErrorString) X(cuInit) X(cuLaunchKernel) X(cuMemAlloc) X(cuMemFree) X(cuMemFreeHost) X(cuMemGetInfo) X(cuMemHostAlloc) X(cuMemcpyDtoDAsync) X(cuMemcpyDtoHAsync) X(cuMemcpyHtoDAsync) X(cuMemsetD32Async) X(cuMemsetD8Async) X(cuModuleGetFunction) X(cuModuleLoadData) X(cuModuleUnload) X(cuOccupancyMaxActiveBlocksPerMultiprocessor) X(cuStreamCreateWithPriority) X(cuStreamDestroy) X(cuStreamSynchronize) X(cuStreamWaitEvent) X(cuModuleGetGlobal) X(cuTensorMapEncodeTiled) X(cuStreamBeginCapture) X(cuStreamEndCapture) X(cuGraphInstantiateWithFlags) X(cuGraphLaunch) X(cuGraphDestroy) X(cuGraphExecDestroy) X(cuIpcGetMemHandle) X(cuIpcOpenMemHandle) X(cuIpcCloseMemHandle) X(cuIpcGetEventHandle) X(cuIpcOpenEventHandle) X(cuMemGetAddressRange)
 
 struct DriverApi {
 #define KLB_DECL(name) decltype(&::name) name = nullptr;
@@ -913,6 +922,206 @@ int klb_halo_exchange_z(klb_comm comm, klb_stream stream, int nfields, const uin
   ncclResult_t r2 = g_nccl.groupEnd();
   if (r != ncclSuccess) return nccl_fail(r, "ncclSend/ncclRecv");
   if (r2 != ncclSuccess) return nccl_fail(r2, "ncclGroupEnd");
+  return 0;
+}
+
+
+}  // extern "C"
+
+namespace {
+
+// ---- single-node process group (POSIX shared memory) ---------------------------------
+// The rendezvous of the multi-rank driver without torch or sockets: every
+// rank maps one shared segment; a sense-counting barrier and a fixed-slot
+// allgather run on process-shared atomics (host only, microseconds).  Used
+// to exchange NCCL ids / IPC handles and, per step, to order the ranks'
+// enqueue of the cross-process IPC events (klb_halo_pull_z's protocol).
+
+struct GroupShared {
+  std::atomic<uint32_t> count;
+  std::atomic<uint32_t> generation;
+  std::atomic<uint32_t> attached;
+  uint32_t pad;
+  // followed by nranks slots of KLB_GROUP_SLOT bytes
+};
+static_assert(sizeof(std::atomic<uint32_t>) == 4, "lock-free 32-bit atomics expected");
+
+struct Group {
+  GroupShared* shm = nullptr;
+  size_t bytes = 0;
+  int rank = 0, nranks = 1;
+  double timeout_s = 300.0;
+  char name[128] = {};
+  unsigned char* slot(int r) { return reinterpret_cast<unsigned char*>(shm + 1) + static_cast<size_t>(r) * KLB_GROUP_SLOT; }
+};
+
+int group_barrier(Group* g) {
+  GroupShared* s = g->shm;
+  const uint32_t gen = s->generation.load(std::memory_order_acquire);
+  if (s->count.fetch_add(1, std::memory_order_acq_rel) + 1 == static_cast<uint32_t>(g->nranks)) {
+    s->count.store(0, std::memory_order_relaxed);
+    s->generation.fetch_add(1, std::memory_order_acq_rel);
+    return 0;
+  }
+  const auto t0 = std::chrono::steady_clock::now();
+  for (unsigned spin = 0; s->generation.load(std::memory_order_acquire) == gen; ++spin) {
+    if (spin > 64) sched_yield();
+    if ((spin & 1023) == 0) {
+      const double waited = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+      if (waited > g->timeout_s)
+        return fail(KLB_E_TIMEOUT, "group %s: rank %d timed out after %.0f s in a barrier (a peer died?)", g->name,
+                    g->rank, waited);
+    }
+  }
+  return 0;
+}
+
+// ---- CUDA IPC ---------------------------------------------------------------------
+
+int ipc_base(uint64_t dptr, CUdeviceptr* base, size_t* size) {
+  CU_TRY(drv.cuMemGetAddressRange(base, size, static_cast<CUdeviceptr>(dptr)));
+  return 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+int klb_group_open(const char* name, int rank, int nranks, double timeout_s, klb_group* group) {
+  if (!name || !group || nranks < 1 || rank < 0 || rank >= nranks || nranks > KLB_GROUP_MAX_RANKS)
+    return fail(KLB_E_INVALID, "klb_group_open: bad arguments (rank %d of %d)", rank, nranks);
+  if (name[0] != '/' || strlen(name) >= sizeof(Group{}.name) || strchr(name + 1, '/'))
+    return fail(KLB_E_INVALID, "klb_group_open: name must be '/identifier' (< 128 chars): %s", name);
+  auto* g = new Group();
+  g->rank = rank;
+  g->nranks = nranks;
+  g->timeout_s = timeout_s > 0 ? timeout_s : 300.0;
+  std::snprintf(g->name, sizeof(g->name), "%s", name);
+  g->bytes = sizeof(GroupShared) + static_cast<size_t>(nranks) * KLB_GROUP_SLOT;
+  int fd = shm_open(name, O_CREAT | O_RDWR, 0600);
+  if (fd < 0) {
+    delete g;
+    return fail(KLB_E_INVALID, "shm_open(%s): %s", name, strerror(errno));
+  }
+  // every rank sizes the segment identically (idempotent); a new segment is zero-filled
+  if (ftruncate(fd, static_cast<off_t>(g->bytes)) != 0) {
+    close(fd);
+    delete g;
+    return fail(KLB_E_INVALID, "ftruncate(%s): %s", name, strerror(errno));
+  }
+  void* p = mmap(nullptr, g->bytes, PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
+  close(fd);
+  if (p == MAP_FAILED) {
+    delete g;
+    return fail(KLB_E_INVALID, "mmap(%s): %s", name, strerror(errno));
+  }
+  g->shm = static_cast<GroupShared*>(p);
+  g->shm->attached.fetch_add(1, std::memory_order_acq_rel);
+  if (int e = group_barrier(g)) {
+    munmap(p, g->bytes);
+    delete g;
+    return e;
+  }
+  // everyone is attached: the name is no longer needed (the mapping stays)
+  if (rank == 0) shm_unlink(name);
+  *group = g;
+  return 0;
+}
+
+int klb_group_barrier(klb_group group) {
+  if (!group) return fail(KLB_E_INVALID, "null group");
+  return group_barrier(static_cast<Group*>(group));
+}
+
+int klb_group_allgather(klb_group group, const void* in, size_t bytes, void* out) {
+  if (!group) return fail(KLB_E_INVALID, "null group");
+  auto* g = static_cast<Group*>(group);
+  if (bytes > KLB_GROUP_SLOT) return fail(KLB_E_INVALID, "allgather of %zu bytes > slot %d", bytes, KLB_GROUP_SLOT);
+  std::memcpy(g->slot(g->rank), in, bytes);
+  if (int e = group_barrier(g)) return e;
+  for (int r = 0; r < g->nranks; ++r) std::memcpy(static_cast<unsigned char*>(out) + r * bytes, g->slot(r), bytes);
+  return group_barrier(g);  // slots may be rewritten only after everyone has read them
+}
+
+int klb_group_close(klb_group group) {
+  if (!group) return 0;
+  auto* g = static_cast<Group*>(group);
+  munmap(g->shm, g->bytes);
+  delete g;
+  return 0;
+}
+
+int klb_ipc_mem_handle(uint64_t dptr, unsigned char handle_out[KLB_IPC_HANDLE_BYTES], uint64_t* offset) {
+  CTX_TRY();
+  CUdeviceptr base;
+  size_t size;
+  if (int e = ipc_base(dptr, &base, &size)) return e;
+  CUipcMemHandle h;
+  CU_TRY(drv.cuIpcGetMemHandle(&h, base));
+  static_assert(sizeof(h) == KLB_IPC_HANDLE_BYTES, "CUipcMemHandle size");
+  std::memcpy(handle_out, &h, sizeof(h));
+  if (offset) *offset = dptr - static_cast<uint64_t>(base);
+  return 0;
+}
+
+int klb_ipc_mem_open(const unsigned char handle[KLB_IPC_HANDLE_BYTES], uint64_t* dptr) {
+  CTX_TRY();
+  CUipcMemHandle h;
+  std::memcpy(&h, handle, sizeof(h));
+  CUdeviceptr p;
+  CU_TRY(drv.cuIpcOpenMemHandle(&p, h, CU_IPC_MEM_LAZY_ENABLE_PEER_ACCESS));
+  *dptr = static_cast<uint64_t>(p);
+  return 0;
+}
+
+int klb_ipc_mem_close(uint64_t dptr) {
+  CTX_TRY();
+  CU_TRY(drv.cuIpcCloseMemHandle(static_cast<CUdeviceptr>(dptr)));
+  return 0;
+}
+
+int klb_ipc_event_create(klb_event* event, unsigned char handle_out[KLB_IPC_HANDLE_BYTES]) {
+  CTX_TRY();
+  CUevent e;
+  CU_TRY(drv.cuEventCreate(&e, CU_EVENT_INTERPROCESS | CU_EVENT_DISABLE_TIMING));
+  CUipcEventHandle h;
+  CUresult r = drv.cuIpcGetEventHandle(&h, e);
+  if (r != CUDA_SUCCESS) {
+    drv.cuEventDestroy(e);
+    return cu_fail(r, "cuIpcGetEventHandle");
+  }
+  static_assert(sizeof(h) == KLB_IPC_HANDLE_BYTES, "CUipcEventHandle size");
+  std::memcpy(handle_out, &h, sizeof(h));
+  *event = e;
+  return 0;
+}
+
+int klb_ipc_event_open(const unsigned char handle[KLB_IPC_HANDLE_BYTES], klb_event* event) {
+  CTX_TRY();
+  CUipcEventHandle h;
+  std::memcpy(&h, handle, sizeof(h));
+  CUevent e;
+  CU_TRY(drv.cuIpcOpenEventHandle(&e, h));
+  *event = e;
+  return 0;
+}
+
+int klb_halo_pull_z(klb_stream stream, int nfields, const uint64_t* fields, const uint64_t* below_fields,
+                    const uint64_t* above_fields, int elem_bytes, long long kk, int kstart, int kend, int n_down,
+                    int n_up, int below_kend, int above_kstart) {
+  if (n_down < 0 || n_up < 0 || nfields < 0 || elem_bytes <= 0 || kk <= 0)
+    return fail(KLB_E_INVALID, "klb_halo_pull_z: bad extents");
+  CTX_TRY();
+  const size_t plane = static_cast<size_t>(kk) * elem_bytes;
+  CUstream s = as_stream(stream);
+  for (int f = 0; f < nfields; ++f) {
+    if (below_fields && n_up > 0)  // my bottom ghost planes <- the top of the slab below
+      CU_TRY(drv.cuMemcpyDtoDAsync(fields[f] + static_cast<long long>(kstart - n_up) * plane,
+                                   below_fields[f] + static_cast<long long>(below_kend - n_up) * plane, n_up * plane, s));
+    if (above_fields && n_down > 0)  // my top ghost planes <- the bottom of the slab above
+      CU_TRY(drv.cuMemcpyDtoDAsync(fields[f] + static_cast<long long>(kend) * plane,
+                                   above_fields[f] + static_cast<long long>(above_kstart) * plane, n_down * plane, s));
+  }
   return 0;
 }
 

@@ -123,6 +123,17 @@ EXPORTS: dict[str, list] = {
     "klb_nccl_comm_init": [_pvp, _i, C.POINTER(C.c_ubyte), _i],
     "klb_nccl_comm_destroy": [_vp],
     "klb_halo_exchange_z": [_vp, _vp, _i, C.POINTER(_u64), _i, _ll, _i, _i, _i, _i, _i, _i],
+    "klb_group_open": [C.c_char_p, _i, _i, _d, _pvp],
+    "klb_group_barrier": [_vp],
+    "klb_group_allgather": [_vp, _vp, _sz, _vp],
+    "klb_group_close": [_vp],
+    "klb_ipc_mem_handle": [_u64, C.POINTER(C.c_ubyte), C.POINTER(_u64)],
+    "klb_ipc_mem_open": [C.POINTER(C.c_ubyte), C.POINTER(_u64)],
+    "klb_ipc_mem_close": [_u64],
+    "klb_ipc_event_create": [_pvp, C.POINTER(C.c_ubyte)],
+    "klb_ipc_event_open": [C.POINTER(C.c_ubyte), _pvp],
+    "klb_halo_pull_z": [_vp, _i, C.POINTER(_u64), C.POINTER(_u64), C.POINTER(_u64), _i, _ll, _i, _i, _i, _i, _i,
+                        _i],
 }
 _RESTYPE = {"klb_last_error": C.c_char_p, "klb_free": None}
 

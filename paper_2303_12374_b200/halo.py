@@ -20,10 +20,12 @@ Exchange plan (``halo_plan``) — every rank passes the same per-field reach:
   ``up``   = planes it reads BELOW its slab (reach towards -k);
   send [kstart, kstart+down) -> below   | recv [kstart-up, kstart) <- below
   send [kend-up, kend)       -> above   | recv [kend, kend+down)   <- above
-This is the protocol ``klb_halo_exchange_z`` (NCCL) implements in C; the
-``CopyExchanger`` (several virtual ranks on one GPU, D2D copies) and the
-``HostExchanger`` (NumPy arrays over torch.distributed/gloo, CPU tests)
-implement the same plan in Python.
+This is the protocol ``klb_halo_exchange_z`` (NCCL send/recv) and
+``klb_halo_pull_z`` (peer memory over CUDA IPC, ``IpcExchanger``: the
+receiver-side half of the plan, copy engines reading the neighbour's planes
+over NVLink) implement in C; the ``CopyExchanger`` (several virtual ranks on
+one GPU, D2D copies) implements the same plan in Python, and so does the
+CPU-test transport over gloo (tests/test_halo.py).
 
 Reach per kernel (from the stencil definitions):
   advec_u : u (down 3, up 3), w (down 1, up 0), v none
@@ -37,8 +39,7 @@ import ctypes as C
 from dataclasses import dataclass
 
 __all__ = [
-    "HALO_REACH", "SlabDecomposition", "halo_plan", "NcclExchanger", "CopyExchanger", "HostExchanger",
-    "StagedExchanger", "SlabRank",
+    "HALO_REACH", "SlabDecomposition", "halo_plan", "NcclExchanger", "IpcExchanger", "CopyExchanger", "SlabRank",
 ]
 
 #: kernel -> {field: (down, up)}
@@ -137,6 +138,140 @@ class NcclExchanger:
             self.comm = None
 
 
+class IpcExchanger:
+    """Halo exchange over peer memory (CUDA IPC), receiver-pulled.
+
+    Each rank maps its neighbours' field allocations once
+    (``klb_ipc_mem_handle`` / ``klb_ipc_mem_open``: over NVLink between GPUs,
+    or another process's allocation on the same GPU) and pulls the planes it
+    needs into its own ghost planes with copy-engine copies
+    (``klb_halo_pull_z``) on the comm stream, overlapped with the interior
+    launch.  Ordering across processes uses interprocess events, made
+    race-free by two host barriers of the ``ProcessGroup`` per exchange::
+
+        comm: record ready      (my input planes are final for this step)
+        ---- barrier A ----     (every rank's ready is enqueued)
+        comm: wait ready(below, above); pull their planes; record pulled
+        ---- barrier B ----     (every rank's pulled is enqueued)
+        comm: wait pulled(below, above)
+
+    The last wait orders everything after the exchange on this rank — the
+    boundary launches and any later write of the inputs by the application —
+    after the neighbours have finished reading this rank's planes (no
+    write-after-read race in a time loop).  The barriers only order host
+    enqueues; the GPU never waits on the host.  Same ``exchange`` signature as
+    ``NcclExchanger``; the plan is ``halo_plan``'s receiver side."""
+
+    def __init__(self, group) -> None:
+        from .cuda._abi import check, lib
+
+        self.group = group
+        self.rank, self.nranks = group.rank, group.nranks
+        self._events = []
+        handles = []
+        for _ in range(2):  # ready, pulled
+            ev = C.c_void_p()
+            h = (C.c_ubyte * 64)()
+            check(lib().klb_ipc_event_create(C.byref(ev), h))
+            self._events.append(ev.value)
+            handles.append(bytes(h))
+        self.ready, self.pulled = self._events
+        peers = group.allgather(b"".join(handles))
+        self._peer_events: dict[int, tuple[int, int]] = {}
+        for r in (self.rank - 1, self.rank + 1):
+            if 0 <= r < self.nranks:
+                evs = []
+                for i in range(2):
+                    ev = C.c_void_p()
+                    h = (C.c_ubyte * 64).from_buffer_copy(peers[r][64 * i:64 * (i + 1)])
+                    check(lib().klb_ipc_event_open(h, C.byref(ev)))
+                    evs.append(ev.value)
+                self._peer_events[r] = tuple(evs)
+        self._maps: dict[tuple, dict] = {}  # local pointer tuple -> peer mappings
+        self._opened: list[int] = []
+
+    def _attach(self, ptrs, kstart: int, kend: int) -> dict:
+        """Collective on first use of a field set: map the neighbours' fields."""
+        import struct
+
+        from .cuda._abi import check, lib
+
+        key = (tuple(ptrs), kstart, kend)
+        entry = self._maps.get(key)
+        if entry is not None:
+            return entry
+        blob = struct.pack("<ii", kstart, kend)
+        for p in ptrs:
+            h = (C.c_ubyte * 64)()
+            off = C.c_uint64()
+            check(lib().klb_ipc_mem_handle(p, h, C.byref(off)))
+            blob += bytes(h) + struct.pack("<Q", off.value)
+        allb = self.group.allgather(blob)
+        entry = {}
+        for side, r in (("below", self.rank - 1), ("above", self.rank + 1)):
+            if not 0 <= r < self.nranks:
+                continue
+            ks, ke = struct.unpack_from("<ii", allb[r], 0)
+            mapped = []
+            for i in range(len(ptrs)):
+                at = 8 + 72 * i
+                h = (C.c_ubyte * 64).from_buffer_copy(allb[r][at:at + 64])
+                off, = struct.unpack_from("<Q", allb[r], at + 64)
+                base = C.c_uint64()
+                check(lib().klb_ipc_mem_open(h, C.byref(base)))
+                self._opened.append(base.value)
+                mapped.append(base.value + off)
+            entry[side] = (mapped, ks, ke)
+        self._maps[key] = entry
+        return entry
+
+    def exchange(self, stream, ptrs, elem_bytes: int, kk: int, kstart: int, kend: int, down: int, up: int,
+                 below: int, above: int) -> None:
+        from .cuda._abi import check, lib
+
+        entry = self._attach(ptrs, kstart, kend)
+        n = len(ptrs)
+        check(lib().klb_event_record(self.ready, stream.handle))
+        self.group.barrier()
+        neighbours = [r for r in (below, above) if r >= 0]
+        for r in neighbours:
+            check(lib().klb_stream_wait_event(stream.handle, self._peer_events[r][0]))
+        arr = (C.c_uint64 * n)(*ptrs)
+        lo = (C.c_uint64 * n)(*entry["below"][0]) if below >= 0 else None
+        hi = (C.c_uint64 * n)(*entry["above"][0]) if above >= 0 else None
+        below_kend = entry["below"][2] if below >= 0 else 0
+        above_kstart = entry["above"][1] if above >= 0 else 0
+        check(lib().klb_halo_pull_z(stream.handle, n, arr, lo, hi, elem_bytes, kk, kstart, kend, down, up,
+                                    below_kend, above_kstart))
+        check(lib().klb_event_record(self.pulled, stream.handle))
+        self.group.barrier()
+        for r in neighbours:
+            check(lib().klb_stream_wait_event(stream.handle, self._peer_events[r][1]))
+
+    def detach(self) -> None:
+        """Collective: unmap every peer allocation (before fields are freed)."""
+        from .cuda._abi import lib
+
+        lib().klb_device_synchronize()
+        self.group.barrier()  # nobody still copies from a mapping being closed
+        for base in self._opened:
+            lib().klb_ipc_mem_close(base)
+        self._opened, self._maps = [], {}
+        self.group.barrier()  # every peer has unmapped before anyone frees
+
+    def close(self) -> None:
+        from .cuda._abi import lib
+
+        if self._events:
+            self.detach()
+            for a, b in self._peer_events.values():
+                lib().klb_event_destroy(a)
+                lib().klb_event_destroy(b)
+            for ev in self._events:
+                lib().klb_event_destroy(ev)
+            self._events, self._peer_events = [], {}
+
+
 class CopyExchanger:
     """Virtual ranks on ONE device: the halo plan executed as D2D copies.
 
@@ -166,79 +301,6 @@ class CopyExchanger:
                     check(lib().klb_memcpy_dtod(self.ranks[r][name] + first * plane,
                                                 self.ranks[peer][name] + src_first * plane, count * plane,
                                                 stream.handle))
-
-
-class HostExchanger:
-    """The halo plan over torch.distributed (gloo) on NumPy (kcells, jcells, icells) arrays."""
-
-    def __init__(self, rank: int, nranks: int) -> None:
-        self.rank, self.nranks = rank, nranks
-
-    def exchange(self, arrays, kstart: int, kend: int, down: int, up: int, below: int, above: int) -> None:
-        import numpy as np
-        import torch
-        import torch.distributed as dist
-
-        reqs, sinks = [], []
-        for arr in arrays:
-            for op, peer, first, count in halo_plan(kstart, kend, down, up, below, above):
-                if op == "send":
-                    reqs.append(dist.isend(torch.from_numpy(np.ascontiguousarray(arr[first:first + count])), peer))
-                else:
-                    buf = torch.empty(arr[first:first + count].shape, dtype=torch.from_numpy(arr[:1]).dtype)
-                    reqs.append(dist.irecv(buf, peer))
-                    sinks.append((arr, first, count, buf))
-        for req in reqs:
-            req.wait()
-        for arr, first, count, buf in sinks:
-            arr[first:first + count] = buf.numpy()
-
-
-class StagedExchanger:
-    """The same exchange as ``NcclExchanger`` with the planes relayed through
-    pinned host memory over torch.distributed (any backend; gloo here).
-
-    Not a performance transport: it serialises on the host.  It exists so the
-    whole multi-rank path (decomposition, sub-range launches, exchange
-    ordering, max-over-ranks timing, bench output at N > 1) can run as several
-    processes on ONE GPU — NCCL refuses two ranks on one device — which is
-    what ``tests/test_gpu_multiproc.py`` does (selected in ``bench.py`` by
-    ``KL_HALO_TRANSPORT=staged``).  Same signature as ``NcclExchanger.exchange``.
-    """
-
-    def __init__(self, rank: int, nranks: int) -> None:
-        self.rank, self.nranks = rank, nranks
-
-    def exchange(self, stream, ptrs, elem_bytes: int, kk: int, kstart: int, kend: int, down: int, up: int,
-                 below: int, above: int) -> None:
-        import numpy as np
-        import torch
-        import torch.distributed as dist
-
-        from .cuda._abi import check, lib
-
-        plane = kk * elem_bytes
-        stream.synchronize()  # the planes to send are final (the comm stream waited on compute)
-        reqs, sinks = [], []
-        for ptr in ptrs:
-            for op, peer, first, count in halo_plan(kstart, kend, down, up, below, above):
-                buf = np.empty(count * plane, dtype=np.uint8)
-                if op == "send":
-                    check(lib().klb_memcpy_dtoh(buf.ctypes.data, ptr + first * plane, count * plane, stream.handle))
-                    stream.synchronize()
-                    reqs.append(dist.isend(torch.from_numpy(buf), peer))
-                else:
-                    t = torch.from_numpy(buf)
-                    reqs.append(dist.irecv(t, peer))
-                    sinks.append((ptr + first * plane, buf))
-        for req in reqs:
-            req.wait()
-        for dst, buf in sinks:
-            check(lib().klb_memcpy_htod(dst, buf.ctypes.data, buf.nbytes, stream.handle))
-        stream.synchronize()
-
-    def close(self) -> None:
-        pass
 
 
 @dataclass

@@ -7,9 +7,10 @@ Wires the pieces of ``halo.py`` to the runtime launch path:
 * every sub-range (interior / lower / upper, ``SlabRank.subranges``) is
   launched through ``WisdomKernel.launch`` — the application-facing API —
   so each gets its own wisdom selection and compiled instance;
-* ``step()`` issues: halo exchange on the comm stream (NCCL, or D2D copies
-  for virtual ranks), the interior launch on the compute stream concurrently,
-  then the boundary launches after the exchange event.
+* ``step()`` issues: halo exchange on the comm stream (peer-memory pulls over
+  CUDA IPC, NCCL send/recv, or D2D copies for virtual ranks), the interior
+  launch on the compute stream concurrently, then the boundary launches
+  after the exchange event.
 
 All launches are asynchronous; callers time steps with CUDA events on
 ``compute`` (the comm stream is joined back into it every step).
@@ -197,6 +198,11 @@ class SlabDriver:
         return len(plan)
 
     def close(self) -> None:
+        """Collective when the exchanger maps peer memory (IPC): every rank
+        unmaps its neighbours' fields before any rank frees its own."""
+        detach = getattr(self.exchanger, "detach", None)
+        if callable(detach):
+            detach()
         self.problem.close()
         if self.comm is not None:
             self.comm.close()

@@ -3,7 +3,8 @@
 Per SURVEY.md §8d: layer thicknesses ``dz[k] ~ U(0.8, 1.2)`` drawn from a
 splitmix64 stream, ``zh`` (half levels) accumulated upward from
 ``zh[kstart] = 0``, ``z`` at cell centres, ``dzh = z[k] - z[k-1]``,
-``rhoref = exp(-z/10)``, ``rhorefh = exp(-zh/10)``.  Arrays have one entry per
+``rhoref = exp(-z/H)``, ``rhorefh = exp(-zh/H)`` with H = 10 up to 64 levels
+and stretched with deeper grids (``scale_height``).  Arrays have one entry per
 GLOBAL ghost-padded level; a z-slab slices its window (no exchange needed).
 """
 
@@ -65,10 +66,25 @@ def make_profiles(kcells: int, kgc: int) -> Profiles:
     dzh = np.empty(kcells)
     dzh[1:] = z[1:] - z[:-1]
     dzh[0] = dz[0]
+    height = scale_height(kcells, kgc)
     return Profiles(
         dz=dz,
         dzi=1.0 / dz,
         dzhi=1.0 / dzh,
-        rhoref=np.exp(-z / 10.0),
-        rhorefh=np.exp(-zh[:-1] / 10.0),
+        rhoref=np.exp(-z / height),
+        rhorefh=np.exp(-zh[:-1] / height),
     )
+
+
+def scale_height(kcells: int, kgc: int) -> float:
+    """Density scale height of the synthetic reference state.
+
+    SURVEY §8d gives ``exp(-z/10)``; with dz ~ 1 per level that is kept for
+    grids up to 64 levels, and deeper grids stretch it with the domain
+    (10 per 64 levels): unstretched, ``rhoref`` at z ~ 1000 is ~1e-44, below
+    fp32's normal range, so an fp32 1024-level grid would divide by flushed
+    denormals and compute inf/NaN in its top ~15 % of planes (caught by the
+    bench-shape parity test).  The profile stays a global function of the
+    level, so z-slabs still slice it without an exchange."""
+    ktot = kcells - 2 * kgc
+    return 10.0 * max(1.0, ktot / 64.0)

@@ -67,7 +67,9 @@ def window_error(prob: StencilProblem, kernel: str, kb: int, ke: int) -> dict:
     out = {}
     for name, r in ref.items():
         got = download_planes(prob, name, kb, ke).astype(np.float64)
-        out[name] = float(np.max(np.abs(got - r)) / np.max(np.abs(r)))
+        # a NaN/inf anywhere (output or reference) is an unbounded error
+        err = float(np.max(np.abs(got - r)) / np.max(np.abs(r)))
+        out[name] = err if np.isfinite(err) else float("inf")
     return out
 
 
@@ -110,7 +112,8 @@ def rel_error(got: np.ndarray, ref: np.ndarray, layout: GridLayout) -> float:
     gi = layout.interior(got).astype(np.float64)
     ri = layout.interior(ref)
     scale = np.max(np.abs(ri))
-    return float(np.max(np.abs(gi - ri)) / scale)
+    err = float(np.max(np.abs(gi - ri)) / scale)
+    return err if np.isfinite(err) else float("inf")
 
 
 def run_config(ctx, compiler, kernel, layout, config, k_range=None):

@@ -81,10 +81,37 @@ def _oracle(kernel, f, prof, interior):
     return {"ut": ut, "vt": vt, "wt": wt}
 
 
+class HostExchanger:
+    """The halo plan over torch.distributed (gloo) on NumPy (kcells, jcells, icells)
+    arrays — the CPU-test transport of the same ``halo_plan`` the C-ABI
+    transports (NCCL send/recv, CUDA-IPC pull) run on the GPU."""
+
+    def __init__(self, rank: int, nranks: int) -> None:
+        self.rank, self.nranks = rank, nranks
+
+    def exchange(self, arrays, kstart: int, kend: int, down: int, up: int, below: int, above: int) -> None:
+        import numpy as np
+        import torch
+        import torch.distributed as dist
+
+        reqs, sinks = [], []
+        for arr in arrays:
+            for op, peer, first, count in halo_plan(kstart, kend, down, up, below, above):
+                if op == "send":
+                    reqs.append(dist.isend(torch.from_numpy(np.ascontiguousarray(arr[first:first + count])), peer))
+                else:
+                    buf = torch.empty(arr[first:first + count].shape, dtype=torch.from_numpy(arr[:1]).dtype)
+                    reqs.append(dist.irecv(buf, peer))
+                    sinks.append((arr, first, count, buf))
+        for req in reqs:
+            req.wait()
+        for arr, first, count, buf in sinks:
+            arr[first:first + count] = buf.numpy()
+
+
 def _rank_main(rank, nranks, port, kernel, queue):
     import torch.distributed as dist
 
-    from paper_2303_12374_b200.halo import HostExchanger
     from paper_2303_12374_b200.stencils.profiles import make_profiles
 
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
