@@ -78,3 +78,17 @@ def _map(fn, items, threads, pool):
         return
     with ThreadPoolExecutor(max_workers=threads) as tp:
         list(tp.map(fn, items))
+
+
+def synth_field(seed, lo, hi, icells, jcells, kcells, igc, jgc, k_offset=0, dtype=np.float64, threads=1, pool=None):
+    """C twin of oracle.synth.synth_field (bit-exact), z-chunks on ``threads``."""
+    out = np.empty((kcells, jcells, icells), dtype=dtype)
+    suffix = "f32" if out.dtype == np.float32 else "f64"
+    fn = getattr(_lib(), f"synth_field_{suffix}")
+
+    def run(kr):
+        fn(_ptr(out), C.c_uint64(seed & 0xFFFFFFFFFFFFFFFF), C.c_double(lo), C.c_double(hi), icells, jcells, igc, jgc,
+           k_offset, kr[0], kr[1])
+
+    _map(run, _chunks(0, kcells, threads), threads, pool)
+    return out

@@ -16,6 +16,7 @@
  */
 #include <math.h>
 #include <stddef.h>
+#include <stdint.h>
 
 #define IDX(i, j, k) ((i) + (ptrdiff_t)(j) * jj + (ptrdiff_t)(k) * kk)
 
@@ -97,3 +98,38 @@
 
 DEFINE_KERNELS(double, f64)
 DEFINE_KERNELS(float, f32)
+
+/* Synthetic input fields, bit-exact with oracle/synth.py and the device
+ * generator klb_synth_field (value of element (i,j,k) = draw n+1 of
+ * SplitMix64(seed), n the global logical index with periodic x/y ghosts,
+ * mapped to [lo, hi) by two IEEE double ops — no FMA contraction: -std=c11).
+ * Fills planes [k0, k1) of a contiguous (kcells, jcells, icells) array whose
+ * plane 0 is global plane k_offset; the CPU reference arm fills whole 1024^3
+ * grids with it, one z-chunk per host thread. */
+static inline uint64_t synth_mix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+#define DEFINE_SYNTH(T, SUFFIX)                                                                          \
+  void synth_field_##SUFFIX(T* out, uint64_t seed, double lo, double hi, int icells, int jcells, int igc, \
+                            int jgc, int k_offset, int k0, int k1) {                                      \
+    const int itot = icells - 2 * igc, jtot = jcells - 2 * jgc;                                           \
+    const double span = hi - lo;                                                                          \
+    for (int k = k0; k < k1; ++k)                                                                         \
+      for (int j = 0; j < jcells; ++j) {                                                                  \
+        const int js = jgc + ((j - jgc) % jtot + jtot) % jtot;                                            \
+        T* row = out + ((ptrdiff_t)k * jcells + j) * icells;                                              \
+        for (int i = 0; i < icells; ++i) {                                                                \
+          const int is = igc + ((i - igc) % itot + itot) % itot;                                          \
+          const uint64_t n = ((uint64_t)(k + k_offset) * jcells + js) * icells + is;                      \
+          const uint64_t h = synth_mix64(seed + (n + 1ull) * 0x9E3779B97F4A7C15ull);                      \
+          const double x = (double)(h >> 11) * 0x1.0p-53;                                                 \
+          row[i] = (T)(lo + span * x);                                                                    \
+        }                                                                                                 \
+      }                                                                                                   \
+  }
+
+DEFINE_SYNTH(float, f32)
+DEFINE_SYNTH(double, f64)

@@ -89,13 +89,14 @@ def test_bench_spawns_its_own_ranks():
     assert len(lines) == 1, out.stdout
     line = lines[0]
     assert line["n_gpus"] == 2 and line["value"] > 0 and line["config"]["decomposition"] == "z-slab x2"
-    assert line["config"]["halo_transport"] == "ipc" and "comm nranks=2" in out.stderr
+    assert line["halo_transport"] == "ipc" and "comm nranks=2" in out.stderr
     assert line["e2e"]["value"] > 0 and line["gpu_launches"] > 0
     ref = subprocess.run([sys.executable, "bench.py", *common, "--impl", "reference"], cwd=ROOT, env=env,
                          capture_output=True, text=True, timeout=900)
     assert ref.returncode == 0, ref.stdout[-2000:] + ref.stderr[-2000:]
     lines = _lines(ref.stdout)
     assert len(lines) == 1 and lines[0]["impl"] == "reference" and lines[0]["value"] > 0
+    assert lines[0]["config"] == line["config"]  # the driver matches the arms by config
 
 
 def test_bench_under_torchrun_prints_one_line():
