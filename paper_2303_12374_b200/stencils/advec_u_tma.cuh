@@ -40,6 +40,9 @@
 #ifndef DEPTH
 #define DEPTH 2
 #endif
+#ifndef KL_YSPLIT
+#define KL_YSPLIT 0  // 0: blocks of kTYT rows; n > 0: n near-equal row runs (entry below)
+#endif
 
 #include "kl_pack.cuh"
 #include "kl_tma.cuh"
@@ -229,8 +232,10 @@ struct AdvecTma {
     }
 
     Cursor cur;
+    const bool active = j0 + lj0 < jend;  // a strip past the block's last row only keeps the barriers
     for (int k = k0; k < k1; ++k) {
       const Planes pl = begin_step(k, cur);
+      if (!active) continue;
       const real *xy = pl.xy, *zf = pl.zf, *vp = pl.vp, *wp = pl.wp, *tp = pl.tp;
       const real rh_top = zprof[2 * (k - k0)];
       const real zfac120 = zprof[2 * (k - k0) + 1];
@@ -353,8 +358,10 @@ struct AdvecTma {
     const f2 dx2(dxi120), dy2(dyi120);
 
     Cursor cur;
+    const bool active = j0 + lj0 < jend;  // a strip past the block's last row only keeps the barriers
     for (int k = k0; k < k1; ++k) {
       const Planes pl = begin_step(k, cur);
+      if (!active) continue;
       const real *xy = pl.xy, *zf = pl.zf, *vp = pl.vp, *wp = pl.wp, *tp = pl.tp;
       const f2 rh_top(zprof[2 * (k - k0)]);
       const f2 zfac(zprof[2 * (k - k0) + 1]);
@@ -498,12 +505,20 @@ KL_ENTRY(real* __restrict__ ut, const real* __restrict__ u, const real* __restri
   real* const zprof = ring_v + kNV * kVS;                                     // [ZCHUNK][2]
 
   const unsigned nbx = kl::ceil_div(iend - istart, kXT);
-  const unsigned nby = kl::ceil_div(jend - jstart, kTYT);
+  const unsigned nby = KL_YSPLIT > 0 ? KL_YSPLIT : kl::ceil_div(jend - jstart, kTYT);
   const unsigned nbz = kl::ceil_div(kend - kstart, ZCHUNK);
   int bx, by, bz;
   kl::unravel(blockIdx.x, nbx, nby, nbz, bx, by, bz);
   const int i0 = istart + bx * kXT;
-  const int j0 = jstart + by * kTYT;
+  // rows of this block: tiles of kTYT rows, or (KL_YSPLIT) the y extent cut
+  // into KL_YSPLIT near-equal runs of at most kTYT rows, so the grid can be
+  // sized to whole waves of the SMs whatever jtot / kTYT is
+  const int jt = jend - jstart;
+  const int j0 = KL_YSPLIT > 0 ? jstart + static_cast<int>((static_cast<long long>(by) * jt) / KL_YSPLIT)
+                               : jstart + by * kTYT;
+  const int jhi = KL_YSPLIT > 0 ? jstart + static_cast<int>((static_cast<long long>(by + 1) * jt) / KL_YSPLIT)
+                                : jend;
+  if (jhi - j0 > kTYT && KL_YSPLIT > 0) __trap();
   const int k0 = kstart + bz * ZCHUNK;
   const int k1 = min(k0 + ZCHUNK, kend);
   const int tid = threadIdx.x + threadIdx.y * BLOCK_X;
@@ -532,7 +547,7 @@ KL_ENTRY(real* __restrict__ ut, const real* __restrict__ u, const real* __restri
   m.k1 = k1;
   m.tid = tid;
   m.iend = iend;
-  m.jend = jend;
+  m.jend = jhi;
   m.xu = xu - sh_u;
   m.xv = xv - sh_v;
   m.xw = xw - sh_w;
