@@ -494,17 +494,19 @@ def suite_measure(ctx, compiler, wisdom_dir, peak, suite=SUITE):
 GRAPH_SUITE = [("diff_uvw", "fp64", (64, 64, 64), "config 1"), ("advec_u", "fp32", (128, 128, 128), "128^3")]
 
 
-def graph_measure(ctx, compiler, wisdom_dir, n=200):
-    """Launch-bound small problems: n back-to-back applications of the tuned
-    kernel (L2 warm, no flush between them) enqueued one bound launch at a
-    time vs replayed as one captured CUDA graph (WisdomKernel.graph); device
-    time per application from events on the launching stream, plus the host
-    enqueue cost per application."""
+def graph_measure(ctx, compiler, wisdom_dir, peak, n=200):
+    """Launch-bound small problems (config 1): n back-to-back applications of
+    the tuned kernel (L2 warm, no flush between them — the working set stays
+    in L2) enqueued one bound launch at a time, with programmatic dependent
+    launch (PDL), replayed as one captured CUDA graph, and as a graph with
+    PDL edges; device time per application from events on the launching
+    stream, plus the host enqueue cost per application.  The cold (L2
+    flushed, eager) figure of the same kernel is the ``suite`` row."""
     from paper_2303_12374_b200.capture import CapturePolicy
     from paper_2303_12374_b200.cuda import Event, Stream
     from paper_2303_12374_b200.dispatch import WisdomKernel
     from paper_2303_12374_b200.stencils.layout import GridLayout
-    from paper_2303_12374_b200.stencils.problem import StencilProblem
+    from paper_2303_12374_b200.stencils.problem import KERNEL_FIELDS, StencilProblem
 
     rows = []
     stream = Stream.create()
@@ -514,32 +516,44 @@ def graph_measure(ctx, compiler, wisdom_dir, n=200):
             prob = StencilProblem(kernel, lay, ctx)
             wk = WisdomKernel(prob.definition, compiler, wisdom_dir=wisdom_dir, capture_policy=CapturePolicy())
             run = wk.bind(ctx.ident, prob.args(), stream=stream)
+            run_pdl = wk.bind(ctx.ident, prob.args(), stream=stream, pdl=True)
             g = wk.graph(ctx.ident, prob.args(), stream, repeat=n)
-            row = {"config": tag, "kernel": kernel, "precision": precision, "grid": list(grid), "applications": n}
-            for variant in ("eager", "graph"):
+            gp = wk.graph(ctx.ident, prob.args(), stream, repeat=n, pdl=True)
+            footprint = len(KERNEL_FIELDS[kernel]) * lay.alloc_bytes
+            row = {"config": tag, "kernel": kernel, "precision": precision, "grid": list(grid), "applications": n,
+                   "algorithmic_bytes_per_application": prob.algorithmic_bytes,
+                   "working_set_bytes": footprint, "l2_resident": footprint < 126e6}
+            variants = {"eager": lambda: [run() for _ in range(n)],
+                        "eager_pdl": lambda: [run_pdl() for _ in range(n)],
+                        "graph": lambda: g.launch(stream), "graph_pdl": lambda: gp.launch(stream)}
+            for variant, go in variants.items():
                 best = None
                 for _ in range(3):
-                    (run() if variant == "eager" else g.launch(stream))  # warm
+                    go()  # warm
                     stream.synchronize()
                     e0, e1 = Event(), Event()
                     e0.record(stream)
                     t0 = time.perf_counter()
-                    if variant == "eager":
-                        for _ in range(n):
-                            run()
-                    else:
-                        g.launch(stream)
+                    go()
                     host = time.perf_counter() - t0
                     e1.record(stream)
                     e1.synchronize()
                     dev = e0.elapsed_ms(e1) * 1e-3
                     if best is None or dev < best[0]:
                         best = (dev, host)
-                row[variant] = {"us_per_application": round(best[0] / n * 1e6, 3),
+                per = best[0] / n
+                row[variant] = {"us_per_application": round(per * 1e6, 3),
                                 "host_enqueue_us_per_application": round(best[1] / n * 1e6, 3),
-                                "gcells": round(lay.cells * n / best[0] / 1e9, 2)}
+                                "gcells": round(lay.cells / per / 1e9, 2),
+                                # L2-resident: the HBM roofline does not bound these; GB/s of algorithmic
+                                # bytes per application, reported beside (not against) the HBM peak
+                                "algorithmic_gbs": round(prob.algorithmic_bytes / per / 1e9, 1),
+                                "of_hbm_peak": round(prob.algorithmic_bytes / per / 1e9 / peak, 3)}
             row["graph_speedup"] = round(row["eager"]["us_per_application"] / row["graph"]["us_per_application"], 3)
+            row["graph_pdl_speedup"] = round(row["eager"]["us_per_application"] /
+                                             row["graph_pdl"]["us_per_application"], 3)
             g.close()
+            gp.close()
             prob.close()
             rows.append(row)
     finally:
@@ -673,7 +687,7 @@ def run_ours(args, dist):
         except Exception as err:
             line["fusion"] = {"error": repr(err)[:300]}
         try:
-            line["graph"] = graph_measure(ctx, compiler, wisdom_dir)
+            line["graph"] = graph_measure(ctx, compiler, wisdom_dir, peak)
         except Exception as err:
             line["graph"] = {"error": repr(err)[:300]}
     driver.close()

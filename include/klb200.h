@@ -121,6 +121,15 @@ int klb_occupancy_blocks_per_sm(klb_function fn, int block_threads, int dynamic_
  * pointers to each argument value. */
 int klb_launch(klb_function fn, const unsigned grid[3], const unsigned block[3],
                unsigned dynamic_smem, klb_stream stream, void** params);
+/* klb_launch with launch attributes.  KLB_LAUNCH_PDL: programmatic
+ * dependent launch — the kernel may start launching while the previous
+ * kernel on `stream` drains (every stencil calls griddepcontrol.wait before
+ * its first global read and griddepcontrol.launch_dependents after its last
+ * one), hiding the launch gap between back-to-back applications; inside a
+ * stream capture it becomes a programmatic graph edge. */
+#define KLB_LAUNCH_PDL 1u
+int klb_launch_ex(klb_function fn, const unsigned grid[3], const unsigned block[3],
+                  unsigned dynamic_smem, klb_stream stream, void** params, unsigned flags);
 /* Timed replay: `warmup` untimed launches, then `reps` launches each bracketed
  * by events on `stream`; when flush_bytes > 0 the buffer at flush_ptr is
  * overwritten before every launch (outside the timed window) so each launch

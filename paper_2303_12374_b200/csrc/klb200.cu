@@ -51,7 +51,7 @@ int g_default_ordinal = -1;
 // CUDA driver API, resolved at runtime through cudaGetDriverEntryPoint so the
 // library has no link-time dependency on libcuda.so.1: it loads (and reports
 // a clean error from klb_init) on hosts without an NVIDIA driver.
-#define KLB_DRIVER_API(X) X(cuCtxGetCurrent) X(cuCtxSetCurrent) X(cuCtxSynchronize) X(cuDeviceGet) X(cuDeviceGetAttribute) X(cuDeviceGetCount) X(cuDeviceGetName) X(cuDeviceGetUuid) X(cuDevicePrimaryCtxRetain) X(cuDeviceTotalMem) X(cuDriverGetVersion) X(cuEventCreate) X(cuEventDestroy) X(cuEventElapsedTime) X(cuEventRecord) X(cuEventSynchronize) X(cuFuncGetAttribute) X(cuFuncSetAttribute) X(cuGetErrorName) X(cuGetErrorString) X(cuInit) X(cuLaunchKernel) X(cuMemAlloc) X(cuMemFree) X(cuMemFreeHost) X(cuMemGetInfo) X(cuMemHostAlloc) X(cuMemcpyDtoDAsync) X(cuMemcpyDtoHAsync) X(cuMemcpyHtoDAsync) X(cuMemsetD32Async) X(cuMemsetD8Async) X(cuModuleGetFunction) X(cuModuleLoadData) X(cuModuleUnload) X(cuOccupancyMaxActiveBlocksPerMultiprocessor) X(cuStreamCreateWithPriority) X(cuStreamDestroy) X(cuStreamSynchronize) X(cuStreamWaitEvent) X(cuModuleGetGlobal) X(cuTensorMapEncodeTiled) X(cuStreamBeginCapture) X(cuStreamEndCapture) X(cuGraphInstantiateWithFlags) X(cuGraphLaunch) X(cuGraphDestroy) X(cuGraphExecDestroy) X(cuIpcGetMemHandle) X(cuIpcOpenMemHandle) X(cuIpcCloseMemHandle) X(cuIpcGetEventHandle) X(cuIpcOpenEventHandle) X(cuMemGetAddressRange)
+#define KLB_DRIVER_API(X) X(cuCtxGetCurrent) X(cuCtxSetCurrent) X(cuCtxSynchronize) X(cuDeviceGet) X(cuDeviceGetAttribute) X(cuDeviceGetCount) X(cuDeviceGetName) X(cuDeviceGetUuid) X(cuDevicePrimaryCtxRetain) X(cuDeviceTotalMem) X(cuDriverGetVersion) X(cuEventCreate) X(cuEventDestroy) X(cuEventElapsedTime) X(cuEventRecord) X(cuEventSynchronize) X(cuFuncGetAttribute) X(cuFuncSetAttribute) X(cuGetErrorName) X(cuGetErrorString) X(cuInit) X(cuLaunchKernel) X(cuLaunchKernelEx) X(cuMemAlloc) X(cuMemFree) X(cuMemFreeHost) X(cuMemGetInfo) X(cuMemHostAlloc) X(cuMemcpyDtoDAsync) X(cuMemcpyDtoHAsync) X(cuMemcpyHtoDAsync) X(cuMemsetD32Async) X(cuMemsetD8Async) X(cuModuleGetFunction) X(cuModuleLoadData) X(cuModuleUnload) X(cuOccupancyMaxActiveBlocksPerMultiprocessor) X(cuStreamCreateWithPriority) X(cuStreamDestroy) X(cuStreamSynchronize) X(cuStreamWaitEvent) X(cuModuleGetGlobal) X(cuTensorMapEncodeTiled) X(cuStreamBeginCapture) X(cuStreamEndCapture) X(cuGraphInstantiateWithFlags) X(cuGraphLaunch) X(cuGraphDestroy) X(cuGraphExecDestroy) X(cuIpcGetMemHandle) X(cuIpcOpenMemHandle) X(cuIpcCloseMemHandle) X(cuIpcGetEventHandle) X(cuIpcOpenEventHandle) X(cuMemGetAddressRange)
 
 struct DriverApi {
 #define KLB_DECL(name) decltype(&::name) name = nullptr;
@@ -535,6 +535,34 @@ int klb_launch(klb_function fn, const unsigned grid[3], const unsigned block[3],
   CTX_TRY();
   CU_TRY(drv.cuLaunchKernel(reinterpret_cast<CUfunction>(fn), grid[0], grid[1], grid[2], block[0], block[1], block[2],
                         dynamic_smem, as_stream(stream), params, nullptr));
+  return 0;
+}
+
+int klb_launch_ex(klb_function fn, const unsigned grid[3], const unsigned block[3], unsigned dynamic_smem,
+                  klb_stream stream, void** params, unsigned flags) {
+  if (flags & ~static_cast<unsigned>(KLB_LAUNCH_PDL)) return fail(KLB_E_INVALID, "unknown launch flags %#x", flags);
+  CTX_TRY();
+  CUlaunchConfig cfg = {};
+  cfg.gridDimX = grid[0];
+  cfg.gridDimY = grid[1];
+  cfg.gridDimZ = grid[2];
+  cfg.blockDimX = block[0];
+  cfg.blockDimY = block[1];
+  cfg.blockDimZ = block[2];
+  cfg.sharedMemBytes = dynamic_smem;
+  cfg.hStream = as_stream(stream);
+  CUlaunchAttribute attr[1];
+  if (flags & KLB_LAUNCH_PDL) {
+    // programmatic dependent launch: this grid may begin launching once every
+    // block of the previous kernel on the stream has triggered
+    // (griddepcontrol.launch_dependents) or exited; it waits for that
+    // kernel's completion and memory flush at griddepcontrol.wait (kl_common.cuh)
+    attr[0].id = CU_LAUNCH_ATTRIBUTE_PROGRAMMATIC_STREAM_SERIALIZATION;
+    attr[0].value.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+  }
+  CU_TRY(drv.cuLaunchKernelEx(&cfg, reinterpret_cast<CUfunction>(fn), params, nullptr));
   return 0;
 }
 

@@ -90,6 +90,7 @@ EXPORTS: dict[str, list] = {
     "klb_function_set_max_dynamic_smem": [_vp, _i],
     "klb_occupancy_blocks_per_sm": [_vp, _i, _i, C.POINTER(_i)],
     "klb_launch": [_vp, _u3, _u3, _u, _vp, _pvp],
+    "klb_launch_ex": [_vp, _u3, _u3, _u, _vp, _pvp, _u],
     "klb_time_launches": [_vp, _u3, _u3, _u, _vp, _pvp, _i, _i, _u64, _sz, C.POINTER(C.c_float)],
     "klb_mem_alloc": [_sz, C.POINTER(_u64)],
     "klb_mem_free": [_u64],

@@ -272,22 +272,34 @@ class CudaExecutable(ExecutableHandle):
             self._geoms[geometry] = (grid, block, smem)
         return grid, block, smem
 
-    def bound(self, geometry: LaunchGeometry, args: Sequence[object], stream: Stream | None = None):
+    def bound(self, geometry: LaunchGeometry, args: Sequence[object], stream: Stream | None = None,
+              pdl: bool = False):
         """A zero-argument callable enqueueing this launch: grid, block and the
         packed parameters (TMA descriptors included) are built once, so each
         call is one C-ABI launch — the paper's cached-launch path
-        (PAPER.md:607-625).  ``args`` must stay valid while it is used."""
+        (PAPER.md:607-625).  ``args`` must stay valid while it is used.
+        ``pdl``: programmatic dependent launch (``klb_launch_ex``), so
+        back-to-back launches overlap one's launch with the other's drain."""
         grid, block, smem = self._prepare(geometry)
         params, keep, staged = self._params(args, stream)
         if staged:
             raise LaunchError("bound launches need device-resident arguments")
         handle = stream.handle if stream is not None else (self.ctx.stream.handle if self.ctx else None)
-        fn, launch = self.function, lib().klb_launch
+        fn = self.function
+        if pdl:
+            launch_ex = lib().klb_launch_ex
 
-        def run() -> None:
-            rc = launch(fn, grid, block, smem, handle, params)
-            if rc:
-                check(rc)
+            def run() -> None:
+                rc = launch_ex(fn, grid, block, smem, handle, params, 1)
+                if rc:
+                    check(rc)
+        else:
+            launch = lib().klb_launch
+
+            def run() -> None:
+                rc = launch(fn, grid, block, smem, handle, params)
+                if rc:
+                    check(rc)
 
         run.keep = (grid, block, params, keep)  # the ctypes objects outlive the closure's callers
         return run

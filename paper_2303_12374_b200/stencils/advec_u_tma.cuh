@@ -495,6 +495,8 @@ KL_ENTRY(real* __restrict__ ut, const real* __restrict__ u, const real* __restri
          const int istart, const int jstart, const int kstart, const int iend, const int jend,
          const int kend, const __grid_constant__ KlTmaParams tma) {
   if (jj != KL_JJ || kk != KL_KK) __trap();
+  kl::pdl_trigger();  // programmatic dependent launch (kl_common.cuh): the next kernel may launch
+  kl::pdl_wait();     // no global access before the previous kernel on the stream has completed
   // param-space address of the descriptors (__grid_constant__: no local copy)
   const TmaDesc* const maps = &tma.map[0];
   extern __shared__ __align__(128) unsigned char kl_smem_raw[];

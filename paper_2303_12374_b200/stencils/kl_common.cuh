@@ -55,6 +55,17 @@ typedef KL_REAL real;
 
 namespace kl {
 
+// Programmatic dependent launch (sm_90+; klb_launch_ex KLB_LAUNCH_PDL): a
+// kernel launched with the attribute may be scheduled while the previous
+// kernel on the stream drains.  pdl_wait() blocks until that kernel has
+// completed and its writes are visible — every stencil calls it before its
+// first global read (after its shared-memory/mbarrier setup, which thereby
+// overlaps the previous kernel's tail); pdl_trigger() after a block's last
+// global read lets the next kernel start launching.  Both are no-ops for a
+// kernel launched without the attribute.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // 1-D block id -> 3-D block coordinates; the first letter of UNRAVEL is the
 // fastest-varying axis (PAPER.md: "for (Z,X,Y) ... first along Z, then X, then Y").
 __device__ __forceinline__ void unravel(unsigned b, unsigned nbx, unsigned nby, unsigned nbz,

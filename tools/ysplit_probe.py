@@ -3,7 +3,7 @@ configurations with -D KL_YSPLIT=n, launch nbx*n*nbz blocks, verify against
 the default configuration's output and time (L2 flushed).  GPU only.
 
     python tools/ysplit_probe.py --kernel advec_u --precision fp32 --grid 256,256,256 \
-        --config '{"block_x":32,"block_y":8,"tile_x":4,"tile_y":1,"zchunk":128,"depth":4}' --ysplit 0,37,74
+        --case '{"block_y":8,"tile_y":1,"zchunk":128,"depth":4,"ysplit":37}' --case '{}'
 """
 
 from __future__ import annotations
@@ -23,8 +23,8 @@ def main(argv=None) -> int:
     ap.add_argument("--kernel", default="advec_u")
     ap.add_argument("--precision", default="fp32")
     ap.add_argument("--grid", default="256,256,256")
-    ap.add_argument("--config", action="append", required=True, help="JSON overrides of the wisdom config")
-    ap.add_argument("--ysplit", default="0")
+    ap.add_argument("--case", action="append", required=True,
+                    help='JSON overrides of the wisdom config plus "ysplit" (0 = natural tiling)')
     ap.add_argument("--reps", type=int, default=15)
     ap.add_argument("--json-out")
     a = ap.parse_args(argv)
@@ -49,9 +49,11 @@ def main(argv=None) -> int:
     out = open(a.json_out, "a") if a.json_out else None
     bytes_ = BYTES_PER_CELL_WORDS[a.kernel] * lay.elem_bytes * lay.cells
     peak = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["hbm_gbs"] if (ROOT / "MEASURED_PEAKS.json").exists() else 6458.7
-    for text in a.config:
-        cfg = dict(base, **json.loads(text))
-        for n in (int(x) for x in a.ysplit.split(",")):
+    for text in a.case:
+        over = json.loads(text)
+        n = int(over.pop("ysplit", 0))
+        cfg = dict(base, **over)
+        if True:
             req = d.render_compile_request(cfg, ex.problem, ex.scalar_env)
             if n:
                 req = CompileRequest(req.source, req.entry, req.defines + (f"-D KL_YSPLIT={n}",), req.flags)
