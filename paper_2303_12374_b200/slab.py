@@ -135,44 +135,51 @@ class SlabDriver:
                 launched += 1
         return launched
 
-    def step_host(self, host: dict[str, int], chunks: int = 16) -> int:
+    def step_host(self, host: dict[str, int], chunks: int = 16, copy_streams: int = 1) -> int:
         """One step streamed from/to pinned host memory (``stream.py``).
 
         ``host`` maps every field to a pinned host buffer laid out exactly like
         the device allocation (``layout.alloc_bytes``); inputs and RMW outputs
         are read from it, the tendencies written back.  Enqueued on the
         compute, h2d, d2h (and comm) streams and joined back into ``compute``;
-        returns the number of kernels launched."""
+        returns the number of kernels launched.  ``copy_streams`` > 1 spreads
+        the chunks' uploads (and downloads) round-robin over that many
+        streams per direction, so several copy engines share the link."""
         from .cuda._abi import check, lib
         from .stream import stream_plan
 
         lay = self.layout
-        if self._stream_state is None or self._stream_state[0] != chunks:
+        if self._stream_state is None or self._stream_state[0] != (chunks, copy_streams):
             fields = tuple(self.problem.fields)
             plan = stream_plan(self.kernel, fields, self.problem.outputs(), self.ranges, lay.kcells, lay.kstart,
                                lay.kend, self.below, self.above, chunks)
             args = {st.name: self.problem.args(st.k_range) for st in plan}
             events = [(Event(), Event()) for _ in plan]
-            if self._h2d is None:
-                self._h2d, self._d2h = Stream.create(), Stream.create()
-                self._ev_join = Event()
-            self._stream_state = (chunks, plan, args, events)
+            if self._h2d is None or len(self._h2d) != copy_streams:
+                for st in (self._h2d or []) + (self._d2h or []):
+                    st.close()
+                self._h2d = [Stream.create() for _ in range(copy_streams)]
+                self._d2h = [Stream.create() for _ in range(copy_streams)]
+                self._ev_join = [Event() for _ in range(copy_streams)]
+            self._stream_state = ((chunks, copy_streams), plan, args, events)
         _, plan, args, events = self._stream_state
+        ns = len(self._h2d)
         plane = lay.kk * lay.elem_bytes
         lead = lay.lead * lay.elem_bytes
         dev = {n: a.ptr for n, a in self.problem.fields.items()}
         ident = self.ctx.ident
 
         start = self._ev_start.record(self.compute)
-        self._h2d.wait(start)
-        self._d2h.wait(start)
+        for st in self._h2d + self._d2h:
+            st.wait(start)
         n_boundary = sum(1 for st in plan if st.after_halo)
         for i, st in enumerate(plan):
+            up = self._h2d[i % ns]
             for c in st.uploads:
                 off = lead + c.p0 * plane
                 check(lib().klb_memcpy_htod(dev[c.field] + off, host[c.field] + off, (c.p1 - c.p0) * plane,
-                                            self._h2d.handle))
-            events[i][0].record(self._h2d)
+                                            up.handle))
+            events[i][0].record(up)
             if self.exchanger is not None and i + 1 == max(n_boundary, 1):
                 self.exchange(after=events[i][0])
         order = [i for i, st in enumerate(plan) if not st.after_halo] + [i for i, st in enumerate(plan) if st.after_halo]
@@ -185,14 +192,16 @@ class SlabDriver:
                 waited_halo = True
             self.wisdom.launch(ident, args[st.name], stream=self.compute)
             events[i][1].record(self.compute)
-            self._d2h.wait(events[i][1])
+            down = self._d2h[i % ns]
+            down.wait(events[i][1])
             for c in st.downloads:
                 off = lead + c.p0 * plane
                 check(lib().klb_memcpy_dtoh(host[c.field] + off, dev[c.field] + off, (c.p1 - c.p0) * plane,
-                                            self._d2h.handle))
+                                            down.handle))
         if self.exchanger is not None and not waited_halo:
             self.compute.wait(self._ev_halo)
-        self.compute.wait(self._ev_join.record(self._d2h))
+        for ev, down in zip(self._ev_join, self._d2h):
+            self.compute.wait(ev.record(down))
         self.stream_bytes = (sum((c.p1 - c.p0) * plane for st in plan for c in st.uploads),
                              sum((c.p1 - c.p0) * plane for st in plan for c in st.downloads))
         return len(plan)
@@ -206,6 +215,5 @@ class SlabDriver:
         self.problem.close()
         if self.comm is not None:
             self.comm.close()
-        for s in (self._h2d, self._d2h):
-            if s is not None:
-                s.close()
+        for s in (self._h2d or []) + (self._d2h or []):
+            s.close()

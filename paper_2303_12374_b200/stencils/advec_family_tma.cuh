@@ -380,7 +380,7 @@ KL_ENTRY(real* __restrict__ tend,
          const real dxi, const real dyi, const int jj, const int kk, const int istart, const int jstart,
          const int kstart, const int iend, const int jend, const int kend, const __grid_constant__ KlTmaParams tma) {
   if (jj != KL_JJ || kk != KL_KK) __trap();
-  kl::pdl_trigger();  // programmatic dependent launch (kl_common.cuh): the next kernel may launch
+  const kl::PdlTriggerAtExit kl_pdl_exit;  // programmatic dependent launch (kl_common.cuh)
   kl::pdl_wait();     // no global access before the previous kernel on the stream has completed
 #if ADV_KIND == ADV_S
   const real* phi = s;

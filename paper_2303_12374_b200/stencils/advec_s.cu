@@ -33,7 +33,7 @@ KL_ENTRY(real* __restrict__ st, const real* __restrict__ s, const real* __restri
          const real* __restrict__ dzi, const real dxi, const real dyi, const int jj, const int kk, const int istart,
          const int jstart, const int kstart, const int iend, const int jend, const int kend) {
   if (jj != KL_JJ || kk != KL_KK) __trap();
-  kl::pdl_trigger();  // programmatic dependent launch (kl_common.cuh): the next kernel may launch
+  const kl::PdlTriggerAtExit kl_pdl_exit;  // programmatic dependent launch (kl_common.cuh)
   kl::pdl_wait();     // no global access before the previous kernel on the stream has completed
   constexpr long long I1 = 1, J1 = KL_JJ, K1 = KL_KK;
   const real dx60 = dxi * real(1.0 / 60.0), dy60 = dyi * real(1.0 / 60.0);

@@ -72,7 +72,7 @@ KL_ENTRY(real* __restrict__ ut, const real* __restrict__ u, const real* __restri
          const int istart, const int jstart, const int kstart, const int iend, const int jend,
          const int kend) {
   check_pitch<true>(jj, kk);
-  kl::pdl_trigger();  // programmatic dependent launch (kl_common.cuh): the next kernel may launch
+  const kl::PdlTriggerAtExit kl_pdl_exit;  // programmatic dependent launch (kl_common.cuh)
   kl::pdl_wait();     // no global access before the previous kernel on the stream has completed
   const unsigned nbx = kl::ceil_div(iend - istart, BLOCK_X * TILE_X);
   const unsigned nby = kl::ceil_div(jend - jstart, BLOCK_Y * TILE_Y);

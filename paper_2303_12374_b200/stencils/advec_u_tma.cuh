@@ -40,8 +40,8 @@
 #ifndef DEPTH
 #define DEPTH 2
 #endif
-#ifndef KL_YSPLIT
-#define KL_YSPLIT 0  // 0: blocks of kTYT rows; n > 0: n near-equal row runs (entry below)
+#ifndef KL_YBAL
+#define KL_YBAL 0  // 0: blocks of kTYT rows; > 0: near-equal row runs, as many as the grid holds (entry)
 #endif
 
 #include "kl_pack.cuh"
@@ -495,7 +495,7 @@ KL_ENTRY(real* __restrict__ ut, const real* __restrict__ u, const real* __restri
          const int istart, const int jstart, const int kstart, const int iend, const int jend,
          const int kend, const __grid_constant__ KlTmaParams tma) {
   if (jj != KL_JJ || kk != KL_KK) __trap();
-  kl::pdl_trigger();  // programmatic dependent launch (kl_common.cuh): the next kernel may launch
+  const kl::PdlTriggerAtExit kl_pdl_exit;  // programmatic dependent launch (kl_common.cuh)
   kl::pdl_wait();     // no global access before the previous kernel on the stream has completed
   // param-space address of the descriptors (__grid_constant__: no local copy)
   const TmaDesc* const maps = &tma.map[0];
@@ -507,20 +507,20 @@ KL_ENTRY(real* __restrict__ ut, const real* __restrict__ u, const real* __restri
   real* const zprof = ring_v + kNV * kVS;                                     // [ZCHUNK][2]
 
   const unsigned nbx = kl::ceil_div(iend - istart, kXT);
-  const unsigned nby = KL_YSPLIT > 0 ? KL_YSPLIT : kl::ceil_div(jend - jstart, kTYT);
   const unsigned nbz = kl::ceil_div(kend - kstart, ZCHUNK);
+  // rows of this block: tiles of kTYT rows, or (ysplit > 0, KL_YBAL) the y
+  // extent cut into nby near-equal runs of at most kTYT rows, nby taken from
+  // the launched grid — the definition sizes it to whole waves of the SMs
+  // (definitions.YSPLIT_VALUES), whatever jtot / kTYT is
+  const int jt = jend - jstart;
+  const unsigned nby = KL_YBAL > 0 ? gridDim.x / (nbx * nbz) : kl::ceil_div(jt, kTYT);
   int bx, by, bz;
   kl::unravel(blockIdx.x, nbx, nby, nbz, bx, by, bz);
   const int i0 = istart + bx * kXT;
-  // rows of this block: tiles of kTYT rows, or (KL_YSPLIT) the y extent cut
-  // into KL_YSPLIT near-equal runs of at most kTYT rows, so the grid can be
-  // sized to whole waves of the SMs whatever jtot / kTYT is
-  const int jt = jend - jstart;
-  const int j0 = KL_YSPLIT > 0 ? jstart + static_cast<int>((static_cast<long long>(by) * jt) / KL_YSPLIT)
-                               : jstart + by * kTYT;
-  const int jhi = KL_YSPLIT > 0 ? jstart + static_cast<int>((static_cast<long long>(by + 1) * jt) / KL_YSPLIT)
-                                : jend;
-  if (jhi - j0 > kTYT && KL_YSPLIT > 0) __trap();
+  const int j0 = KL_YBAL > 0 ? jstart + static_cast<int>((static_cast<long long>(by) * jt) / nby)
+                             : jstart + by * kTYT;
+  const int jhi = KL_YBAL > 0 ? jstart + static_cast<int>((static_cast<long long>(by + 1) * jt) / nby) : jend;
+  if (KL_YBAL > 0 && jhi - j0 > kTYT) __trap();  // the grid must hold >= ceil(jt / kTYT) row runs
   const int k0 = kstart + bz * ZCHUNK;
   const int k1 = min(k0 + ZCHUNK, kend);
   const int tid = threadIdx.x + threadIdx.y * BLOCK_X;

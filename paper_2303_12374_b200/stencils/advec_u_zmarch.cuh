@@ -33,7 +33,7 @@ KL_ENTRY(real* __restrict__ ut, const real* __restrict__ u, const real* __restri
          const int istart, const int jstart, const int kstart, const int iend, const int jend,
          const int kend) {
   if (jj != KL_JJ || kk != KL_KK) __trap();
-  kl::pdl_trigger();  // programmatic dependent launch (kl_common.cuh): the next kernel may launch
+  const kl::PdlTriggerAtExit kl_pdl_exit;  // programmatic dependent launch (kl_common.cuh)
   kl::pdl_wait();     // no global access before the previous kernel on the stream has completed
   extern __shared__ __align__(16) unsigned char kl_smem_raw[];
   real* const tiles = reinterpret_cast<real*>(kl_smem_raw);  // [2][KL_SH][KL_SW]

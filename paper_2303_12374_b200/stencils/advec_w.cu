@@ -35,7 +35,7 @@ KL_ENTRY(real* __restrict__ wt, const real* __restrict__ u, const real* __restri
          const real dxi, const real dyi, const int jj, const int kk, const int istart, const int jstart,
          const int kstart, const int iend, const int jend, const int kend) {
   if (jj != KL_JJ || kk != KL_KK) __trap();
-  kl::pdl_trigger();  // programmatic dependent launch (kl_common.cuh): the next kernel may launch
+  const kl::PdlTriggerAtExit kl_pdl_exit;  // programmatic dependent launch (kl_common.cuh)
   kl::pdl_wait();     // no global access before the previous kernel on the stream has completed
   constexpr long long I1 = 1, J1 = KL_JJ, K1 = KL_KK;
   const real dx120 = dxi * real(1.0 / 120.0), dy120 = dyi * real(1.0 / 120.0);

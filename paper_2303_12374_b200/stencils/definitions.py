@@ -68,6 +68,13 @@ def base_kernel(kernel: str) -> str:
     return FUSED_KERNELS[kernel][0] if kernel in FUSED_KERNELS else kernel
 
 STAGING_VALUES = ("DIRECT", "ZMARCH", "TMA")
+#: ``ysplit`` (advec_u TMA): 0 = blocks of block_y*tile_y rows; k > 0 = the y
+#: extent cut into near-equal runs of at most block_y*tile_y rows, as many as
+#: make nbx*nby*nbz ~ k blocks per SM of the B200's 148 (a grid of whole
+#: waves whatever jtot / rows-per-block is; advec_u_tma.cuh KL_YBAL)
+YSPLIT_KERNELS = ("advec_u",)
+YSPLIT_VALUES = (0, 1, 2)
+B200_SMS = 148
 DEPTH_VALUES = (0, 1, 2, 3)
 ZCHUNK_VALUES = (1, 8, 16, 32, 64, 128)
 
@@ -275,6 +282,8 @@ def stencil_space(kernel: str = "advec_u", precision: str = "fp32") -> ConfigSpa
         TunableParam("zchunk", ZCHUNK_VALUES, 1),
         TunableParam("depth", DEPTH_VALUES, 0),
     ]
+    if kernel in YSPLIT_KERNELS:
+        params.append(TunableParam("ysplit", YSPLIT_VALUES, 0))
     restrictions = [
         BLOCK_LIMIT_RESTRICTION,
         'staging != "DIRECT" || zchunk == 1',
@@ -289,6 +298,8 @@ def stencil_space(kernel: str = "advec_u", precision: str = "fp32") -> ConfigSpa
         (f'staging != "ZMARCH" || ({_ZMARCH_PLANE_LIMIT[kernel]})' if kernel == "diff_uvw" else
          f'staging == "DIRECT" || ({_ZMARCH_PLANE_LIMIT[kernel]})'),
     ] + [r.replace("{SMEM_TMA}", _SMEM_TMA[kernel].format(S=size)) for r in _TMA_LIMIT.get(kernel, [])]
+    if kernel in YSPLIT_KERNELS:
+        restrictions.append('ysplit == 0 || staging == "TMA"')
     return ConfigSpace(params, restrictions)
 
 
@@ -405,6 +416,10 @@ def _definition(kernel: str, precision: str) -> KernelDefinition:
         "ceil_div(problem_x, block_x * tile_x) * ceil_div(problem_y, block_y * tile_y) * "
         "ceil_div(problem_z, block_z * tile_z * zchunk)"
     )
+    if kernel in YSPLIT_KERNELS:
+        nbxz = "(ceil_div(problem_x, block_x * tile_x) * ceil_div(problem_z, block_z * tile_z * zchunk))"
+        grid_x = (f"{nbxz} * max(ceil_div(problem_y, block_y * tile_y), "
+                  f"min(ysplit, 1) * (({B200_SMS} * ysplit) / {nbxz}))")
     defines = [
         ("BLOCK_X", "block_x"), ("BLOCK_Y", "block_y"), ("BLOCK_Z", "block_z"),
         ("TILE_X", "tile_x"), ("TILE_Y", "tile_y"), ("TILE_Z", "tile_z"),
@@ -413,7 +428,7 @@ def _definition(kernel: str, precision: str) -> KernelDefinition:
         ("UNRAVEL", "unravel"), ("MIN_BLOCKS", "min_blocks"),
         ("STAGING", "staging"), ("ZCHUNK", "zchunk"), ("DEPTH", "depth"),
         ("KL_JJ", p("jj")), ("KL_KK", p("kk")),
-    ]
+    ] + ([("KL_YBAL", "ysplit")] if kernel in YSPLIT_KERNELS else [])
     return KernelDefinition(
         f"{kernel}_{precision}",
         space,

@@ -65,7 +65,7 @@ KL_ENTRY(real* __restrict__ st, const real* __restrict__ s, const real* __restri
          const int kk, const int istart, const int jstart, const int kstart, const int iend, const int jend,
          const int kend) {
   if (jj != KL_JJ || kk != KL_KK) __trap();
-  kl::pdl_trigger();  // programmatic dependent launch (kl_common.cuh): the next kernel may launch
+  const kl::PdlTriggerAtExit kl_pdl_exit;  // programmatic dependent launch (kl_common.cuh)
   kl::pdl_wait();     // no global access before the previous kernel on the stream has completed
   const DiffC tr = make_traits(dzi, dzhi, rhoref, rhorefh, dxi, dyi, tpri);
   kl::direct_tiles(istart, jstart, kstart, iend, jend, kend, [&](int k) { return tr.plane(k); },
@@ -91,7 +91,7 @@ KL_ENTRY(real* __restrict__ st, const real* __restrict__ s, const real* __restri
          const int kk, const int istart, const int jstart, const int kstart, const int iend, const int jend,
          const int kend, const __grid_constant__ KlTmaParams tma) {
   if (jj != KL_JJ || kk != KL_KK) __trap();
-  kl::pdl_trigger();  // programmatic dependent launch (kl_common.cuh): the next kernel may launch
+  const kl::PdlTriggerAtExit kl_pdl_exit;  // programmatic dependent launch (kl_common.cuh)
   kl::pdl_wait();     // no global access before the previous kernel on the stream has completed
   const DiffC tr = make_traits(dzi, dzhi, rhoref, rhorefh, dxi, dyi, tpri);
   const real* const hp[2] = {s, evisc};

@@ -595,7 +595,7 @@ KL_ENTRY(real* __restrict__ ut, real* __restrict__ vt, real* __restrict__ wt, co
          const int jj, const int kk, const int istart, const int jstart, const int kstart, const int iend,
          const int jend, const int kend, const __grid_constant__ KlTmaParams tma) {
   if (jj != KL_JJ || kk != KL_KK) __trap();
-  kl::pdl_trigger();  // programmatic dependent launch (kl_common.cuh): the next kernel may launch
+  const kl::PdlTriggerAtExit kl_pdl_exit;  // programmatic dependent launch (kl_common.cuh)
   kl::pdl_wait();     // no global access before the previous kernel on the stream has completed
   extern __shared__ __align__(128) unsigned char kl_smem_raw[];
   unsigned char* base = kl_smem_raw + ((128u - (kl::smem_u32(kl_smem_raw) & 127u)) & 127u);

@@ -59,12 +59,18 @@ namespace kl {
 // kernel launched with the attribute may be scheduled while the previous
 // kernel on the stream drains.  pdl_wait() blocks until that kernel has
 // completed and its writes are visible — every stencil calls it before its
-// first global read (after its shared-memory/mbarrier setup, which thereby
-// overlaps the previous kernel's tail); pdl_trigger() after a block's last
-// global read lets the next kernel start launching.  Both are no-ops for a
+// first global read; pdl_trigger() as a block leaves (PdlTriggerAtExit)
+// lets the next kernel's blocks launch into the slots this grid's finishing
+// blocks free, before the grid's completion is signalled.  Both are no-ops for a
 // kernel launched without the attribute.
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+// Triggers when the block leaves the kernel (every return path): triggering
+// at entry let the next kernel's blocks occupy SM slots while this grid still
+// had blocks to schedule — measured slower (bench ``graph`` rows, r02f).
+struct PdlTriggerAtExit {
+  __device__ __forceinline__ ~PdlTriggerAtExit() { pdl_trigger(); }
+};
 
 // 1-D block id -> 3-D block coordinates; the first letter of UNRAVEL is the
 // fastest-varying axis (PAPER.md: "for (Z,X,Y) ... first along Z, then X, then Y").

@@ -19,7 +19,7 @@ KL_ENTRY(real* __restrict__ ut, real* __restrict__ vt, real* __restrict__ wt, re
          real* __restrict__ v, real* __restrict__ w, const real rk_a, const real rk_bdt, const int jj, const int kk,
          const int istart, const int jstart, const int kstart, const int iend, const int jend, const int kend) {
   if (jj != KL_JJ || kk != KL_KK) __trap();
-  kl::pdl_trigger();  // programmatic dependent launch (kl_common.cuh): the next kernel may launch
+  const kl::PdlTriggerAtExit kl_pdl_exit;  // programmatic dependent launch (kl_common.cuh)
   kl::pdl_wait();     // no global access before the previous kernel on the stream has completed
   kl::direct_tiles(
       istart, jstart, kstart, iend, jend, kend, [](int) { return 0; },

@@ -106,11 +106,12 @@ def test_nccl_single_rank_exchange_is_a_noop(gpu_ctx):
     assert ver.value >= 22700
 
 
-@pytest.mark.parametrize("kernel", ["advec_u", "diff_uvw"])
-def test_host_streamed_step_matches_device_step(gpu_ctx, tmp_path, kernel):
+@pytest.mark.parametrize("kernel,copy_streams", [("advec_u", 1), ("diff_uvw", 1), ("diff_uvw", 2), ("advec_u", 3)])
+def test_host_streamed_step_matches_device_step(gpu_ctx, tmp_path, kernel, copy_streams):
     """SlabDriver.step_host (fields in pinned host memory, chunked H2D |
-    launch | D2H on three streams) returns the same tendencies as step() on
-    device-resident fields, and leaves the host inputs untouched."""
+    launch | D2H on overlapped streams, one or several copy streams per
+    direction) returns the same tendencies as step() on device-resident
+    fields, and leaves the host inputs untouched."""
     from paper_2303_12374_b200.cuda import HostPinned, NvrtcCompiler
     from paper_2303_12374_b200.cuda._abi import check, lib
     from paper_2303_12374_b200.slab import SlabDriver
@@ -139,7 +140,7 @@ def test_host_streamed_step_matches_device_step(gpu_ctx, tmp_path, kernel):
     for n, arr in prob.fields.items():
         check(lib().klb_memset_d8(arr.ptr, 0xFF, nbytes, None))
     gpu_ctx.synchronize()
-    launches = drv.step_host({n: b.ptr for n, b in host.items()}, chunks=5)
+    launches = drv.step_host({n: b.ptr for n, b in host.items()}, chunks=5, copy_streams=copy_streams)
     drv.compute.synchronize()
     assert launches == 5
     h2d, d2h = drv.stream_bytes

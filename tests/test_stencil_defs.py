@@ -168,3 +168,29 @@ def test_capture_metadata_with_embedded_source_fits_the_format_cap(kernel):
         descs = [(i, "input", "f32", 1, 4, 0) for i in range(14)]
         blob = metadata_block(d, (1024, 1024, 1024), [ScalarArg(20, "i32", 1)] * 12, descs, "app", "t")
         assert len(blob) < 60 * 1024, len(blob)
+
+
+def test_advec_u_ysplit_sizes_the_grid_to_whole_waves():
+    """advec_u's ``ysplit`` knob (TMA only): the grid holds ~ysplit blocks per
+    SM of the B200 (148), never fewer row runs than ceil(jtot / rows per
+    block) (the kernel traps otherwise), and 0 keeps the natural tiling."""
+    from paper_2303_12374_b200.stencils.definitions import B200_SMS, definition_for
+    from paper_2303_12374_b200.stencils.layout import GridLayout
+
+    d = definition_for("advec_u", "fp32")
+    lay = GridLayout(256, 256, 256, "fp32")
+    env = {"arg9": lay.jj, "arg10": lay.kk}
+    base = dict(d.space.default_config()[0], staging="TMA", block_x=32, block_y=8, tile_x=4, tile_y=1,
+                contiguous_x=True, zchunk=64, depth=2)
+    grids = {}
+    for ys in (0, 1, 2):
+        cfg = dict(base, ysplit=ys)
+        assert d.space.is_valid(cfg), ys
+        grids[ys] = d.derive_geometry(cfg, (256, 256, 256), env).grid[0]
+        req = d.render_compile_request(cfg, (256, 256, 256), env)
+        assert f"-D KL_YBAL={ys}" in req.defines
+    nbxz = 2 * 4
+    assert grids[0] == nbxz * 32                      # 256 rows / 8 per block
+    assert grids[1] == nbxz * 32                      # 148 / 8 = 18 runs < 32 needed: natural count kept
+    assert grids[2] == nbxz * (2 * B200_SMS // nbxz) == 296  # 37 runs of <= 7 rows, 2 blocks per SM
+    assert not d.space.is_valid(dict(d.space.default_config()[0], ysplit=1))  # DIRECT: pinned to 0

@@ -1,5 +1,5 @@
-"""Probe the balanced y split (KL_YSPLIT) of a TMA kernel: compile the given
-configurations with -D KL_YSPLIT=n, launch nbx*n*nbz blocks, verify against
+"""Probe the balanced y split (KL_YBAL, n row runs) of a TMA kernel: compile the given
+configurations with -D KL_YBAL=1, launch nbx*n*nbz blocks, verify against
 the default configuration's output and time (L2 flushed).  GPU only.
 
     python tools/ysplit_probe.py --kernel advec_u --precision fp32 --grid 256,256,256 \
@@ -56,7 +56,9 @@ def main(argv=None) -> int:
         if True:
             req = d.render_compile_request(cfg, ex.problem, ex.scalar_env)
             if n:
-                req = CompileRequest(req.source, req.entry, req.defines + (f"-D KL_YSPLIT={n}",), req.flags)
+                req = CompileRequest(req.source, req.entry,
+                                     tuple(x for x in req.defines if not x.startswith("-D KL_YBAL=")) +
+                                     ("-D KL_YBAL=1",), req.flags)
             geom = d.derive_geometry(cfg, ex.problem, ex.scalar_env)
             if n:
                 txy = cfg["block_x"] * cfg["tile_x"]
