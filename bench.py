@@ -460,9 +460,11 @@ def ncu_traffic(kernel_key_prefix):
     return None, None
 
 
-def suite_measure(ctx, compiler, wisdom_dir, peak, suite=SUITE):
+def suite_measure(ctx, compiler, wisdom_dir, peak, suite=SUITE, cpu=False):
     """BASELINE configs 1-3 (+ the north_star 512^3 fp32 pair) on one GPU:
-    tuned (wisdom) vs default, L2 flushed per rep."""
+    tuned (wisdom) vs default, L2 flushed per rep; with ``cpu`` also the C
+    restatement of the path on the whole grid on all host threads (advec_u /
+    diff_uvw rows; median of 3 steps, 1 at >= 512^3)."""
     from paper_2303_12374_b200.capture import CapturePolicy
     from paper_2303_12374_b200.dispatch import WisdomKernel
     from paper_2303_12374_b200.stencils.layout import GridLayout
@@ -487,6 +489,17 @@ def suite_measure(ctx, compiler, wisdom_dir, peak, suite=SUITE):
             row[variant] = {"us": round(t * 1e6, 2), "gcells": round(lay.cells / t / 1e9, 2), "gbs": round(gbs, 1),
                             "frac": round(gbs / peak, 4), "match_kind": kind}
         prob.close()
+        if cpu and kernel in ("advec_u", "diff_uvw"):
+            try:
+                threads = host_threads()
+                oracle = CpuOracle(kernel, precision, grid, threads, full=True)
+                oracle.step()
+                rate, secs_cpu = oracle.rate(reps=1 if lay.cells >= 512 ** 3 else 3)
+                oracle.close()
+                row["cpu"] = {"gcells": round(rate, 5), "cores": threads, "kind": "port",
+                              "sample": f"whole grid; {oracle.kind}; step {secs_cpu:.4f} s"}
+            except Exception as err:  # report, never hide
+                row["cpu"] = {"error": repr(err)[:200]}
         rows.append(row)
     return rows
 
@@ -675,7 +688,7 @@ def run_ours(args, dist):
                       f"threads; median of 3 ({secs:.3f} s each)"}
     if dist.rank == 0 and dist.world == 1 and args.suite:
         try:
-            line["suite"] = suite_measure(ctx, compiler, wisdom_dir, peak)
+            line["suite"] = suite_measure(ctx, compiler, wisdom_dir, peak, cpu=not args.no_cpu_baseline)
         except Exception as err:
             line["suite"] = {"error": repr(err)[:300]}
         try:
