@@ -418,8 +418,10 @@ def _definition(kernel: str, precision: str) -> KernelDefinition:
     )
     if kernel in YSPLIT_KERNELS:
         nbxz = "(ceil_div(problem_x, block_x * tile_x) * ceil_div(problem_z, block_z * tile_z * zchunk))"
+        # at least the natural count (<= block_y*tile_y rows per run), at most
+        # problem_y runs (every run holds a row)
         grid_x = (f"{nbxz} * max(ceil_div(problem_y, block_y * tile_y), "
-                  f"min(ysplit, 1) * (({B200_SMS} * ysplit) / {nbxz}))")
+                  f"min(ysplit, 1) * min(problem_y, ({B200_SMS} * ysplit) / {nbxz}))")
     defines = [
         ("BLOCK_X", "block_x"), ("BLOCK_Y", "block_y"), ("BLOCK_Z", "block_z"),
         ("TILE_X", "tile_x"), ("TILE_Y", "tile_y"), ("TILE_Z", "tile_z"),

@@ -161,6 +161,31 @@ def test_advec_tma_column_tiles_match_oracle(gpu_ctx, compiler, precision):
 
 
 @pytest.mark.parametrize("precision", ["fp32", "fp64"])
+def test_advec_tma_balanced_row_runs_match_oracle(gpu_ctx, compiler, precision):
+    """advec_u TMA with ``ysplit`` > 0: the y extent cut into near-equal row
+    runs (grid sized to whole waves, definitions.YSPLIT_VALUES) — runs shorter
+    than the block's rows, strips past a run's end idle — on ragged grids and
+    on a k sub-range (the planes outside it untouched)."""
+    from paper_2303_12374_b200.stencils.definitions import definition_for
+    from paper_2303_12374_b200.stencils.layout import GridLayout
+
+    space = definition_for("advec_u", precision).space
+    base = _default("advec_u", precision)
+    cases = [dict(block_x=32, block_y=4, tile_x=2, tile_y=2, depth=2, zchunk=16, ysplit=1),
+             dict(block_x=16, block_y=4, tile_x=4, tile_y=2, depth=2, zchunk=8, ysplit=2),
+             dict(block_x=32, block_y=8, tile_x=4, tile_y=1, depth=1, zchunk=32, ysplit=2)]
+    for grid, k_range in (((45, 23, 19), None), ((130, 37, 41), None), ((96, 61, 30), (5, 27))):
+        lay = GridLayout(*grid, precision)
+        ref, _ = oracle_outputs("advec_u", lay, k_range=k_range)
+        for case in cases:
+            cfg = dict(base, staging="TMA", contiguous_x=True, **case)
+            assert space.is_valid(cfg), case
+            got = run_config(gpu_ctx, compiler, "advec_u", lay, cfg, k_range=k_range)
+            err = rel_error(got["ut"], ref["ut"], lay)
+            assert err <= TOL[precision], (grid, case, err)
+
+
+@pytest.mark.parametrize("precision", ["fp32", "fp64"])
 def test_diff_tma_column_tiles_match_oracle(gpu_ctx, compiler, precision):
     """diff_uvw TMA with tile_x consecutive columns per thread (x-face reuse,
     vectorised shared-memory reads and tendency stores), on grids whose x/y

@@ -194,3 +194,16 @@ def test_advec_u_ysplit_sizes_the_grid_to_whole_waves():
     assert grids[1] == nbxz * 32                      # 148 / 8 = 18 runs < 32 needed: natural count kept
     assert grids[2] == nbxz * (2 * B200_SMS // nbxz) == 296  # 37 runs of <= 7 rows, 2 blocks per SM
     assert not d.space.is_valid(dict(d.space.default_config()[0], ysplit=1))  # DIRECT: pinned to 0
+
+
+def test_advec_u_ysplit_never_makes_empty_row_runs():
+    from paper_2303_12374_b200.stencils.definitions import definition_for
+    from paper_2303_12374_b200.stencils.layout import GridLayout
+
+    d = definition_for("advec_u", "fp32")
+    lay = GridLayout(45, 23, 19, "fp32")
+    env = {"arg9": lay.jj, "arg10": lay.kk}
+    cfg = dict(d.space.default_config()[0], staging="TMA", block_x=32, block_y=4, tile_x=2, tile_y=2,
+               contiguous_x=True, zchunk=8, depth=2, ysplit=2)
+    g = d.derive_geometry(cfg, (45, 23, 19), env).grid[0]
+    assert g == 1 * 3 * 23  # nbx * nbz * min(jtot, 296 / 3): one row per run, none empty
