@@ -587,9 +587,17 @@ def run_ours(args, dist):
     peak, peak_src = peaks()
     exchanger, transport = None, None
     if dist.world > 1:
-        # ipc (default): neighbours map each other's fields (CUDA IPC) and pull
-        # halo planes over NVLink with copy engines; nccl: ncclSend/ncclRecv
-        transport = os.environ.get("KL_HALO_TRANSPORT", "ipc")
+        # ipc: neighbours map each other's fields (CUDA IPC) and pull halo
+        # planes over NVLink with copy engines; nccl: ncclSend/ncclRecv;
+        # auto (default): ipc if every rank's probe succeeds, else nccl
+        transport = os.environ.get("KL_HALO_TRANSPORT", "auto")
+        if transport == "auto":
+            # peer memory when every rank can map its neighbours (agreed over
+            # the group), else NCCL for the whole job
+            ok, why = IpcExchanger.probe(dist.group)
+            transport = "ipc" if ok else "nccl"
+            if not ok and dist.rank == 0:
+                print(f"klb: IPC transport unavailable ({why}); using NCCL", file=sys.stderr, flush=True)
         if transport == "nccl":
             uid = dist.broadcast_bytes(NcclExchanger.unique_id() if dist.rank == 0 else None, 128)
             exchanger = NcclExchanger(dist.rank, dist.world, uid)

@@ -190,6 +190,64 @@ class IpcExchanger:
         self._maps: dict[tuple, dict] = {}  # local pointer tuple -> peer mappings
         self._opened: list[int] = []
 
+    @staticmethod
+    def probe(group) -> tuple[bool, str]:
+        """Collective: can every rank map its neighbours' device memory and
+        open their interprocess events?  Each rank exports a small buffer and
+        an event, opens its neighbours', copies one value from each, and the
+        outcome is agreed over the group (every rank returns the same
+        ``(ok, reason)``), so a job falls back to another transport as a whole."""
+        import struct
+
+        from .cuda._abi import KlbError, check, lib
+        from .cuda.device import DeviceArray
+
+        buf = DeviceArray(256)
+        mark = struct.pack("<Q", 0x6B6C62000000 + group.rank)
+        ev = C.c_void_p()
+        opened, peer_events, why = [], [], ""
+        try:
+            check(lib().klb_memcpy_htod(buf.ptr, mark, 8, None))
+            check(lib().klb_device_synchronize())
+            h, off, eh = (C.c_ubyte * 64)(), C.c_uint64(), (C.c_ubyte * 64)()
+            check(lib().klb_ipc_mem_handle(buf.ptr, h, C.byref(off)))
+            check(lib().klb_ipc_event_create(C.byref(ev), eh))
+            blob = bytes(h) + struct.pack("<Q", off.value) + bytes(eh)
+        except KlbError as err:
+            blob, why = b"\0" * 136, f"rank {group.rank}: export failed: {err}"
+        peers = group.allgather(blob)
+        ok = not why
+        for r in (group.rank - 1, group.rank + 1):
+            if not ok or not 0 <= r < group.nranks:
+                continue
+            try:
+                base = C.c_uint64()
+                check(lib().klb_ipc_mem_open((C.c_ubyte * 64).from_buffer_copy(peers[r][:64]), C.byref(base)))
+                opened.append(base.value)
+                off_r, = struct.unpack_from("<Q", peers[r], 64)
+                got = C.create_string_buffer(8)
+                check(lib().klb_memcpy_dtoh(got, base.value + off_r, 8, None))
+                check(lib().klb_device_synchronize())
+                if got.raw != struct.pack("<Q", 0x6B6C62000000 + r):
+                    raise KlbError(-1, "peer value mismatch")
+                pe = C.c_void_p()
+                check(lib().klb_ipc_event_open((C.c_ubyte * 64).from_buffer_copy(peers[r][72:136]), C.byref(pe)))
+                peer_events.append(pe.value)
+            except KlbError as err:
+                ok, why = False, f"rank {group.rank}: peer {r}: {err}"
+        verdict = group.allgather(struct.pack("<?", ok) + why.encode()[:200].ljust(200, b"\0"))
+        group.barrier()  # every peer finished reading before anything is unmapped / freed
+        for base in opened:
+            lib().klb_ipc_mem_close(base)
+        for pe in peer_events:
+            lib().klb_event_destroy(pe)
+        if ev.value:
+            lib().klb_event_destroy(ev.value)
+        group.barrier()
+        buf.free()
+        bad = [v[1:].rstrip(b"\0").decode(errors="replace") for v in verdict if not v[0]]
+        return (not bad), "; ".join(bad)
+
     def _attach(self, ptrs, kstart: int, kend: int) -> dict:
         """Collective on first use of a field set: map the neighbours' fields."""
         import struct

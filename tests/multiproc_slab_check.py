@@ -49,10 +49,15 @@ def main() -> int:
     from paper_2303_12374_b200.stencils.layout import GridLayout
     from stencil_helpers import oracle_outputs
 
-    kernel, precision, grid = sys.argv[1], sys.argv[2], tuple(int(x) for x in sys.argv[3].split(","))
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     group = ProcessGroup(rank, world, timeout=300)
     ctx = open_device(int(os.environ.get("KL_DEVICE_ORDINAL", os.environ.get("LOCAL_RANK", "0"))))
+    if sys.argv[1] == "probe":  # the collective transport probe bench.py runs before choosing IPC
+        ok, why = IpcExchanger.probe(group)
+        group.close()
+        print(f"rank {rank} {'ok' if ok else 'FAIL'} probe {why}", flush=True)
+        return 0 if ok else 1
+    kernel, precision, grid = sys.argv[1], sys.argv[2], tuple(int(x) for x in sys.argv[3].split(","))
     if os.environ.get("KL_HALO_TRANSPORT", "ipc") == "nccl":
         uid = group.broadcast(NcclExchanger.unique_id() if rank == 0 else None, size=128)
         ex = NcclExchanger(rank, world, uid)

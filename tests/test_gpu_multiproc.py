@@ -73,6 +73,15 @@ def test_spawned_ranks_without_torch_match_oracle(kernel, precision, grid, nproc
     assert len(re.findall(r"rank \d+ ok ", out)) == nproc and "FAIL" not in out, out
 
 
+def test_ipc_probe_agrees_across_ranks():
+    """IpcExchanger.probe: every rank maps its neighbours' memory, reads a
+    marker value through the mapping and opens their interprocess events —
+    the check bench.py runs (KL_HALO_TRANSPORT=auto) before choosing IPC."""
+    codes, out, err = _spawn(3, "tests/multiproc_slab_check.py", "probe")
+    assert codes == [0, 0, 0], out[-2000:] + err[-3000:]
+    assert len(re.findall(r"rank \d ok probe", out)) == 3, out
+
+
 def _lines(stdout):
     return [json.loads(x) for x in stdout.splitlines() if x.startswith("{")]
 
