@@ -68,6 +68,11 @@ def base_kernel(kernel: str) -> str:
     return FUSED_KERNELS[kernel][0] if kernel in FUSED_KERNELS else kernel
 
 STAGING_VALUES = ("DIRECT", "ZMARCH", "TMA")
+#: ``xshare`` (evisc_smag TMA, tile_x == 1): lane 31 of each warp evaluates
+#: only the west-face edges of the next column and every lane takes its east
+#: edges from its right neighbour by shuffle — 31 output columns per warp
+#: (evisc_smag_tma.cuh KL_XSHARE)
+XSHARE_KERNELS = ("evisc_smag",)
 #: ``ysplit`` (advec_u TMA): 0 = blocks of block_y*tile_y rows; k > 0 = the y
 #: extent cut into near-equal runs of at most block_y*tile_y rows, as many as
 #: make nbx*nby*nbz ~ k blocks per SM of the B200's 148 (a grid of whole
@@ -263,7 +268,7 @@ def stencil_space(kernel: str = "advec_u", precision: str = "fp32") -> ConfigSpa
             TunableParam("zchunk", ZCHUNK_VALUES, 1),
             TunableParam("depth", DEPTH_VALUES, 0),
         ]
-        return ConfigSpace(params, [
+        restrictions = [
             BLOCK_LIMIT_RESTRICTION,
             'staging != "DIRECT" || (zchunk == 1 && depth == 0)',
             'staging != "TMA" || (zchunk > 1 && depth > 0 && block_z == 1 && tile_z == 1 && !unroll_x && '
@@ -271,7 +276,11 @@ def stencil_space(kernel: str = "advec_u", precision: str = "fp32") -> ConfigSpa
             '((tile_x == 1 && !contiguous_x) || (tile_x > 1 && contiguous_x)) && '
             'block_x * block_y >= 32 && block_x * tile_x <= 128 && '
             + _plane_family_smem(kernel).format(S=size) + f" <= {SMEM_OPTIN_BYTES})",
-        ])
+        ]
+        if kernel in XSHARE_KERNELS:
+            params.append(TunableParam("xshare", (0, 1), 0))
+            restrictions.append('xshare == 0 || (staging == "TMA" && tile_x == 1 && block_x >= 32)')
+        return ConfigSpace(params, restrictions)
     if kernel in FAMILY_KERNELS:
         # DIRECT staging only: the B200 knobs are pinned, the Table-2 space is the search space
         params = table2_params() + [TunableParam("staging", ("DIRECT",), "DIRECT"),
@@ -416,6 +425,9 @@ def _definition(kernel: str, precision: str) -> KernelDefinition:
         "ceil_div(problem_x, block_x * tile_x) * ceil_div(problem_y, block_y * tile_y) * "
         "ceil_div(problem_z, block_z * tile_z * zchunk)"
     )
+    if kernel in XSHARE_KERNELS:
+        grid_x = grid_x.replace("ceil_div(problem_x, block_x * tile_x)",
+                                "ceil_div(problem_x, block_x * tile_x - xshare * (block_x / 32))")
     if kernel in YSPLIT_KERNELS:
         nbxz = "(ceil_div(problem_x, block_x * tile_x) * ceil_div(problem_z, block_z * tile_z * zchunk))"
         # at least the natural count (<= block_y*tile_y rows per run), at most
@@ -430,7 +442,8 @@ def _definition(kernel: str, precision: str) -> KernelDefinition:
         ("UNRAVEL", "unravel"), ("MIN_BLOCKS", "min_blocks"),
         ("STAGING", "staging"), ("ZCHUNK", "zchunk"), ("DEPTH", "depth"),
         ("KL_JJ", p("jj")), ("KL_KK", p("kk")),
-    ] + ([("KL_YBAL", "ysplit")] if kernel in YSPLIT_KERNELS else [])
+    ] + ([("KL_YBAL", "ysplit")] if kernel in YSPLIT_KERNELS else []) + (
+        [("KL_XSHARE", "xshare")] if kernel in XSHARE_KERNELS else [])
     return KernelDefinition(
         f"{kernel}_{precision}",
         space,

@@ -26,6 +26,12 @@
 #ifndef DEPTH
 #define DEPTH 2
 #endif
+#ifndef KL_XSHARE
+#define KL_XSHARE 0
+#endif
+#if KL_XSHARE && (TILE_X != 1 || BLOCK_X % 32 != 0)
+#error "evisc_smag x-edge sharing needs TILE_X == 1 and whole warps along x"
+#endif
 
 #include "kl_pack.cuh"
 #include "kl_tma.cuh"
@@ -34,7 +40,13 @@ namespace {
 constexpr int kS = static_cast<int>(sizeof(real));
 constexpr int kE = 16 / kS;
 constexpr int kTX = TILE_X, kTY = TILE_Y;
-constexpr int kXT = BLOCK_X * kTX;
+// KL_XSHARE (xshare knob): lane 31 of every warp is a helper that evaluates
+// only the west-face edges of the column after the warp's 31 output columns;
+// every lane's east-face edges are its right neighbour's west-face edges (a
+// shuffle) instead of a second evaluation — 32 edge evaluations per 31
+// columns instead of 62 along x.
+constexpr bool kXS = KL_XSHARE != 0;
+constexpr int kXT = kXS ? BLOCK_X / 32 * 31 : BLOCK_X * kTX;  // output columns per block
 constexpr int kTYT = BLOCK_Y * kTY;
 __host__ __device__ constexpr int rup(int a, int b) { return (a + b - 1) / b * b; }
 constexpr int kBW = rup(kXT + 2 + kE - 1, kE);  // columns i0-1 .. i0+kXT (start rounded down to 16 B)
@@ -119,6 +131,7 @@ struct EviscTma {
   const TmaDesc* maps;
   real dxi, dyi, cs;
   int j0, k0, k1, tid, iend, jend, ic, lj0;
+  bool helper;  // KL_XSHARE: lane 31 evaluates edges only, stores nothing
   int xh[3], hof[3];  // per-field box starts / (strip row 0, column ic) offsets in a slot
 
   __device__ __forceinline__ void issue(int slot, int p) const {
@@ -138,11 +151,12 @@ struct EviscTma {
     for (int t = 0; t < kTY; ++t) {
       real ex[kTX + 1];
 #pragma unroll
-      for (int a = 0; a <= kTX; ++a) {
+      for (int a = 0; a <= (kXS ? 0 : kTX); ++a) {
         const int o = t * kBW + a;
         const real s = (uh[o] - ul[o]) * dzh1 + (wh[o] - wh[o - 1]) * dxi;
         ex[a] = s * s;
       }
+      if constexpr (kXS) ex[1] = __shfl_down_sync(0xffffffffu, ex[0], 1);  // the right neighbour's west edge
 #pragma unroll
       for (int c = 0; c < kTX; ++c) out.xz[t][c] = ex[c] + ex[c + 1];
     }
@@ -306,6 +320,9 @@ struct EviscTma {
       top_faces(pk, pk1, dzh1, top);
 
       const real *u = pk + hof[0], *v = pk + hof[1], *w = pk + hof[2], *w1 = pk1 + hof[2];
+      // east u of each cell; the helper lane (no output, computes along with
+      // its warp) reads its own column so the last warp's stays in the box
+      const real* ue = u + ((kXS && helper) ? 0 : 1);
       // xy edges at the tile's corners (rows t = 0..kTY, columns a = 0..kTX), x-pair sums
       //   edge (i-1/2+a, j-1/2+t): (u[i+a,j+t]-u[i+a,j+t-1]) dyi + (v[i+a,j+t]-v[i+a-1,j+t]) dxi
       real pxy[kTY + 1][kTX];
@@ -313,14 +330,16 @@ struct EviscTma {
       for (int t = 0; t <= kTY; ++t) {
         real e[kTX + 1];
 #pragma unroll
-        for (int a = 0; a <= kTX; ++a) {
+        for (int a = 0; a <= (kXS ? 0 : kTX); ++a) {
           const int o = t * kBW + a;
           const real s = (u[o] - u[o - kBW]) * dyi + (v[o] - v[o - 1]) * dxi;
           e[a] = s * s;
         }
+        if constexpr (kXS) e[1] = __shfl_down_sync(0xffffffffu, e[0], 1);
 #pragma unroll
         for (int c = 0; c < kTX; ++c) pxy[t][c] = e[c] + e[c + 1];
       }
+
       real* const orow = evisc + ic + static_cast<long long>(j0 + lj0) * KL_JJ + static_cast<long long>(k) * KL_KK;
 #pragma unroll
       for (int t = 0; t < kTY; ++t) {
@@ -328,12 +347,12 @@ struct EviscTma {
 #pragma unroll
         for (int c = 0; c < kTX; ++c) {
           const int o = t * kBW + c;
-          const real dx = (u[o + 1] - u[o]) * dxi, dy = (v[o + kBW] - v[o]) * dyi, dzz = (w1[o] - w[o]) * dz;
+          const real dx = (ue[o] - u[o]) * dxi, dy = (v[o + kBW] - v[o]) * dyi, dzz = (w1[o] - w[o]) * dz;
           const real diag = dx * dx + dy * dy + dzz * dzz;
           const real off = (pxy[t][c] + pxy[t + 1][c]) + (bot.xz[t][c] + top.xz[t][c]) + (bot.yz[t][c] + top.yz[t][c]);
           out[c] = fac * kl::sqrt_fast(real(2) * diag + real(0.25) * off);
         }
-        if (j0 + lj0 + t < jend) {
+        if (j0 + lj0 + t < jend && !(kXS && helper)) {
           real* dst = orow + t * KL_JJ;
           if (VEC && ic + kTX <= iend) {
             constexpr int VA = kTX < kE ? kTX : kE;
@@ -414,7 +433,11 @@ KL_ENTRY(real* __restrict__ evisc, const real* __restrict__ u, const real* __res
   m.iend = iend;
   m.jend = jend;
   m.lj0 = threadIdx.y * kTY;
-  const int cx = kTX * static_cast<int>(threadIdx.x);
+  // column of this thread within the block: kTX per thread, or (KL_XSHARE)
+  // 31 per warp with lane 31 on the next warp's first column (the helper)
+  const int lane = static_cast<int>(threadIdx.x) & 31;
+  const int cx = kXS ? static_cast<int>(threadIdx.x) / 32 * 31 + lane : kTX * static_cast<int>(threadIdx.x);
+  m.helper = kXS && lane == 31;
   m.ic = i0 + cx;
   const real* const hp[3] = {u, v, w};
 #pragma unroll

@@ -190,3 +190,27 @@ def test_family_tma_plane_march_matches_oracle(gpu_ctx, compiler, kernel, precis
             for name in ref:
                 err = rel_error(got[name], ref[name], lay)
                 assert err <= TOL[precision], (grid, cfg, name, err)
+
+
+@pytest.mark.parametrize("precision", ["fp32", "fp64"])
+def test_evisc_tma_shared_x_edges_match_oracle(gpu_ctx, compiler, precision):
+    """evisc_smag TMA with ``xshare``: 31 output columns per warp, lane 31 a
+    helper whose west-face edges are its neighbours' east-face edges (warp
+    shuffles) — block widths 32..128 on ragged grids (partial warps and
+    blocks along x), a k sub-range, and the scalar store path."""
+    from paper_2303_12374_b200.stencils.layout import GridLayout
+
+    space = _space("evisc_smag", precision)
+    base = space.default_config()[0]
+    cases = [dict(block_x=32, block_y=4, tile_y=2, depth=2, zchunk=16),
+             dict(block_x=64, block_y=2, tile_y=4, depth=1, zchunk=8, unravel="XYZ"),
+             dict(block_x=128, block_y=2, tile_y=4, depth=2, zchunk=32, unravel="XYZ")]
+    for grid, k_range in (((45, 23, 19), None), ((130, 37, 41), None), ((200, 30, 24), (6, 21))):
+        lay = GridLayout(*grid, precision)
+        ref, _ = oracle_outputs("evisc_smag", lay, k_range=k_range)
+        for case in cases:
+            cfg = dict(base, staging="TMA", tile_x=1, xshare=1, **case)
+            assert space.is_valid(cfg), case
+            got = run_config(gpu_ctx, compiler, "evisc_smag", lay, cfg, k_range=k_range)
+            err = rel_error(got["evisc"], ref["evisc"], lay)
+            assert err <= TOL[precision], (grid, case, err)

@@ -207,3 +207,19 @@ def test_advec_u_ysplit_never_makes_empty_row_runs():
                contiguous_x=True, zchunk=8, depth=2, ysplit=2)
     g = d.derive_geometry(cfg, (45, 23, 19), env).grid[0]
     assert g == 1 * 3 * 23  # nbx * nbz * min(jtot, 296 / 3): one row per run, none empty
+
+
+def test_evisc_xshare_grid_counts_31_columns_per_warp():
+    from paper_2303_12374_b200.stencils.definitions import definition_for
+    from paper_2303_12374_b200.stencils.layout import GridLayout
+
+    d = definition_for("evisc_smag", "fp32")
+    lay = GridLayout(512, 512, 512, "fp32")
+    env = {"arg9": lay.jj, "arg10": lay.kk}
+    cfg = dict(d.space.default_config()[0], staging="TMA", block_x=128, block_y=2, tile_x=1, tile_y=4, zchunk=64,
+               depth=2)
+    g0 = d.derive_geometry(dict(cfg, xshare=0), (512, 512, 512), env).grid[0]
+    g1 = d.derive_geometry(dict(cfg, xshare=1), (512, 512, 512), env).grid[0]
+    assert g0 == 4 * 64 * 8 and g1 == 5 * 64 * 8  # ceil(512 / 124) = 5 blocks along x
+    assert "-D KL_XSHARE=1" in d.render_compile_request(dict(cfg, xshare=1), (512, 512, 512), env).defines
+    assert not d.space.is_valid(dict(cfg, xshare=1, tile_x=2, contiguous_x=True))
