@@ -27,6 +27,7 @@ def main():
     ap.add_argument("--grid", required=True)
     ap.add_argument("--config", required=True, help="JSON config (merged over the default) or a .wisdom file")
     ap.add_argument("--out", default="/tmp/k.cubin")
+    ap.add_argument("--define", action="append", default=[], help="extra NAME=VALUE compile-time switch")
     a = ap.parse_args()
     d = definition_for(a.kernel, a.precision)
     grid = tuple(int(x) for x in a.grid.split(","))
@@ -44,7 +45,13 @@ def main():
     else:
         cfg = dict(default, **json.loads(a.config))
     print(json.dumps(cfg, sort_keys=True))
-    img = NvrtcCompiler().compile_many([d.render_compile_request(cfg, problem, env)], B200)[0].result()
+    req = d.render_compile_request(cfg, problem, env)
+    if a.define:
+        from paper_2303_12374_b200.kerneldef import CompileRequest
+        names = tuple(f"-D {x.split('=')[0]}=" for x in a.define)
+        req = CompileRequest(req.source, req.entry, tuple(x for x in req.defines if not x.startswith(names)) +
+                             tuple(f"-D {x}" for x in a.define), req.flags)
+    img = NvrtcCompiler().compile_many([req], B200)[0].result()
     Path(a.out).write_bytes(img.cubin)
     print(a.out, len(img.cubin))
 

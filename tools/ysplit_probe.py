@@ -4,6 +4,9 @@ the default configuration's output and time (L2 flushed).  GPU only.
 
     python tools/ysplit_probe.py --kernel advec_u --precision fp32 --grid 256,256,256 \
         --case '{"block_y":8,"tile_y":1,"zchunk":128,"depth":4,"ysplit":37}' --case '{}'
+
+A case may carry extra compile-time switches, e.g. '{"defines": {"KL_SKEL": 1}}'
+(advec_u_tma.cuh's data-movement skeleton; its verify_err is meaningless).
 """
 
 from __future__ import annotations
@@ -52,6 +55,7 @@ def main(argv=None) -> int:
     for text in a.case:
         over = json.loads(text)
         n = int(over.pop("ysplit", 0))
+        extra = {str(k): int(v) for k, v in over.pop("defines", {}).items()}  # e.g. {"KL_SKEL": 1}
         cfg = dict(base, **over)
         if True:
             req = d.render_compile_request(cfg, ex.problem, ex.scalar_env)
@@ -59,6 +63,11 @@ def main(argv=None) -> int:
                 req = CompileRequest(req.source, req.entry,
                                      tuple(x for x in req.defines if not x.startswith("-D KL_YBAL=")) +
                                      ("-D KL_YBAL=1",), req.flags)
+            if extra:
+                names = {f"-D {k}=" for k in extra}
+                req = CompileRequest(req.source, req.entry,
+                                     tuple(x for x in req.defines if not any(x.startswith(p) for p in names)) +
+                                     tuple(f"-D {k}={v}" for k, v in extra.items()), req.flags)
             geom = d.derive_geometry(cfg, ex.problem, ex.scalar_env)
             if n:
                 txy = cfg["block_x"] * cfg["tile_x"]
@@ -81,7 +90,7 @@ def main(argv=None) -> int:
                 print(f"{json.dumps(cfg, sort_keys=True)} ysplit={n}: {e!r}", flush=True)
                 continue
             t = statistics.median(secs)
-            rec = {"kernel": a.kernel, "precision": a.precision, "grid": list(grid), "config": cfg, "ysplit": n,
+            rec = {"defines": extra, "kernel": a.kernel, "precision": a.precision, "grid": list(grid), "config": cfg, "ysplit": n,
                    "blocks": geom.grid[0], "smem": geom.shared_mem_bytes, "us": t * 1e6, "min_us": min(secs) * 1e6,
                    "frac": bytes_ / t / 1e9 / peak, "verify_err": err}
             print(json.dumps(rec, sort_keys=True), flush=True)
