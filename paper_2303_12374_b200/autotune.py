@@ -21,7 +21,7 @@ import time
 from pathlib import Path
 
 from .backend import STATUS_OK
-from .tuner import Budget, save_session, tune
+from .tuner import Budget, load_checkpoint, save_session, tune
 from .wisdom import append_result, load_or_create, wisdom_path
 
 __all__ = ["tune_problem", "main", "FOCUSED_TMA"]
@@ -39,7 +39,12 @@ def tune_problem(kernel: str, precision: str, grid: tuple[int, int, int], ctx, *
                  budget: Budget | None = None, seed: int = 0, wisdom_dir: str | Path | None = "wisdom",
                  session_dir: str | Path | None = None, k_range: tuple[int, int] | None = None,
                  repetitions: int = 7, warmup: int = 3, restrict: str | None = None, family: str | None = None,
-                 isolate: bool = False, log=print):
+                 isolate: bool = False, checkpoint: bool = False, resume: bool = False, log=print):
+    """One tuning session of ``kernel`` at ``grid`` on the B200 (writes the
+    session into ``session_dir`` and the result into ``wisdom_dir``).
+    ``checkpoint`` streams the session file while measuring; ``resume``
+    continues that file if an earlier run of the same session left one
+    (tuner.SessionCheckpoint / load_checkpoint)."""
     from .cuda.executor import CudaReplayExecutor
     from .stencils.layout import GridLayout
     from .stencils.problem import StencilProblem
@@ -85,9 +90,20 @@ def tune_problem(kernel: str, precision: str, grid: tuple[int, int, int], ctx, *
         from .space import ConfigSpace
 
         space = ConfigSpace(space.params, list(space.restrictions) + [restrict])
+    session_path = None
+    if session_dir is not None:
+        Path(session_dir).mkdir(parents=True, exist_ok=True)
+        tag = (f".{family.lower()}" if family else "") + (".restricted" if restrict else "")
+        stem = f"{kernel}_{precision}_{'x'.join(map(str, executor.problem))}.{strategy}{tag}.seed{seed}"
+        session_path = Path(session_dir) / f"{stem}.klsession"
+    prior = None
+    if resume and session_path is not None and session_path.exists():
+        prior = load_checkpoint(session_path)
+        log(f"  resuming {session_path.name}: {len(prior.evaluations)} evaluations recorded")
     session = tune(space, executor, strategy=strategy, budget=budget or Budget(max_evaluations=50),
                    seed=seed, device=ctx.ident, kernel_key=definition.kernel_key(),
-                   problem=executor.problem, on_evaluation=progress)
+                   problem=executor.problem, on_evaluation=progress, resume=prior,
+                   checkpoint=session_path if (checkpoint or prior is not None) else None)
     cells = executor.problem[0] * executor.problem[1] * executor.problem[2]
     from .stencils.problem import BYTES_PER_CELL_WORDS
 
@@ -107,11 +123,8 @@ def tune_problem(kernel: str, precision: str, grid: tuple[int, int, int], ctx, *
         if us:
             summary[f"{tag}_gcells"] = cells / (us * 1e-6) / 1e9
             summary[f"{tag}_gbs"] = cells * words * layout.elem_bytes / (us * 1e-6) / 1e9
-    if session_dir is not None:
-        Path(session_dir).mkdir(parents=True, exist_ok=True)
-        tag = (f".{family.lower()}" if family else "") + (".restricted" if restrict else "")
-        stem = f"{kernel}_{precision}_{'x'.join(map(str, executor.problem))}.{strategy}{tag}.seed{seed}"
-        save_session(session, Path(session_dir) / f"{stem}.klsession")
+    if session_path is not None:
+        save_session(session, session_path)
     if wisdom_dir is not None and session.best is not None:
         wfile = load_or_create(wisdom_dir, session.kernel_key)
         append_result(wfile, session)
@@ -148,6 +161,9 @@ def main(argv=None) -> int:
                     help="measure in a worker process replaced after a sticky CUDA error (cuda/isolated.py)")
     ap.add_argument("--family", choices=("DIRECT", "ZMARCH", "TMA"), default=None,
                     help="tune one staging family (its fixed knobs narrowed; see definitions.family_space)")
+    ap.add_argument("--checkpoint", action="store_true", help="stream the session file while measuring")
+    ap.add_argument("--resume", action="store_true",
+                    help="continue the session file an interrupted run of the same session left in --sessions")
     a = ap.parse_args(argv)
     from .cuda import open_device
 
@@ -156,7 +172,8 @@ def main(argv=None) -> int:
     restrict = FOCUSED_TMA if a.focused else a.restrict
     _, summary = tune_problem(a.kernel, a.precision, grid, ctx, strategy=a.strategy,
                               budget=Budget(a.budget_evals, a.budget_seconds), seed=a.seed, wisdom_dir=a.wisdom,
-                              session_dir=a.sessions, restrict=restrict, family=a.family, isolate=a.isolate)
+                              session_dir=a.sessions, restrict=restrict, family=a.family, isolate=a.isolate,
+                              checkpoint=a.checkpoint, resume=a.resume)
     line = json.dumps(summary, sort_keys=True)
     print(line)
     if a.json_out:

@@ -43,6 +43,10 @@
 #ifndef KL_YBAL
 #define KL_YBAL 0  // 0: blocks of kTYT rows; > 0: near-equal row runs, as many as the grid holds (entry)
 #endif
+#ifndef KL_SKEL
+#define KL_SKEL 0  // diagnostic only (tools/skeleton_probe.py): 1 = keep the TMA rings, barriers and ut
+                   // stores but replace the stencil by ut += 1 — the data-movement floor of the tiling
+#endif
 
 #include "kl_pack.cuh"
 #include "kl_tma.cuh"
@@ -236,6 +240,19 @@ struct AdvecTma {
     for (int k = k0; k < k1; ++k) {
       const Planes pl = begin_step(k, cur);
       if (!active) continue;
+      if (KL_SKEL) {
+        const long long kofs = static_cast<long long>(k) * K1;
+#pragma unroll
+        for (int t = 0; t < kTY; ++t) {
+          real tr[kTX], out[kTX];
+          ld_span<VA, 0, kTX>(tr, pl.tp + t * kTW);
+#pragma unroll
+          for (int c = 0; c < kTX; ++c) out[c] = tr[c] + real(1);
+          const int j = j0 + lj0 + t;
+          if (j < jend && ic + kTX <= iend) st_span<VA>(ut + ic + static_cast<long long>(j) * KL_JJ + kofs, out);
+        }
+        continue;
+      }
       const real *xy = pl.xy, *zf = pl.zf, *vp = pl.vp, *wp = pl.wp, *tp = pl.tp;
       const real rh_top = zprof[2 * (k - k0)];
       const real zfac120 = zprof[2 * (k - k0) + 1];
@@ -362,6 +379,19 @@ struct AdvecTma {
     for (int k = k0; k < k1; ++k) {
       const Planes pl = begin_step(k, cur);
       if (!active) continue;
+      if (KL_SKEL) {
+        const long long kofs = static_cast<long long>(k) * K1;
+#pragma unroll
+        for (int t = 0; t < kTY; ++t) {
+          real tr[kTX], out[kTX];
+          ld_span<VA, 0, kTX>(tr, pl.tp + t * kTW);
+#pragma unroll
+          for (int c = 0; c < kTX; ++c) out[c] = tr[c] + real(1);
+          const int j = j0 + lj0 + t;
+          if (j < jend && ic + kTX <= iend) st_span<VA>(ut + ic + static_cast<long long>(j) * KL_JJ + kofs, out);
+        }
+        continue;
+      }
       const real *xy = pl.xy, *zf = pl.zf, *vp = pl.vp, *wp = pl.wp, *tp = pl.tp;
       const f2 rh_top(zprof[2 * (k - k0)]);
       const f2 zfac(zprof[2 * (k - k0) + 1]);

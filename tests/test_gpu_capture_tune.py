@@ -258,3 +258,24 @@ def test_streaming_replay_of_a_multi_gb_capture(tmp_path):
     # fields sit at lead*4 = 116 mod 128 (rows 128-byte aligned); profiles at 0
     assert out["address_mods"].count(out["ptr_mod"]) == 7 and out["ptr_mod"] == 116
     assert out["replay_mods"] == out["address_mods"]
+
+
+def test_autotune_checkpoint_resume_on_gpu(gpu_ctx, tmp_path):
+    """A B200 tuning session streamed to disk (checkpoint) and continued
+    (resume): the continuation keeps the recorded measurements of the first
+    run and measures only the new proposals (SURVEY §5 checkpoint/resume)."""
+    from paper_2303_12374_b200.autotune import tune_problem
+    from paper_2303_12374_b200.tuner import Budget, load_session
+
+    kw = dict(strategy="random", seed=5, wisdom_dir=None, session_dir=tmp_path, repetitions=3, warmup=1,
+              family="TMA", log=lambda *a: None)
+    first, _ = tune_problem("advec_u", "fp32", (64, 48, 40), gpu_ctx, budget=Budget(3, None), checkpoint=True, **kw)
+    (path,) = list(tmp_path.glob("*.klsession"))
+    seen = []
+    kw["log"] = seen.append
+    second, _ = tune_problem("advec_u", "fp32", (64, 48, 40), gpu_ctx, budget=Budget(6, None), resume=True, **kw)
+    assert any("resuming" in str(x) for x in seen)
+    assert len(second.evaluations) == 6
+    for a, b in zip(first.evaluations, second.evaluations[:3]):
+        assert a.config == b.config and a.measurement.objective == b.measurement.objective
+    assert len(load_session(path).evaluations) == 6
