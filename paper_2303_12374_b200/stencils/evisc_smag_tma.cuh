@@ -29,6 +29,10 @@
 #ifndef KL_XSHARE
 #define KL_XSHARE 0
 #endif
+#ifndef KL_SKEL
+#define KL_SKEL 0  // diagnostic only (tools/ysplit_probe.py defines): 1 = keep the TMA ring, barriers and
+                   // evisc stores, replace the strain-rate arithmetic by one read of u — the data-movement floor
+#endif
 #if KL_XSHARE && (TILE_X != 1 || BLOCK_X % 32 != 0)
 #error "evisc_smag x-edge sharing needs TILE_X == 1 and whole warps along x"
 #endif
@@ -316,6 +320,19 @@ struct EviscTma {
       const real* pk = ring + sk * kSlot;
       const real* pk1 = ring + sk1 * kSlot;
       const real dz = lv.dz, dzh1 = lv.dzh1, fac = lv.fac;
+      if (KL_SKEL) {
+        real* const srow = evisc + ic + static_cast<long long>(j0 + lj0) * KL_JJ + static_cast<long long>(k) * KL_KK;
+#pragma unroll
+        for (int t = 0; t < kTY; ++t)
+#pragma unroll
+          for (int c = 0; c < kTX; ++c)
+            if (j0 + lj0 + t < jend && ic + c < iend && !(kXS && helper)) srow[t * KL_JJ + c] = pk1[hof[0] + t * kBW + c];
+        sprev = sk;
+        sk = sk1;
+        sk1 = sk1 + 1 == kNS ? 0 : sk1 + 1;
+        ph1 ^= sk1 == 0 ? 1u : 0u;
+        continue;
+      }
       Faces top;
       top_faces(pk, pk1, dzh1, top);
 
