@@ -39,7 +39,8 @@ import ctypes as C
 from dataclasses import dataclass
 
 __all__ = [
-    "HALO_REACH", "SlabDecomposition", "halo_plan", "NcclExchanger", "IpcExchanger", "CopyExchanger", "SlabRank",
+    "HALO_REACH", "SlabDecomposition", "halo_plan", "NcclExchanger", "IpcExchanger", "CopyExchanger", "LocalPeers",
+    "SlabRank",
 ]
 
 #: kernel -> {field: (down, up)}
@@ -52,6 +53,7 @@ HALO_REACH = {
     "diff_c": {"s": (1, 1), "evisc": (1, 1)},
     "evisc_smag": {"u": (1, 1), "v": (1, 1), "w": (1, 0)},
     "diff_uvw_rk3": {"evisc": (1, 1), "u": (1, 1), "v": (1, 1), "w": (1, 1)},
+    "diff_uvw_peer": {"evisc": (1, 1), "u": (1, 1), "v": (1, 1), "w": (1, 1)},
     "rk3_uvw": {},
 }
 
@@ -187,8 +189,8 @@ class IpcExchanger:
                     check(lib().klb_ipc_event_open(h, C.byref(ev)))
                     evs.append(ev.value)
                 self._peer_events[r] = tuple(evs)
-        self._maps: dict[tuple, dict] = {}  # local pointer tuple -> peer mappings
-        self._opened: list[int] = []
+        self._maps: dict[tuple, dict] = {}  # (local pointer tuple, kstart, kend) -> peer mappings
+        self._opened: dict[tuple, list[int]] = {}  # same key -> the mapped bases to close
 
     @staticmethod
     def probe(group) -> tuple[bool, str]:
@@ -277,11 +279,42 @@ class IpcExchanger:
                 off, = struct.unpack_from("<Q", allb[r], at + 64)
                 base = C.c_uint64()
                 check(lib().klb_ipc_mem_open(h, C.byref(base)))
-                self._opened.append(base.value)
+                self._opened.setdefault(key, []).append(base.value)
                 mapped.append(base.value + off)
             entry[side] = (mapped, ks, ke)
         self._maps[key] = entry
         return entry
+
+    def peer_fields(self, fields: dict[str, int], kstart: int, kend: int) -> dict:
+        """Collective: the neighbours' pointers of ``fields`` (name -> local
+        pointer) mapped into this process, ``{"below"|"above": (name ->
+        pointer, their kstart, their kend)}`` — what the fused-halo kernel
+        (diff_uvw_peer) reads the planes outside the slab from."""
+        names = list(fields)
+        entry = self._attach([fields[n] for n in names], kstart, kend)
+        return {side: (dict(zip(names, mapped)), ks, ke) for side, (mapped, ks, ke) in entry.items()}
+
+    def fence_ready(self, stream, below: int, above: int) -> None:
+        """Order ``stream`` after the neighbours' work that produced their
+        input planes (each rank records, a host barrier, each waits)."""
+        from .cuda._abi import check, lib
+
+        check(lib().klb_event_record(self.ready, stream.handle))
+        self.group.barrier()
+        for r in (below, above):
+            if r >= 0:
+                check(lib().klb_stream_wait_event(stream.handle, self._peer_events[r][0]))
+
+    def fence_done(self, stream, below: int, above: int) -> None:
+        """Order ``stream``'s later work after the neighbours have finished
+        reading this rank's planes (no write-after-read race in a time loop)."""
+        from .cuda._abi import check, lib
+
+        check(lib().klb_event_record(self.pulled, stream.handle))
+        self.group.barrier()
+        for r in (below, above):
+            if r >= 0:
+                check(lib().klb_stream_wait_event(stream.handle, self._peer_events[r][1]))
 
     def exchange(self, stream, ptrs, elem_bytes: int, kk: int, kstart: int, kend: int, down: int, up: int,
                  below: int, above: int) -> None:
@@ -289,11 +322,7 @@ class IpcExchanger:
 
         entry = self._attach(ptrs, kstart, kend)
         n = len(ptrs)
-        check(lib().klb_event_record(self.ready, stream.handle))
-        self.group.barrier()
-        neighbours = [r for r in (below, above) if r >= 0]
-        for r in neighbours:
-            check(lib().klb_stream_wait_event(stream.handle, self._peer_events[r][0]))
+        self.fence_ready(stream, below, above)
         arr = (C.c_uint64 * n)(*ptrs)
         lo = (C.c_uint64 * n)(*entry["below"][0]) if below >= 0 else None
         hi = (C.c_uint64 * n)(*entry["above"][0]) if above >= 0 else None
@@ -301,20 +330,23 @@ class IpcExchanger:
         above_kstart = entry["above"][1] if above >= 0 else 0
         check(lib().klb_halo_pull_z(stream.handle, n, arr, lo, hi, elem_bytes, kk, kstart, kend, down, up,
                                     below_kend, above_kstart))
-        check(lib().klb_event_record(self.pulled, stream.handle))
-        self.group.barrier()
-        for r in neighbours:
-            check(lib().klb_stream_wait_event(stream.handle, self._peer_events[r][1]))
+        self.fence_done(stream, below, above)
 
-    def detach(self) -> None:
-        """Collective: unmap every peer allocation (before fields are freed)."""
+    def detach(self, ptrs=None) -> None:
+        """Collective: unmap the neighbours' allocations mapped for field sets
+        of the local pointers ``ptrs`` (all when None) — before the fields are
+        freed.  Mappings of other field sets (another driver sharing this
+        exchanger, e.g. a fused-halo slab launch holding peer pointers) stay."""
         from .cuda._abi import lib
 
         lib().klb_device_synchronize()
         self.group.barrier()  # nobody still copies from a mapping being closed
-        for base in self._opened:
-            lib().klb_ipc_mem_close(base)
-        self._opened, self._maps = [], {}
+        mine = None if ptrs is None else set(ptrs)
+        for key in list(self._maps):
+            if mine is None or set(key[0]) <= mine:
+                for base in self._opened.pop(key, []):
+                    lib().klb_ipc_mem_close(base)
+                del self._maps[key]
         self.group.barrier()  # every peer has unmapped before anyone frees
 
     def close(self) -> None:
@@ -328,6 +360,38 @@ class IpcExchanger:
             for ev in self._events:
                 lib().klb_event_destroy(ev)
             self._events, self._peer_events = [], {}
+
+
+class LocalPeers:
+    """Virtual ranks on ONE device for the fused-halo kernel: rank ``r``'s
+    neighbours' fields are plain allocations of the same context, and every
+    rank's launches go to one stream, so the fences are no-ops.  ``ranks[r]``
+    = (name -> pointer of element (0,0,0), kstart, kend); ``for_rank(r)`` is
+    the per-rank view ``SlabDriver(halo="fused")`` takes as its exchanger."""
+
+    def __init__(self, ranks: list[tuple[dict[str, int], int, int]]) -> None:
+        self.ranks = ranks
+
+    def for_rank(self, r: int) -> "LocalPeers._View":
+        return LocalPeers._View(self, r)
+
+    class _View:
+        def __init__(self, owner: "LocalPeers", rank: int) -> None:
+            self.owner, self.rank = owner, rank
+
+        def peer_fields(self, fields: dict[str, int], kstart: int, kend: int) -> dict:
+            out = {}
+            for side, r in (("below", self.rank - 1), ("above", self.rank + 1)):
+                if 0 <= r < len(self.owner.ranks):
+                    ptrs, ks, ke = self.owner.ranks[r]
+                    out[side] = ({n: ptrs[n] for n in fields}, ks, ke)
+            return out
+
+        def fence_ready(self, stream, below: int, above: int) -> None:
+            pass
+
+        def fence_done(self, stream, below: int, above: int) -> None:
+            pass
 
 
 class CopyExchanger:

@@ -10,7 +10,13 @@ Wires the pieces of ``halo.py`` to the runtime launch path:
 * ``step()`` issues: halo exchange on the comm stream (peer-memory pulls over
   CUDA IPC, NCCL send/recv, or D2D copies for virtual ranks), the interior
   launch on the compute stream concurrently, then the boundary launches
-  after the exchange event.
+  after the exchange event;
+* ``halo="fused"`` (diff_uvw): no exchange and no sub-ranges — ONE launch of
+  ``diff_uvw_peer`` over the whole slab, whose TMA staging reads the planes
+  just outside the slab straight from the neighbours' fields through
+  peer-mapped pointers (``IpcExchanger.peer_fields``; ``LocalPeers`` for
+  virtual ranks), between two cross-rank fences (the neighbours' inputs are
+  final / they are done reading ours).
 
 All launches are asynchronous; callers time steps with CUDA events on
 ``compute`` (the comm stream is joined back into it every step).
@@ -24,6 +30,7 @@ from .capture import CapturePolicy
 from .cuda.device import DeviceContext, Event, Stream
 from .dispatch import WisdomKernel
 from .halo import HALO_REACH, SlabDecomposition, SlabRank
+from .stencils.definitions import definition_for
 from .stencils.layout import GridLayout
 from .stencils.problem import StencilProblem
 from .stencils.profiles import make_profiles
@@ -34,9 +41,16 @@ __all__ = ["SlabDriver"]
 class SlabDriver:
     def __init__(self, kernel: str, precision: str, grid: tuple[int, int, int], ctx: DeviceContext, *,
                  rank: int = 0, nranks: int = 1, exchanger=None, compiler=None,
-                 wisdom_dir: str | Path | None = None, ghost: int = 3) -> None:
+                 wisdom_dir: str | Path | None = None, ghost: int = 3, halo: str = "exchange") -> None:
         from .cuda.compiler import NvrtcCompiler
 
+        if halo not in ("exchange", "fused"):
+            raise ValueError(f"halo must be 'exchange' or 'fused', not {halo!r}")
+        if halo == "fused" and kernel != "diff_uvw":
+            raise ValueError("the fused halo (diff_uvw_peer) exists for diff_uvw")
+        self.fused = halo == "fused"
+        if self.fused and nranks > 1 and exchanger is None:
+            raise ValueError("the fused halo needs an exchanger that maps the neighbours' fields")
         self.kernel, self.precision, self.grid = kernel, precision, tuple(grid)
         self.ctx = ctx
         self.rank, self.nranks = rank, nranks
@@ -47,13 +61,17 @@ class SlabDriver:
         self.layout = GridLayout(grid[0], grid[1], self.slab.count, precision, ghost, ghost, ghost)
         profiles = make_profiles(self.global_layout.kcells, ghost)
         self.compute = ctx.stream
-        self.comm = Stream.create() if exchanger is not None else None
-        self.problem = StencilProblem(kernel, self.layout, ctx, k_offset=self.slab.offset,
-                                      kcells_global=self.global_layout.kcells, profiles=profiles, stream=self.compute)
+        self.comm = Stream.create() if exchanger is not None and not self.fused else None
+        self.problem = StencilProblem("diff_uvw_peer" if self.fused else kernel, self.layout, ctx,
+                                      k_offset=self.slab.offset, kcells_global=self.global_layout.kcells,
+                                      profiles=profiles, stream=self.compute)
         self.compiler = compiler or NvrtcCompiler(ctx)
+        # the fused kernel selects from diff_uvw's wisdom (same space and problem sizes)
+        base_key = definition_for(kernel, precision).kernel_key() if self.fused else None
         self.wisdom = WisdomKernel(self.problem.definition, self.compiler, wisdom_dir=wisdom_dir or ".",
-                                   capture_policy=CapturePolicy())
-        self.ranges = self.slab.subranges()
+                                   capture_policy=CapturePolicy(), wisdom_key=base_key)
+        self.ranges = {"slab": (self.layout.kstart, self.layout.kend)} if self.fused else self.slab.subranges()
+        self._peers_attached = not (self.fused and exchanger is not None and nranks > 1)
         self.args = {name: self.problem.args(rng) for name, rng in self.ranges.items()}
         self.below, self.above = self.decomposition.neighbours(rank)
         self._ev_start = Event()
@@ -66,8 +84,27 @@ class SlabDriver:
         self.stream_bytes = (0, 0)  # (h2d, d2h) bytes of the last step_host
 
     # -- setup -------------------------------------------------------------------------
+    def attach_peers(self) -> None:
+        """Fused halo: map the neighbours' evisc/u/v/w and point the slab
+        launch's peer arguments at them (collective over the ranks when the
+        exchanger maps IPC memory; done once, on first use)."""
+        if self._peers_attached:
+            return
+        lay = self.layout
+        names = ("evisc", "u", "v", "w")
+        got = self.exchanger.peer_fields({n: self.problem.field_ptr(n) for n in names}, lay.kstart, lay.kend)
+        sides = {}
+        for side, (ptrs, ks, ke) in got.items():
+            # the neighbour's allocation differs from ours only in its plane count
+            count = lay.span_elems + ((ke - ks) - (lay.kend - lay.kstart)) * lay.kk
+            sides[side] = (ptrs, count, ke if side == "below" else ks)
+        self.problem.set_peers(below=sides.get("below"), above=sides.get("above"))
+        self.args = {name: self.problem.args(rng) for name, rng in self.ranges.items()}
+        self._peers_attached = True
+
     def resolve(self) -> dict:
         """Select + compile every sub-range before timing; returns name -> (config, match_kind)."""
+        self.attach_peers()
         out = {}
         for name, args in self.args.items():
             report = self.wisdom.launch(self.ctx.ident, args, stream=self.compute)
@@ -110,8 +147,6 @@ class SlabDriver:
     def step(self, time_kernel: tuple[Event, Event] | None = None) -> int:
         """Enqueue one step; returns the number of kernels launched."""
         ident = self.ctx.ident
-        self.exchange()
-        launched = 0
         bound = self._bound
 
         def run(name):
@@ -119,6 +154,22 @@ class SlabDriver:
                 bound[name]()
             else:
                 self.wisdom.launch(ident, self.args[name], stream=self.compute)
+
+        if self.fused:
+            self.attach_peers()
+            ex = self.exchanger
+            if ex is not None:
+                ex.fence_ready(self.compute, self.below, self.above)
+            if time_kernel is not None:
+                time_kernel[0].record(self.compute)
+            run("slab")
+            if time_kernel is not None:
+                time_kernel[1].record(self.compute)
+            if ex is not None:
+                ex.fence_done(self.compute, self.below, self.above)
+            return 1
+        self.exchange()
+        launched = 0
 
         if "interior" in self.args:
             if time_kernel is not None:
@@ -148,6 +199,8 @@ class SlabDriver:
         from .cuda._abi import check, lib
         from .stream import stream_plan
 
+        if self.fused:
+            raise ValueError("step_host streams the exchange variant (halo='exchange')")
         lay = self.layout
         if self._stream_state is None or self._stream_state[0] != (chunks, copy_streams):
             fields = tuple(self.problem.fields)
@@ -211,7 +264,7 @@ class SlabDriver:
         unmaps its neighbours' fields before any rank frees its own."""
         detach = getattr(self.exchanger, "detach", None)
         if callable(detach):
-            detach()
+            detach([self.problem.field_ptr(n) for n in self.problem.fields])
         self.problem.close()
         if self.comm is not None:
             self.comm.close()

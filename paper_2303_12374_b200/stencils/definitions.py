@@ -59,7 +59,10 @@ ADV_FAMILY = ("advec_v", "advec_w", "advec_s")
 PLANE_FAMILY = {"diff_c": (2, 1, 3), "evisc_smag": (3, 0, 2)}
 #: hot-path kernels with a fused epilogue: same space and
 #: staging families as their base kernel, compiled with a -D switch
-FUSED_KERNELS = {"diff_uvw_rk3": ("diff_uvw", "KL_RK3")}
+FUSED_KERNELS = {"diff_uvw_rk3": ("diff_uvw", "KL_RK3"),
+                 # z-slab halo fused into the TMA staging: planes outside the
+                 # slab are read from the neighbours' fields (diff_uvw.cu KL_PEER)
+                 "diff_uvw_peer": ("diff_uvw", "KL_PEER")}
 ALL_KERNELS = KERNELS + tuple(FUSED_KERNELS) + FAMILY_KERNELS
 
 
@@ -127,6 +130,15 @@ ARG_LAYOUT = {
                     ("rhorefh", "input"), ("u_next", "output"), ("v_next", "output"), ("w_next", "output")],
         "scalars": ["dxi", "dyi", "rk_a", "rk_bdt", "jj", "kk", "istart", "jstart", "kstart", "iend", "jend",
                     "kend"],
+    },
+    "diff_uvw_peer": {
+        "buffers": [("ut", "output"), ("vt", "output"), ("wt", "output"), ("evisc", "input"), ("u", "input"),
+                    ("v", "input"), ("w", "input"), ("dzi", "input"), ("dzhi", "input"), ("rhoref", "input"),
+                    ("rhorefh", "input"), ("evisc_lo", "input"), ("u_lo", "input"), ("v_lo", "input"),
+                    ("w_lo", "input"), ("evisc_hi", "input"), ("u_hi", "input"), ("v_hi", "input"),
+                    ("w_hi", "input")],
+        "scalars": ["dxi", "dyi", "peer_klo", "peer_khi", "peer_shift_lo", "peer_shift_hi", "jj", "kk", "istart",
+                    "jstart", "kstart", "iend", "jend", "kend"],
     },
     "rk3_uvw": {
         "buffers": [("ut", "output"), ("vt", "output"), ("wt", "output"), ("u", "output"), ("v", "output"),

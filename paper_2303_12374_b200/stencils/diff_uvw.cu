@@ -37,9 +37,36 @@
 #define KL_RK3_BUFFERS
 #define KL_RK3_SCALARS
 #endif
-// argument positions of jj / kk (definitions.ARG_LAYOUT) for the TMA spec
-#define KL_POS_JJ (KL_RK3 ? 18 : 13)
-#define KL_POS_KK (KL_RK3 ? 19 : 14)
+// KL_PEER (kernel diff_uvw_peer, SURVEY §5's B200 option for the z-slab
+// halo): the planes just outside the rank's slab are not exchanged into ghost
+// planes first — the TMA loads of every plane p < peer_klo (p >= peer_khi)
+// read plane p + peer_shift_lo (p + peer_shift_hi) of the neighbour's field
+// through a peer-mapped pointer (CUDA IPC over NVLink), so one launch covers
+// the whole slab and the exchange is fused into the stencil's staging.  The
+// peer pointers have the local fields' layout; a rank without a neighbour on
+// a side passes its own fields and a bound no plane reaches.
+#ifndef KL_PEER
+#define KL_PEER 0
+#endif
+#if KL_PEER
+#if STAGING != 2
+#error "KL_PEER (diff_uvw_peer) reads the neighbours' planes in the TMA staging only"
+#endif
+#define KL_PEER_BUFFERS                                                                                 \
+  , const real* __restrict__ evisc_lo, const real* __restrict__ u_lo, const real* __restrict__ v_lo,  \
+      const real* __restrict__ w_lo, const real* __restrict__ evisc_hi, const real* __restrict__ u_hi, \
+      const real* __restrict__ v_hi, const real* __restrict__ w_hi
+#define KL_PEER_SCALARS , const int peer_klo, const int peer_khi, const int peer_shift_lo, const int peer_shift_hi
+#else
+#define KL_PEER_BUFFERS
+#define KL_PEER_SCALARS
+#endif
+// argument positions of jj / kk (definitions.ARG_LAYOUT) for the TMA spec:
+// 11 buffers (+3 RK3, +8 peer), dxi, dyi (+2 RK3, +4 peer scalars), jj, kk
+#define KL_POS_JJ (13 + 5 * KL_RK3 + 12 * KL_PEER)
+#define KL_POS_KK (KL_POS_JJ + 1)
+// first peer buffer (evisc_lo) and the peer count of the TMA spec
+#define KL_POS_PEER (11 + 3 * KL_RK3)
 
 namespace {
 
@@ -136,7 +163,8 @@ extern "C" __global__ void __launch_bounds__(KL_THREADS, MIN_BLOCKS)
 KL_ENTRY(real* __restrict__ ut, real* __restrict__ vt, real* __restrict__ wt, const real* __restrict__ evisc,
          const real* __restrict__ u, const real* __restrict__ v, const real* __restrict__ w,
          const real* __restrict__ dzi, const real* __restrict__ dzhi, const real* __restrict__ rhoref,
-         const real* __restrict__ rhorefh KL_RK3_BUFFERS, const real dxi, const real dyi KL_RK3_SCALARS,
+         const real* __restrict__ rhorefh KL_RK3_BUFFERS KL_PEER_BUFFERS, const real dxi,
+         const real dyi KL_RK3_SCALARS KL_PEER_SCALARS,
          const int jj, const int kk, const int istart, const int jstart, const int kstart, const int iend,
          const int jend, const int kend) {
   if (jj != KL_JJ || kk != KL_KK) __trap();

@@ -426,6 +426,9 @@ struct DiffTma {
   real *un, *vn, *wn;  // u, v, w of the next RK3 substep
   real rk_a, rk_bdt;
 #endif
+#if KL_PEER
+  int peer_klo, peer_khi, peer_shift_lo, peer_shift_hi;  // planes read from the neighbours (diff_uvw.cu)
+#endif
   const real* zprof;  // [ZCHUNK][5] per-plane factors
   real* ring;
   unsigned long long* full;
@@ -441,8 +444,24 @@ struct DiffTma {
     unsigned long long* bar = full + slot;
     real* dst = ring + slot * kSlot;
     kl::mbar_expect_tx(bar, kTxBytes);
+#if KL_PEER
+    // a plane outside the slab comes from the neighbour's field (maps 7..10
+    // below, 11..14 above) at the neighbour's own plane index
+    const TmaDesc* hm = maps;
+    int hp = p;
+    if (p < peer_klo) {
+      hm = maps + 7;
+      hp = p + peer_shift_lo;
+    } else if (p >= peer_khi) {
+      hm = maps + 11;
+      hp = p + peer_shift_hi;
+    }
+#pragma unroll
+    for (int f = 0; f < 4; ++f) kl::tma_load_3d(dst + f * kFS, hm + f, bar, xh[f], j0 - 1, hp);
+#else
 #pragma unroll
     for (int f = 0; f < 4; ++f) kl::tma_load_3d(dst + f * kFS, maps + f, bar, xh[f], j0 - 1, p);
+#endif
 #pragma unroll
     for (int f = 0; f < 3; ++f) kl::tma_load_3d(dst + 4 * kFS + f * kTS, maps + 4 + f, bar, xt, j0, p);
   }
@@ -578,20 +597,30 @@ struct DiffTma {
 // (definitions.ARG_LAYOUT["diff_uvw"] / ["diff_uvw_rk3"])
 #define KL_J KL_POS_JJ
 #define KL_K KL_POS_KK
-extern "C" __device__ const int kl_tma_spec[1 + 5 * 7] = {
-    7, 3, KL_J, KL_K, kBW, kBH, 4, KL_J, KL_K, kBW, kBH, 5, KL_J, KL_K, kBW, kBH, 6, KL_J, KL_K, kBW, kBH,
-    0, KL_J, KL_K, kTW, kTYT, 1, KL_J, KL_K, kTW, kTYT, 2, KL_J, KL_K, kTW, kTYT};
+#define KL_NMAPS (7 + 8 * KL_PEER)
+extern "C" __device__ const int kl_tma_spec[1 + 5 * KL_NMAPS] = {
+    KL_NMAPS, 3, KL_J, KL_K, kBW, kBH, 4, KL_J, KL_K, kBW, kBH, 5, KL_J, KL_K, kBW, kBH, 6, KL_J, KL_K, kBW, kBH,
+    0, KL_J, KL_K, kTW, kTYT, 1, KL_J, KL_K, kTW, kTYT, 2, KL_J, KL_K, kTW, kTYT
+#if KL_PEER
+    // the neighbours' evisc, u, v, w (below, then above), same boxes as the local ones
+    , KL_POS_PEER + 0, KL_J, KL_K, kBW, kBH, KL_POS_PEER + 1, KL_J, KL_K, kBW, kBH,
+    KL_POS_PEER + 2, KL_J, KL_K, kBW, kBH, KL_POS_PEER + 3, KL_J, KL_K, kBW, kBH,
+    KL_POS_PEER + 4, KL_J, KL_K, kBW, kBH, KL_POS_PEER + 5, KL_J, KL_K, kBW, kBH,
+    KL_POS_PEER + 6, KL_J, KL_K, kBW, kBH, KL_POS_PEER + 7, KL_J, KL_K, kBW, kBH
+#endif
+};
 #undef KL_J
 #undef KL_K
 struct __align__(64) KlTmaParams {
-  TmaDesc map[7];
+  TmaDesc map[KL_NMAPS];
 };
 
 extern "C" __global__ void __launch_bounds__(KL_THREADS, MIN_BLOCKS)
 KL_ENTRY(real* __restrict__ ut, real* __restrict__ vt, real* __restrict__ wt, const real* __restrict__ evisc,
          const real* __restrict__ u, const real* __restrict__ v, const real* __restrict__ w,
          const real* __restrict__ dzi, const real* __restrict__ dzhi, const real* __restrict__ rhoref,
-         const real* __restrict__ rhorefh KL_RK3_BUFFERS, const real dxi, const real dyi KL_RK3_SCALARS,
+         const real* __restrict__ rhorefh KL_RK3_BUFFERS KL_PEER_BUFFERS, const real dxi,
+         const real dyi KL_RK3_SCALARS KL_PEER_SCALARS,
          const int jj, const int kk, const int istart, const int jstart, const int kstart, const int iend,
          const int jend, const int kend, const __grid_constant__ KlTmaParams tma) {
   if (jj != KL_JJ || kk != KL_KK) __trap();
@@ -620,6 +649,14 @@ KL_ENTRY(real* __restrict__ ut, real* __restrict__ vt, real* __restrict__ wt, co
   m.wn = wn;
   m.rk_a = rk_a;
   m.rk_bdt = rk_bdt;
+#endif
+#if KL_PEER
+  m.peer_klo = peer_klo;
+  m.peer_khi = peer_khi;
+  m.peer_shift_lo = peer_shift_lo;
+  m.peer_shift_hi = peer_shift_hi;
+  // (the peer fields share the local layout, so their boxes start at the
+  // local x coordinates; the host checks the 16-byte phase of each pointer)
 #endif
   m.ring = ring;
   m.full = full;

@@ -36,6 +36,7 @@ KERNEL_FIELDS = {
     "diff_c": ("st", "s", "evisc"),
     "evisc_smag": ("evisc", "u", "v", "w"),
     "diff_uvw_rk3": ("ut", "vt", "wt", "evisc", "u", "v", "w", "u_next", "v_next", "w_next"),
+    "diff_uvw_peer": ("ut", "vt", "wt", "evisc", "u", "v", "w"),
     "rk3_uvw": ("ut", "vt", "wt", "u", "v", "w"),
 }
 #: algorithmic HBM words per interior cell: advec_u reads u,v,w,ut
@@ -46,6 +47,8 @@ BYTES_PER_CELL_WORDS = {"advec_u": 5, "diff_uvw": 10, "advec_v": 5, "advec_w": 5
                         "evisc_smag": 4,
                         # diff_uvw + RK3 epilogue: reads evisc,u,v,w,ut,vt,wt, writes ut,vt,wt,u',v',w'
                         "diff_uvw_rk3": 13,
+                        # diff_uvw with its z-halo read from the neighbours' fields: same words per cell
+                        "diff_uvw_peer": 10,
                         # the separate RK3 pass: read + write u,v,w,ut,vt,wt
                         "rk3_uvw": 12}
 #: MicroHH defaults of the model constants the family kernels take
@@ -56,6 +59,10 @@ CS = 0.23   # Smagorinsky constant
 RK_A = -5.0 / 9.0
 RK_BDT = 15.0 / 16.0 * 0.01
 _PROFILE_FIELDS = ("rhoref", "rhorefh", "dzi", "dzhi")
+#: diff_uvw_peer's neighbour-field arguments -> the local field they mirror
+_PEER_FIELDS = {f"{f}_{side}": f for side in ("lo", "hi") for f in ("evisc", "u", "v", "w")}
+#: peer_klo / peer_khi of a side without a neighbour: a plane no launch reaches
+_NO_PEER = 1 << 30
 
 
 class StencilProblem:
@@ -79,6 +86,10 @@ class StencilProblem:
         self.profiles = glob.window(k_offset, layout.kcells).as_dtype(layout.dtype)
         self.fields: dict[str, DeviceArray] = {}
         self._borrowed: set[str] = set()  # fields aliased from another problem (share_fields)
+        # diff_uvw_peer: neighbour fields (name -> (pointer, element count)) and
+        # (peer_klo, peer_khi, peer_shift_lo, peer_shift_hi); default: none
+        self.peers: dict[str, tuple[int, int]] = {}
+        self.peer_bounds = (-_NO_PEER, _NO_PEER, 0, 0)
         for name in KERNEL_FIELDS[kernel]:
             arr = DeviceArray(layout.alloc_bytes)
             arr.zero(self.stream)
@@ -125,6 +136,10 @@ class StencilProblem:
         for name, role in ARG_LAYOUT[self.kernel]["buffers"]:
             if name in self.fields:
                 args.append(DeviceBuffer(pos, role, elem, self.field_ptr(name), lay.span_elems, owner=self.fields[name]))
+            elif name in _PEER_FIELDS:  # no neighbour on that side: the local field, never reached
+                local = _PEER_FIELDS[name]
+                ptr, count = self.peers.get(name, (self.field_ptr(local), lay.span_elems))
+                args.append(DeviceBuffer(pos, role, elem, ptr, count, owner=self.fields[local]))
             else:
                 arr = self.profile_arrays[name]
                 args.append(DeviceBuffer(pos, role, elem, arr.ptr, arr.nbytes // lay.elem_bytes, owner=arr))
@@ -135,6 +150,8 @@ class StencilProblem:
             "iend": ("i32", lay.iend), "jend": ("i32", lay.jend), "kend": ("i32", lay.kend),
             "tpri": (elem, self.tpri), "cs": (elem, self.cs), "rk_a": (elem, self.rk_a),
             "rk_bdt": (elem, self.rk_bdt),
+            "peer_klo": ("i32", self.peer_bounds[0]), "peer_khi": ("i32", self.peer_bounds[1]),
+            "peer_shift_lo": ("i32", self.peer_bounds[2]), "peer_shift_hi": ("i32", self.peer_bounds[3]),
         }
         for name in ARG_LAYOUT[self.kernel]["scalars"]:
             dtype, value = scalars[name]
@@ -153,6 +170,35 @@ class StencilProblem:
         out[pos_ks] = ScalarArg(pos_ks, "i32", kb)
         out[pos_ke] = ScalarArg(pos_ke, "i32", ke)
         return out
+
+    def set_peers(self, below=None, above=None) -> None:
+        """diff_uvw_peer: read the planes outside this slab from the
+        neighbours' fields.  ``below`` / ``above`` = ``(pointers, element
+        count, plane)``: the neighbour's field pointers of element (0,0,0) by
+        name (evisc, u, v, w; device memory this context can address — a CUDA
+        IPC mapping or another allocation of this device), the element count
+        from there (its ``layout.span_elems``) and its local ``kend`` (below)
+        / ``kstart`` (above), so that local plane ``kstart - 1`` maps to
+        ``kend_below - 1`` and ``kend`` to ``kstart_above``."""
+        if self.kernel != "diff_uvw_peer":
+            raise ValueError("set_peers applies to diff_uvw_peer")
+        lay = self.layout
+        peers: dict[str, tuple[int, int]] = {}
+        klo, khi, shlo, shhi = -_NO_PEER, _NO_PEER, 0, 0
+        for side, info in (("lo", below), ("hi", above)):
+            if info is None:
+                continue
+            ptrs, count, plane = info
+            for f in ("evisc", "u", "v", "w"):
+                if (ptrs[f] - self.field_ptr(f)) % 16:
+                    raise ValueError(f"peer {f}_{side} has another 16-byte phase than the local field")
+                peers[f"{f}_{side}"] = (int(ptrs[f]), int(count))
+            if side == "lo":
+                klo, shlo = lay.kstart, int(plane) - lay.kstart
+            else:
+                khi, shhi = lay.kend, int(plane) - lay.kend
+        self.peers, self.peer_bounds = peers, (klo, khi, shlo, shhi)
+        self._args = self._build_args()
 
     def share_fields(self, other: "StencilProblem", names) -> None:
         """Use ``other``'s device buffers for ``names`` — kernels chained in one

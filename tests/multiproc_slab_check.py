@@ -58,14 +58,27 @@ def main() -> int:
         print(f"rank {rank} {'ok' if ok else 'FAIL'} probe {why}", flush=True)
         return 0 if ok else 1
     kernel, precision, grid = sys.argv[1], sys.argv[2], tuple(int(x) for x in sys.argv[3].split(","))
-    if os.environ.get("KL_HALO_TRANSPORT", "ipc") == "nccl":
+    transport = os.environ.get("KL_HALO_TRANSPORT", "ipc")
+    if transport == "nccl":
         uid = group.broadcast(NcclExchanger.unique_id() if rank == 0 else None, size=128)
         ex = NcclExchanger(rank, world, uid)
     else:
         ex = IpcExchanger(group)
+    # "fused": no exchange at all — diff_uvw_peer reads the planes outside the
+    # slab from the neighbours' IPC-mapped fields (the poisoned ghost planes
+    # below are then never read)
     drv = SlabDriver(kernel, precision, grid, ctx, rank=rank, nranks=world, exchanger=ex,
-                     compiler=NvrtcCompiler(ctx), wisdom_dir=str(ROOT / "wisdom"))
+                     compiler=NvrtcCompiler(ctx), wisdom_dir=str(ROOT / "wisdom"),
+                     halo="fused" if transport == "fused" else "exchange")
     drv.resolve()
+    if os.environ.get("KL_CHECK_SHARED"):
+        # another driver on the same exchanger, stepped and closed: closing it
+        # must unmap only its own field set, not drv's peer mappings
+        extra = SlabDriver(kernel, precision, grid, ctx, rank=rank, nranks=world, exchanger=ex,
+                           compiler=NvrtcCompiler(ctx), wisdom_dir=str(ROOT / "wisdom"))
+        extra.resolve()
+        extra.step()
+        extra.close()
     ref, _ = oracle_outputs(kernel, GridLayout(*grid, precision))
     g = drv.layout.kgc
     off, count = drv.slab.offset, drv.slab.count

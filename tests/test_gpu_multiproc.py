@@ -73,6 +73,27 @@ def test_spawned_ranks_without_torch_match_oracle(kernel, precision, grid, nproc
     assert len(re.findall(r"rank \d+ ok ", out)) == nproc and "FAIL" not in out, out
 
 
+@pytest.mark.parametrize("precision,grid,nproc,shared", [("fp32", "64,40,30", 3, False),
+                                                         ("fp64", "40,24,36", 2, False),
+                                                         ("fp32", "48,32,20", 2, True)])
+def test_fused_peer_halo_ranks_match_oracle(precision, grid, nproc, shared):
+    """diff_uvw with the z-halo fused into the kernel: one launch per rank
+    over its whole slab, the planes outside the slab read through CUDA-IPC
+    mappings of the neighbours' fields (the local ghost planes are poisoned
+    and never read).  ``shared``: an exchange-mode driver on the same
+    exchanger is stepped and closed first — its close must leave the fused
+    driver's peer mappings in place."""
+    env = {"KL_HALO_TRANSPORT": "fused", **({"KL_CHECK_SHARED": "1"} if shared else {})}
+    os.environ.update(env)
+    try:
+        codes, out, err = _spawn(nproc, "tests/multiproc_slab_check.py", "diff_uvw", precision, grid)
+    finally:
+        for k in env:
+            del os.environ[k]
+    assert codes == [0] * nproc, out[-2000:] + err[-3000:]
+    assert len(re.findall(r"rank \d+ ok ", out)) == nproc and "FAIL" not in out, out
+
+
 def test_ipc_probe_agrees_across_ranks():
     """IpcExchanger.probe: every rank maps its neighbours' memory, reads a
     marker value through the mapping and opens their interprocess events —

@@ -85,6 +85,61 @@ def test_virtual_ranks_match_single_grid(gpu_ctx, tmp_path, kernel, staging):
         drv.close()
 
 
+@pytest.mark.parametrize("precision", ["fp32", "fp64"])
+def test_fused_peer_halo_virtual_ranks_match_single_grid(gpu_ctx, tmp_path, precision):
+    """halo="fused": every virtual rank launches diff_uvw_peer ONCE over its
+    whole slab; the planes outside the slab come from the neighbours' fields
+    (LocalPeers: other allocations on this device), so the ghost planes are
+    poisoned and never exchanged — and the tendencies equal the undecomposed
+    grid's, for equal slabs (30 planes: 10/10/10) and unequal ones (31:
+    11/10/10, so a neighbour's allocation has another plane count)."""
+    from paper_2303_12374_b200.cuda import NvrtcCompiler
+    from paper_2303_12374_b200.halo import LocalPeers
+    from paper_2303_12374_b200.slab import SlabDriver
+    from paper_2303_12374_b200.stencils.definitions import definition_for
+    from paper_2303_12374_b200.wisdom import WisdomFile, WisdomRecord
+
+    comp = NvrtcCompiler(gpu_ctx)
+    d = definition_for("diff_uvw", precision)
+    cfg = dict(d.space.default_config()[0], staging="TMA", zchunk=8, block_x=32, block_y=4, depth=2)
+    WisdomFile(d.kernel_key(), records=[WisdomRecord(gpu_ctx.ident, (1, 1, 1), cfg, 1.0)]).save(
+        tmp_path / f"{d.kernel_key()}.wisdom")
+    for grid in ((64, 48, 30), (48, 40, 31)):
+        whole = SlabDriver("diff_uvw", precision, grid, gpu_ctx, compiler=comp, wisdom_dir=tmp_path)
+        whole.step()
+        gpu_ctx.synchronize()
+        ref = {n: whole.problem.download(n).copy() for n in whole.problem.outputs()}
+        whole.close()
+        nranks = 3
+        drivers = []
+        peers = LocalPeers([])
+        for r in range(nranks):
+            drv = SlabDriver("diff_uvw", precision, grid, gpu_ctx, rank=r, nranks=nranks, compiler=comp,
+                             wisdom_dir=tmp_path, halo="fused", exchanger=peers.for_rank(r))
+            drivers.append(drv)
+        peers.ranks = [({n: drv.problem.field_ptr(n) for n in ("evisc", "u", "v", "w")}, drv.layout.kstart,
+                        drv.layout.kend) for drv in drivers]
+        for drv in drivers:
+            _poison_ghosts(drv)
+        for drv in drivers:
+            drv.resolve()
+            assert set(drv.ranges) == {"slab"} and set(drv._bound) == {"slab"}
+            assert drv.step() == 1
+        gpu_ctx.synchronize()
+        g = drivers[0].layout.kgc
+        for drv in drivers:
+            off, count = drv.slab.offset, drv.slab.count
+            for name in ref:
+                got = drv.problem.download(name)[g:g + count]
+                want = ref[name][g + off:g + off + count]
+                err = np.max(np.abs(got - want)) / np.max(np.abs(want))
+                assert err <= 1e-13 if precision == "fp64" else err <= 1e-6, (grid, drv.rank, name, err)
+            rep = drv.wisdom.reports[0]
+            assert rep.configuration == cfg and rep.problem == (grid[0], grid[1], count)
+        for drv in drivers:
+            drv.close()
+
+
 def test_nccl_single_rank_exchange_is_a_noop(gpu_ctx):
     """The NCCL path end to end on one GPU: unique id, comm init, grouped
     send/recv call with no neighbours (the only topology one GPU allows)."""

@@ -34,7 +34,8 @@ def main():
     lay = GridLayout(*grid, a.precision)
     from paper_2303_12374_b200.stencils.definitions import ARG_LAYOUT
     nb = len(ARG_LAYOUT[a.kernel]["buffers"])
-    vals = dict(dxi=1.0, dyi=1.0, tpri=3.0, cs=0.23, rk_a=-5 / 9, rk_bdt=0.01, jj=lay.jj, kk=lay.kk, istart=lay.istart, jstart=lay.jstart, kstart=lay.kstart,
+    vals = dict(dxi=1.0, dyi=1.0, tpri=3.0, cs=0.23, rk_a=-5 / 9, rk_bdt=0.01, peer_klo=-(1 << 30), peer_khi=1 << 30,
+                peer_shift_lo=0, peer_shift_hi=0, jj=lay.jj, kk=lay.kk, istart=lay.istart, jstart=lay.jstart, kstart=lay.kstart,
                 iend=lay.iend, jend=lay.jend, kend=lay.kend)
     env = {f"arg{nb + i}": vals[n] for i, n in enumerate(ARG_LAYOUT[a.kernel]["scalars"])}
     problem = d.derive_problem_size(env)
