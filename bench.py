@@ -656,7 +656,9 @@ def run_ours(args, dist):
 
     # the fused halo (diff_uvw_peer reading the neighbours' planes through
     # IPC mappings) needs peer memory; with NCCL only the exchange runs
-    can_fuse = kernel == "diff_uvw" and dist.world > 1 and transport == "ipc"
+    from paper_2303_12374_b200.slab import FUSED_HALO
+
+    can_fuse = kernel in FUSED_HALO and dist.world > 1 and transport == "ipc"
     halo = args.halo if can_fuse else "exchange"
     variants = {}
     results = {}

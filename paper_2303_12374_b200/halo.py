@@ -54,6 +54,7 @@ HALO_REACH = {
     "evisc_smag": {"u": (1, 1), "v": (1, 1), "w": (1, 0)},
     "diff_uvw_rk3": {"evisc": (1, 1), "u": (1, 1), "v": (1, 1), "w": (1, 1)},
     "diff_uvw_peer": {"evisc": (1, 1), "u": (1, 1), "v": (1, 1), "w": (1, 1)},
+    "advec_u_peer": {"u": (3, 3), "w": (1, 0)},
     "rk3_uvw": {},
 }
 

@@ -11,7 +11,7 @@ Wires the pieces of ``halo.py`` to the runtime launch path:
   CUDA IPC, NCCL send/recv, or D2D copies for virtual ranks), the interior
   launch on the compute stream concurrently, then the boundary launches
   after the exchange event;
-* ``halo="fused"`` (diff_uvw): no exchange and no sub-ranges — ONE launch of
+* ``halo="fused"`` (diff_uvw, advec_u): no exchange and no sub-ranges — ONE launch of
   ``diff_uvw_peer`` over the whole slab, whose TMA staging reads the planes
   just outside the slab straight from the neighbours' fields through
   peer-mapped pointers (``IpcExchanger.peer_fields``; ``LocalPeers`` for
@@ -32,10 +32,14 @@ from .dispatch import WisdomKernel
 from .halo import HALO_REACH, SlabDecomposition, SlabRank
 from .stencils.definitions import definition_for
 from .stencils.layout import GridLayout
-from .stencils.problem import StencilProblem
+from .stencils.problem import PEER_KERNELS, StencilProblem
 from .stencils.profiles import make_profiles
 
-__all__ = ["SlabDriver"]
+__all__ = ["SlabDriver", "FUSED_HALO"]
+
+#: kernels with a fused-halo variant (the planes outside the slab read from
+#: the neighbours' fields inside the TMA staging) -> that variant
+FUSED_HALO = {"diff_uvw": "diff_uvw_peer", "advec_u": "advec_u_peer"}
 
 
 class SlabDriver:
@@ -46,8 +50,8 @@ class SlabDriver:
 
         if halo not in ("exchange", "fused"):
             raise ValueError(f"halo must be 'exchange' or 'fused', not {halo!r}")
-        if halo == "fused" and kernel != "diff_uvw":
-            raise ValueError("the fused halo (diff_uvw_peer) exists for diff_uvw")
+        if halo == "fused" and kernel not in FUSED_HALO:
+            raise ValueError(f"the fused halo exists for {tuple(FUSED_HALO)}")
         self.fused = halo == "fused"
         if self.fused and nranks > 1 and exchanger is None:
             raise ValueError("the fused halo needs an exchanger that maps the neighbours' fields")
@@ -62,11 +66,11 @@ class SlabDriver:
         profiles = make_profiles(self.global_layout.kcells, ghost)
         self.compute = ctx.stream
         self.comm = Stream.create() if exchanger is not None and not self.fused else None
-        self.problem = StencilProblem("diff_uvw_peer" if self.fused else kernel, self.layout, ctx,
+        self.problem = StencilProblem(FUSED_HALO[kernel] if self.fused else kernel, self.layout, ctx,
                                       k_offset=self.slab.offset, kcells_global=self.global_layout.kcells,
                                       profiles=profiles, stream=self.compute)
         self.compiler = compiler or NvrtcCompiler(ctx)
-        # the fused kernel selects from diff_uvw's wisdom (same space and problem sizes)
+        # the fused kernel selects from its base kernel's wisdom (same space and problem sizes)
         base_key = definition_for(kernel, precision).kernel_key() if self.fused else None
         self.wisdom = WisdomKernel(self.problem.definition, self.compiler, wisdom_dir=wisdom_dir or ".",
                                    capture_policy=CapturePolicy(), wisdom_key=base_key)
@@ -91,7 +95,7 @@ class SlabDriver:
         if self._peers_attached:
             return
         lay = self.layout
-        names = ("evisc", "u", "v", "w")
+        names = PEER_KERNELS[self.problem.kernel]
         got = self.exchanger.peer_fields({n: self.problem.field_ptr(n) for n in names}, lay.kstart, lay.kend)
         sides = {}
         for side, (ptrs, ks, ke) in got.items():

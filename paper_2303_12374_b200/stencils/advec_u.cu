@@ -26,6 +26,30 @@
 #define STAGING 0
 #endif
 
+// KL_PEER (kernel advec_u_peer): the z-slab halo fused into the TMA staging,
+// as diff_uvw_peer (diff_uvw.cu) — planes p < peer_klo of u (the chunk
+// prologue's loads) come from u_lo, planes p >= peer_khi of u and w (the
+// rings) from u_hi / w_hi, at the neighbour's plane p + peer_shift_lo/hi.
+// (w_lo is never read: w's reach is one plane up.)
+#ifndef KL_PEER
+#define KL_PEER 0
+#endif
+#if KL_PEER
+#if STAGING != 2
+#error "KL_PEER (advec_u_peer) reads the neighbours' planes in the TMA staging only"
+#endif
+#define KL_PEER_BUFFERS                                                                                \
+  , const real* __restrict__ u_lo, const real* __restrict__ w_lo, const real* __restrict__ u_hi,     \
+      const real* __restrict__ w_hi
+#define KL_PEER_SCALARS , const int peer_klo, const int peer_khi, const int peer_shift_lo, const int peer_shift_hi
+#else
+#define KL_PEER_BUFFERS
+#define KL_PEER_SCALARS
+#endif
+// argument positions (definitions.ARG_LAYOUT): 7 buffers (+4 peer), dxi, dyi (+4 peer scalars), jj, kk
+#define KL_POS_JJ (9 + 8 * KL_PEER)
+#define KL_POS_KK (KL_POS_JJ + 1)
+
 namespace {
 
 template <bool kTrap>

@@ -121,6 +121,10 @@ __device__ __forceinline__ void st_span(real* d, const real (&s)[kTX]) {
 struct AdvecTma {
   real* ut;
   const real* u;
+#if KL_PEER
+  const real *u_lo, *u_hi;  // the neighbours' u (the prologue's planes outside the slab)
+  int peer_klo, peer_khi, peer_shift_lo, peer_shift_hi;
+#endif
   const real* rhoref;
   const real* rhorefh;
   const real* dzi;
@@ -137,6 +141,12 @@ struct AdvecTma {
 
   __device__ __forceinline__ void issue_u(int slot, int p) const {
     kl::mbar_expect_tx(bar_u + slot, kTxU);
+#if KL_PEER
+    if (p >= peer_khi) {  // above the slab: the neighbour's u (map 4)
+      kl::tma_load_3d(ring_u + slot * kUS, maps + 4, bar_u + slot, xu, j0 - 3, p + peer_shift_hi);
+      return;
+    }
+#endif
     kl::tma_load_3d(ring_u + slot * kUS, maps + 0, bar_u + slot, xu, j0 - 3, p);
   }
   __device__ __forceinline__ void issue_v(int slot, int p) const {
@@ -144,8 +154,23 @@ struct AdvecTma {
     real* dst = ring_v + slot * kVS;
     kl::mbar_expect_tx(bar, kTxV);
     kl::tma_load_3d(dst + kVO, maps + 1, bar, xv, j0, p);
-    kl::tma_load_3d(dst + kWO, maps + 2, bar, xw, j0, p);
+#if KL_PEER
+    if (p >= peer_khi)  // above the slab: the neighbour's w (map 5); v / ut of that plane are never read
+      kl::tma_load_3d(dst + kWO, maps + 5, bar, xw, j0, p + peer_shift_hi);
+    else
+#endif
+      kl::tma_load_3d(dst + kWO, maps + 2, bar, xw, j0, p);
     kl::tma_load_3d(dst + kTO, maps + 3, bar, xt, j0, p);
+  }
+  // u of plane k0 + d at element offset b of plane k0 (the chunk prologue's
+  // unstaged loads, planes k0-3 .. k0+2: below the slab for the first chunk,
+  // above it for a last chunk shorter than 3 planes — from the neighbours)
+  __device__ __forceinline__ real u_at(long long b, int d) const {
+#if KL_PEER
+    if (k0 + d < peer_klo) return u_lo[b + static_cast<long long>(d + peer_shift_lo) * KL_KK];
+    if (k0 + d >= peer_khi) return u_hi[b + static_cast<long long>(d + peer_shift_hi) * KL_KK];
+#endif
+    return u[b + static_cast<long long>(d) * KL_KK];
   }
   // first fills: u planes k0 .. k1+2 (the last the z-window reads), v/w/ut
   // planes k0 .. k1 (w of plane k1 feeds the last step's top face)
@@ -226,9 +251,9 @@ struct AdvecTma {
         for (int c = 0; c < kTX; ++c) {
           const int i = min(ic + c, iend - 1);
           const long long b = i + static_cast<long long>(j) * KL_JJ + static_cast<long long>(k0) * KL_KK;
-          const real um3 = u[b - 3 * K1];  // planes below the chunk: not staged
+          const real um3 = u_at(b, -3);  // planes below the chunk: not staged
 #pragma unroll
-          for (int m = 0; m < 5; ++m) uq[t][c][m] = u[b + (m - 2) * K1];
+          for (int m = 0; m < 5; ++m) uq[t][c][m] = u_at(b, m - 2);
           fz_bot[t][c] = rh0 * kl::flux5x60(wr[3 + c] + wr[4 + c], um3, uq[t][c][0], uq[t][c][1], uq[t][c][2],
                                             uq[t][c][3], uq[t][c][4]);
         }
@@ -363,9 +388,9 @@ struct AdvecTma {
           const int c = 2 * p;
           const long long rowk = static_cast<long long>(j) * KL_JJ + static_cast<long long>(k0) * KL_KK;
           const long long b0 = min(ic + c, iend - 1) + rowk, b1 = min(ic + c + 1, iend - 1) + rowk;
-          const f2 um3(u[b0 - 3 * K1], u[b1 - 3 * K1]);  // planes below the chunk: not staged
+          const f2 um3(u_at(b0, -3), u_at(b1, -3));  // planes below the chunk: not staged
 #pragma unroll
-          for (int m = 0; m < 5; ++m) uq[t][p][m] = f2(u[b0 + (m - 2) * K1], u[b1 + (m - 2) * K1]);
+          for (int m = 0; m < 5; ++m) uq[t][p][m] = f2(u_at(b0, m - 2), u_at(b1, m - 2));
           const f2 vel(wr[3 + c] + wr[4 + c], wr[4 + c] + wr[5 + c]);
           fz_bot[t][p] = rh0 * kl::flux5x60(vel, um3, uq[t][p][0], uq[t][p][1], uq[t][p][2], uq[t][p][3],
                                              uq[t][p][4]);
@@ -511,19 +536,29 @@ struct Marcher<true> {
 };
 }  // namespace
 
-// positions: ut=0 u=1 v=2 w=3, jj=9 kk=10 (definitions.ARG_LAYOUT["advec_u"])
-extern "C" __device__ const int kl_tma_spec[1 + 5 * 4] = {4, 1, 9, 10, kBW, kBH, 2, 9, 10, kVW, kTYT + 1,
-                                                          3, 9, 10, kVW, kTYT, 0, 9, 10, kTW, kTYT};
+// positions: ut=0 u=1 v=2 w=3, jj / kk = KL_POS_JJ / KL_POS_KK (definitions.ARG_LAYOUT["advec_u"],
+// ["advec_u_peer"]: + u_hi = 9, w_hi = 10 as maps 4, 5)
+#define KL_J KL_POS_JJ
+#define KL_K KL_POS_KK
+#define KL_NMAPS (4 + 2 * KL_PEER)
+extern "C" __device__ const int kl_tma_spec[1 + 5 * KL_NMAPS] = {
+    KL_NMAPS, 1, KL_J, KL_K, kBW, kBH, 2, KL_J, KL_K, kVW, kTYT + 1, 3, KL_J, KL_K, kVW, kTYT, 0, KL_J, KL_K, kTW, kTYT
+#if KL_PEER
+    , 9, KL_J, KL_K, kBW, kBH, 10, KL_J, KL_K, kVW, kTYT
+#endif
+};
+#undef KL_J
+#undef KL_K
 struct __align__(64) KlTmaParams {
-  TmaDesc map[4];
+  TmaDesc map[KL_NMAPS];
 };
 
 extern "C" __global__ void __launch_bounds__(KL_THREADS, MIN_BLOCKS)
 KL_ENTRY(real* __restrict__ ut, const real* __restrict__ u, const real* __restrict__ v,
          const real* __restrict__ w, const real* __restrict__ rhoref, const real* __restrict__ rhorefh,
-         const real* __restrict__ dzi, const real dxi, const real dyi, const int jj, const int kk,
-         const int istart, const int jstart, const int kstart, const int iend, const int jend,
-         const int kend, const __grid_constant__ KlTmaParams tma) {
+         const real* __restrict__ dzi KL_PEER_BUFFERS, const real dxi, const real dyi KL_PEER_SCALARS,
+         const int jj, const int kk, const int istart, const int jstart, const int kstart, const int iend,
+         const int jend, const int kend, const __grid_constant__ KlTmaParams tma) {
   if (jj != KL_JJ || kk != KL_KK) __trap();
   const kl::PdlTriggerAtExit kl_pdl_exit;  // programmatic dependent launch (kl_common.cuh)
   kl::pdl_wait();     // no global access before the previous kernel on the stream has completed
@@ -563,6 +598,14 @@ KL_ENTRY(real* __restrict__ ut, const real* __restrict__ u, const real* __restri
   AdvecTma m;
   m.ut = ut;
   m.u = u;
+#if KL_PEER
+  m.u_lo = u_lo;
+  m.u_hi = u_hi;
+  m.peer_klo = peer_klo;
+  m.peer_khi = peer_khi;
+  m.peer_shift_lo = peer_shift_lo;
+  m.peer_shift_hi = peer_shift_hi;
+#endif
   m.rhoref = rhoref;
   m.rhorefh = rhorefh;
   m.dzi = dzi;

@@ -61,8 +61,10 @@ PLANE_FAMILY = {"diff_c": (2, 1, 3), "evisc_smag": (3, 0, 2)}
 #: staging families as their base kernel, compiled with a -D switch
 FUSED_KERNELS = {"diff_uvw_rk3": ("diff_uvw", "KL_RK3"),
                  # z-slab halo fused into the TMA staging: planes outside the
-                 # slab are read from the neighbours' fields (diff_uvw.cu KL_PEER)
-                 "diff_uvw_peer": ("diff_uvw", "KL_PEER")}
+                 # slab are read from the neighbours' fields (diff_uvw.cu /
+                 # advec_u.cu KL_PEER)
+                 "diff_uvw_peer": ("diff_uvw", "KL_PEER"),
+                 "advec_u_peer": ("advec_u", "KL_PEER")}
 ALL_KERNELS = KERNELS + tuple(FUSED_KERNELS) + FAMILY_KERNELS
 
 
@@ -130,6 +132,13 @@ ARG_LAYOUT = {
                     ("rhorefh", "input"), ("u_next", "output"), ("v_next", "output"), ("w_next", "output")],
         "scalars": ["dxi", "dyi", "rk_a", "rk_bdt", "jj", "kk", "istart", "jstart", "kstart", "iend", "jend",
                     "kend"],
+    },
+    "advec_u_peer": {
+        "buffers": [("ut", "output"), ("u", "input"), ("v", "input"), ("w", "input"),
+                    ("rhoref", "input"), ("rhorefh", "input"), ("dzi", "input"), ("u_lo", "input"),
+                    ("w_lo", "input"), ("u_hi", "input"), ("w_hi", "input")],
+        "scalars": ["dxi", "dyi", "peer_klo", "peer_khi", "peer_shift_lo", "peer_shift_hi", "jj", "kk", "istart",
+                    "jstart", "kstart", "iend", "jend", "kend"],
     },
     "diff_uvw_peer": {
         "buffers": [("ut", "output"), ("vt", "output"), ("wt", "output"), ("evisc", "input"), ("u", "input"),
@@ -429,6 +438,7 @@ def _plane_family_smem(kernel: str) -> str:
 
 def _definition(kernel: str, precision: str) -> KernelDefinition:
     space = stencil_space(kernel, precision)
+    bk = base_kernel(kernel)  # fused variants take their base kernel's knobs and grid
     p = lambda n: f"arg{_pos(kernel, n)}"  # noqa: E731
     size = 4 if precision == "fp32" else 8
     # z extent of one block: block_z*tile_z under DIRECT (zchunk pinned to 1),
@@ -437,10 +447,10 @@ def _definition(kernel: str, precision: str) -> KernelDefinition:
         "ceil_div(problem_x, block_x * tile_x) * ceil_div(problem_y, block_y * tile_y) * "
         "ceil_div(problem_z, block_z * tile_z * zchunk)"
     )
-    if kernel in XSHARE_KERNELS:
+    if bk in XSHARE_KERNELS:
         grid_x = grid_x.replace("ceil_div(problem_x, block_x * tile_x)",
                                 "ceil_div(problem_x, block_x * tile_x - xshare * (block_x / 32))")
-    if kernel in YSPLIT_KERNELS:
+    if bk in YSPLIT_KERNELS:
         nbxz = "(ceil_div(problem_x, block_x * tile_x) * ceil_div(problem_z, block_z * tile_z * zchunk))"
         # at least the natural count (<= block_y*tile_y rows per run), at most
         # problem_y runs (every run holds a row)
@@ -454,8 +464,8 @@ def _definition(kernel: str, precision: str) -> KernelDefinition:
         ("UNRAVEL", "unravel"), ("MIN_BLOCKS", "min_blocks"),
         ("STAGING", "staging"), ("ZCHUNK", "zchunk"), ("DEPTH", "depth"),
         ("KL_JJ", p("jj")), ("KL_KK", p("kk")),
-    ] + ([("KL_YBAL", "ysplit")] if kernel in YSPLIT_KERNELS else []) + (
-        [("KL_XSHARE", "xshare")] if kernel in XSHARE_KERNELS else [])
+    ] + ([("KL_YBAL", "ysplit")] if bk in YSPLIT_KERNELS else []) + (
+        [("KL_XSHARE", "xshare")] if bk in XSHARE_KERNELS else [])
     return KernelDefinition(
         f"{kernel}_{precision}",
         space,

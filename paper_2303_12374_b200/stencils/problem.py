@@ -25,7 +25,7 @@ from .definitions import ARG_LAYOUT, definition_for
 from .layout import GridLayout
 from .profiles import FIELD_SEED_BASE, FIELD_SPECS, Profiles, make_profiles
 
-__all__ = ["StencilProblem", "KERNEL_FIELDS", "BYTES_PER_CELL_WORDS"]
+__all__ = ["StencilProblem", "KERNEL_FIELDS", "BYTES_PER_CELL_WORDS", "PEER_KERNELS"]
 
 KERNEL_FIELDS = {
     "advec_u": ("ut", "u", "v", "w"),
@@ -37,6 +37,7 @@ KERNEL_FIELDS = {
     "evisc_smag": ("evisc", "u", "v", "w"),
     "diff_uvw_rk3": ("ut", "vt", "wt", "evisc", "u", "v", "w", "u_next", "v_next", "w_next"),
     "diff_uvw_peer": ("ut", "vt", "wt", "evisc", "u", "v", "w"),
+    "advec_u_peer": ("ut", "u", "v", "w"),
     "rk3_uvw": ("ut", "vt", "wt", "u", "v", "w"),
 }
 #: algorithmic HBM words per interior cell: advec_u reads u,v,w,ut
@@ -48,7 +49,7 @@ BYTES_PER_CELL_WORDS = {"advec_u": 5, "diff_uvw": 10, "advec_v": 5, "advec_w": 5
                         # diff_uvw + RK3 epilogue: reads evisc,u,v,w,ut,vt,wt, writes ut,vt,wt,u',v',w'
                         "diff_uvw_rk3": 13,
                         # diff_uvw with its z-halo read from the neighbours' fields: same words per cell
-                        "diff_uvw_peer": 10,
+                        "diff_uvw_peer": 10, "advec_u_peer": 5,
                         # the separate RK3 pass: read + write u,v,w,ut,vt,wt
                         "rk3_uvw": 12}
 #: MicroHH defaults of the model constants the family kernels take
@@ -59,8 +60,10 @@ CS = 0.23   # Smagorinsky constant
 RK_A = -5.0 / 9.0
 RK_BDT = 15.0 / 16.0 * 0.01
 _PROFILE_FIELDS = ("rhoref", "rhorefh", "dzi", "dzhi")
-#: diff_uvw_peer's neighbour-field arguments -> the local field they mirror
+#: the fused-halo kernels' neighbour-field arguments -> the local field they mirror
 _PEER_FIELDS = {f"{f}_{side}": f for side in ("lo", "hi") for f in ("evisc", "u", "v", "w")}
+#: fields each fused-halo kernel reads from its neighbours (its halo'd inputs)
+PEER_KERNELS = {"diff_uvw_peer": ("evisc", "u", "v", "w"), "advec_u_peer": ("u", "w")}
 #: peer_klo / peer_khi of a side without a neighbour: a plane no launch reaches
 _NO_PEER = 1 << 30
 
@@ -172,16 +175,16 @@ class StencilProblem:
         return out
 
     def set_peers(self, below=None, above=None) -> None:
-        """diff_uvw_peer: read the planes outside this slab from the
-        neighbours' fields.  ``below`` / ``above`` = ``(pointers, element
-        count, plane)``: the neighbour's field pointers of element (0,0,0) by
-        name (evisc, u, v, w; device memory this context can address — a CUDA
+        """diff_uvw_peer / advec_u_peer: read the planes outside this slab
+        from the neighbours' fields.  ``below`` / ``above`` = ``(pointers,
+        element count, plane)``: the neighbour's field pointers of element
+        (0,0,0) by name (``PEER_KERNELS[kernel]``; device memory this context can address — a CUDA
         IPC mapping or another allocation of this device), the element count
         from there (its ``layout.span_elems``) and its local ``kend`` (below)
         / ``kstart`` (above), so that local plane ``kstart - 1`` maps to
         ``kend_below - 1`` and ``kend`` to ``kstart_above``."""
-        if self.kernel != "diff_uvw_peer":
-            raise ValueError("set_peers applies to diff_uvw_peer")
+        if self.kernel not in PEER_KERNELS:
+            raise ValueError(f"set_peers applies to the fused-halo kernels {tuple(PEER_KERNELS)}")
         lay = self.layout
         peers: dict[str, tuple[int, int]] = {}
         klo, khi, shlo, shhi = -_NO_PEER, _NO_PEER, 0, 0
@@ -189,7 +192,7 @@ class StencilProblem:
             if info is None:
                 continue
             ptrs, count, plane = info
-            for f in ("evisc", "u", "v", "w"):
+            for f in PEER_KERNELS[self.kernel]:
                 if (ptrs[f] - self.field_ptr(f)) % 16:
                     raise ValueError(f"peer {f}_{side} has another 16-byte phase than the local field")
                 peers[f"{f}_{side}"] = (int(ptrs[f]), int(count))

@@ -73,11 +73,13 @@ def test_spawned_ranks_without_torch_match_oracle(kernel, precision, grid, nproc
     assert len(re.findall(r"rank \d+ ok ", out)) == nproc and "FAIL" not in out, out
 
 
-@pytest.mark.parametrize("precision,grid,nproc,shared", [("fp32", "64,40,30", 3, False),
-                                                         ("fp64", "40,24,36", 2, False),
-                                                         ("fp32", "48,32,20", 2, True)])
-def test_fused_peer_halo_ranks_match_oracle(precision, grid, nproc, shared):
-    """diff_uvw with the z-halo fused into the kernel: one launch per rank
+@pytest.mark.parametrize("kernel,precision,grid,nproc,shared", [("diff_uvw", "fp32", "64,40,30", 3, False),
+                                                                ("diff_uvw", "fp64", "40,24,36", 2, False),
+                                                                ("diff_uvw", "fp32", "48,32,20", 2, True),
+                                                                ("advec_u", "fp32", "64,48,40", 3, False),
+                                                                ("advec_u", "fp64", "48,32,30", 2, True)])
+def test_fused_peer_halo_ranks_match_oracle(kernel, precision, grid, nproc, shared):
+    """diff_uvw / advec_u with the z-halo fused into the kernel: one launch per rank
     over its whole slab, the planes outside the slab read through CUDA-IPC
     mappings of the neighbours' fields (the local ghost planes are poisoned
     and never read).  ``shared``: an exchange-mode driver on the same
@@ -86,7 +88,7 @@ def test_fused_peer_halo_ranks_match_oracle(precision, grid, nproc, shared):
     env = {"KL_HALO_TRANSPORT": "fused", **({"KL_CHECK_SHARED": "1"} if shared else {})}
     os.environ.update(env)
     try:
-        codes, out, err = _spawn(nproc, "tests/multiproc_slab_check.py", "diff_uvw", precision, grid)
+        codes, out, err = _spawn(nproc, "tests/multiproc_slab_check.py", kernel, precision, grid)
     finally:
         for k in env:
             del os.environ[k]

@@ -85,10 +85,11 @@ def test_virtual_ranks_match_single_grid(gpu_ctx, tmp_path, kernel, staging):
         drv.close()
 
 
-@pytest.mark.parametrize("precision", ["fp32", "fp64"])
-def test_fused_peer_halo_virtual_ranks_match_single_grid(gpu_ctx, tmp_path, precision):
-    """halo="fused": every virtual rank launches diff_uvw_peer ONCE over its
-    whole slab; the planes outside the slab come from the neighbours' fields
+@pytest.mark.parametrize("kernel,precision", [("diff_uvw", "fp32"), ("diff_uvw", "fp64"), ("advec_u", "fp32"),
+                                              ("advec_u", "fp64")])
+def test_fused_peer_halo_virtual_ranks_match_single_grid(gpu_ctx, tmp_path, kernel, precision):
+    """halo="fused": every virtual rank launches diff_uvw_peer / advec_u_peer
+    ONCE over its whole slab; the planes outside the slab come from the neighbours' fields
     (LocalPeers: other allocations on this device), so the ghost planes are
     poisoned and never exchanged — and the tendencies equal the undecomposed
     grid's, for equal slabs (30 planes: 10/10/10) and unequal ones (31:
@@ -99,13 +100,19 @@ def test_fused_peer_halo_virtual_ranks_match_single_grid(gpu_ctx, tmp_path, prec
     from paper_2303_12374_b200.stencils.definitions import definition_for
     from paper_2303_12374_b200.wisdom import WisdomFile, WisdomRecord
 
+    from paper_2303_12374_b200.stencils.problem import PEER_KERNELS
+
     comp = NvrtcCompiler(gpu_ctx)
-    d = definition_for("diff_uvw", precision)
+    d = definition_for(kernel, precision)
     cfg = dict(d.space.default_config()[0], staging="TMA", zchunk=8, block_x=32, block_y=4, depth=2)
+    if kernel == "advec_u":  # column pairs: the packed fp32 main loop
+        cfg.update(tile_x=2, contiguous_x=True, block_x=16)
+    assert d.space.is_valid(cfg), cfg
     WisdomFile(d.kernel_key(), records=[WisdomRecord(gpu_ctx.ident, (1, 1, 1), cfg, 1.0)]).save(
         tmp_path / f"{d.kernel_key()}.wisdom")
+    fields = PEER_KERNELS[f"{kernel}_peer"]
     for grid in ((64, 48, 30), (48, 40, 31)):
-        whole = SlabDriver("diff_uvw", precision, grid, gpu_ctx, compiler=comp, wisdom_dir=tmp_path)
+        whole = SlabDriver(kernel, precision, grid, gpu_ctx, compiler=comp, wisdom_dir=tmp_path)
         whole.step()
         gpu_ctx.synchronize()
         ref = {n: whole.problem.download(n).copy() for n in whole.problem.outputs()}
@@ -114,11 +121,11 @@ def test_fused_peer_halo_virtual_ranks_match_single_grid(gpu_ctx, tmp_path, prec
         drivers = []
         peers = LocalPeers([])
         for r in range(nranks):
-            drv = SlabDriver("diff_uvw", precision, grid, gpu_ctx, rank=r, nranks=nranks, compiler=comp,
+            drv = SlabDriver(kernel, precision, grid, gpu_ctx, rank=r, nranks=nranks, compiler=comp,
                              wisdom_dir=tmp_path, halo="fused", exchanger=peers.for_rank(r))
             drivers.append(drv)
-        peers.ranks = [({n: drv.problem.field_ptr(n) for n in ("evisc", "u", "v", "w")}, drv.layout.kstart,
-                        drv.layout.kend) for drv in drivers]
+        peers.ranks = [({n: drv.problem.field_ptr(n) for n in fields}, drv.layout.kstart, drv.layout.kend)
+                       for drv in drivers]
         for drv in drivers:
             _poison_ghosts(drv)
         for drv in drivers:

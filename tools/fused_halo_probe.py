@@ -1,8 +1,8 @@
 """Per-rank step of the z-slab decomposition on ONE GPU: the exchange variant
 (interior launch + the two boundary launches; the plane copies overlap the
 interior on a real multi-GPU box, so they are not on this clock) against the
-fused halo (one diff_uvw_peer launch over the whole slab reading the planes
-outside it from the neighbours' fields).  The middle rank of an N-way split
+fused halo (one diff_uvw_peer / advec_u_peer launch over the whole slab
+reading the planes outside it from the neighbours' fields).  The middle rank of an N-way split
 is built with its two neighbours as virtual ranks (LocalPeers), its step timed
 with CUDA events (L2 flushed between steps), and its outputs checked against
 the exchange variant's.  GPU only.
@@ -24,6 +24,7 @@ sys.path.insert(0, str(ROOT))
 
 def main(argv=None) -> int:
     ap = argparse.ArgumentParser()
+    ap.add_argument("--kernel", default="diff_uvw", choices=("diff_uvw", "advec_u"))
     ap.add_argument("--precision", default="fp32")
     ap.add_argument("--grid", default="1024,1024,1024")
     ap.add_argument("--ranks", default="2,4,8")
@@ -36,7 +37,8 @@ def main(argv=None) -> int:
     from paper_2303_12374_b200.cuda import Event, NvrtcCompiler, open_device
     from paper_2303_12374_b200.cuda._abi import check, lib
     from paper_2303_12374_b200.halo import CopyExchanger, HALO_REACH, LocalPeers
-    from paper_2303_12374_b200.slab import SlabDriver
+    from paper_2303_12374_b200.slab import FUSED_HALO, SlabDriver
+    from paper_2303_12374_b200.stencils.problem import PEER_KERNELS
 
     ctx = open_device(0)
     comp = NvrtcCompiler(ctx)
@@ -61,20 +63,20 @@ def main(argv=None) -> int:
     for n in (int(x) for x in a.ranks.split(",")):
         mid = n // 2
         ids = [r for r in (mid - 1, mid, mid + 1) if 0 <= r < n]
-        rec = {"precision": a.precision, "grid": list(grid), "nranks": n, "rank": mid}
+        rec = {"kernel": a.kernel, "precision": a.precision, "grid": list(grid), "nranks": n, "rank": mid}
         for halo in ("exchange", "fused"):
             peers = LocalPeers([])
-            drivers = {r: SlabDriver("diff_uvw", a.precision, grid, ctx, rank=r, nranks=n, compiler=comp,
+            drivers = {r: SlabDriver(a.kernel, a.precision, grid, ctx, rank=r, nranks=n, compiler=comp,
                                      wisdom_dir=ROOT / "wisdom", halo=halo,
                                      exchanger=peers.for_rank(ids.index(r)) if halo == "fused" else None)
                        for r in ids}
-            peers.ranks = [({f: drivers[r].problem.field_ptr(f) for f in ("evisc", "u", "v", "w")},
+            peers.ranks = [({f: drivers[r].problem.field_ptr(f) for f in PEER_KERNELS[FUSED_HALO[a.kernel]]},
                             drivers[r].layout.kstart, drivers[r].layout.kend) for r in ids]
             if halo == "exchange":  # fill the middle rank's ghost planes once (its own copies, untimed)
                 lay = drivers[mid].layout
-                ex = CopyExchanger([{f: drivers[r].problem.field_ptr(f) for f in HALO_REACH["diff_uvw"]}
+                ex = CopyExchanger([{f: drivers[r].problem.field_ptr(f) for f in HALO_REACH[a.kernel]}
                                     for r in ids])
-                ex.exchange_all(ctx.stream, HALO_REACH["diff_uvw"], lay.elem_bytes, lay.kk,
+                ex.exchange_all(ctx.stream, HALO_REACH[a.kernel], lay.elem_bytes, lay.kk,
                                 [(drivers[r].layout.kstart, drivers[r].layout.kend) for r in ids])
             d = drivers[mid]
             sel = d.resolve()
