@@ -143,3 +143,20 @@ def test_cli_checkpoint_and_resume(tmp_path, monkeypatch):
     assert len(load_checkpoint("part.klsession").evaluations) == 12
     assert cli.main(common + ["--budget-evals", "30", "--resume", "part.klsession"]) == 0
     assert session_fingerprint("part.klsession") == session_fingerprint("full.klsession")
+
+
+def test_resuming_into_the_same_file_never_truncates_it(tmp_path):
+    """A resumed run that dies before its first new measurement leaves the
+    checkpoint it resumed from intact (the prefix is rewritten to a temporary
+    file and renamed over it)."""
+    space = stencil3d_space(True)
+    ck = tmp_path / "ck.klsession"
+    kw = dict(strategy="random", seed=9, kernel_key="k", budget=Budget(30, None), checkpoint=ck)
+    with pytest.raises(Crash):
+        tune(space, CountingExecutor(SimCostModel(2, space), die_after=7), **kw)
+    prefix = load_checkpoint(ck)
+    with pytest.raises(Crash):
+        tune(space, CountingExecutor(SimCostModel(2, space), die_after=0), resume=prefix, **kw)
+    again = load_checkpoint(ck)
+    assert [e.config for e in again.evaluations] == [e.config for e in prefix.evaluations]
+    assert not (tmp_path / "ck.klsession.part").exists()
