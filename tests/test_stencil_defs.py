@@ -223,3 +223,36 @@ def test_evisc_xshare_grid_counts_31_columns_per_warp():
     assert g0 == 4 * 64 * 8 and g1 == 5 * 64 * 8  # ceil(512 / 124) = 5 blocks along x
     assert "-D KL_XSHARE=1" in d.render_compile_request(dict(cfg, xshare=1), (512, 512, 512), env).defines
     assert not d.space.is_valid(dict(cfg, xshare=1, tile_x=2, contiguous_x=True))
+
+
+@pytest.mark.parametrize("fused,base", [("diff_uvw_peer", "diff_uvw"), ("advec_u_peer", "advec_u"),
+                                        ("diff_uvw_rk3", "diff_uvw")])
+@pytest.mark.parametrize("precision", PRECISIONS)
+def test_fused_variants_share_their_base_kernel_space_and_launch(fused, base, precision):
+    """A fused variant selects from its base kernel's wisdom (slab.SlabDriver,
+    build()): same space fingerprint, and for the same configuration and
+    problem the same grid, block, shared memory and tunable defines."""
+    from paper_2303_12374_b200.stencils.layout import GridLayout
+
+    fd, bd = definition_for(fused, precision), definition_for(base, precision)
+    assert fd.space.fingerprint() == bd.space.fingerprint()
+    lay = GridLayout(256, 192, 128, precision)
+    vals = dict(dxi=1.0, dyi=1.0, rk_a=0.5, rk_bdt=0.01, jj=lay.jj, kk=lay.kk, istart=lay.istart,
+                jstart=lay.jstart, kstart=lay.kstart, iend=lay.iend, jend=lay.jend, kend=lay.kend,
+                peer_klo=lay.kstart, peer_khi=lay.kend, peer_shift_lo=5, peer_shift_hi=-5)
+
+    def env(k):
+        nb = len(ARG_LAYOUT[k]["buffers"])
+        return {f"arg{nb + i}": vals[n] for i, n in enumerate(ARG_LAYOUT[k]["scalars"])}
+
+    extra = {"ysplit": 2} if "ysplit" in bd.space.param_names else {}
+    cands = [dict(bd.space.default_config()[0], staging="TMA", zchunk=z, depth=1, block_x=32, block_y=4,
+                  tile_x=tx, tile_y=2, contiguous_x=True, **extra) for tx, z in ((4, 64), (2, 32))]
+    cfg = next(c for c in cands if bd.space.is_valid(c))
+    pf, pb = fd.derive_problem_size(env(fused)), bd.derive_problem_size(env(base))
+    assert pf == pb
+    gf, gb = fd.derive_geometry(cfg, pf, env(fused)), bd.derive_geometry(cfg, pb, env(base))
+    assert (gf.grid, gf.block, gf.shared_mem_bytes) == (gb.grid, gb.block, gb.shared_mem_bytes)
+    df = set(fd.render_compile_request(cfg, pf, env(fused)).defines)
+    db = set(bd.render_compile_request(cfg, pb, env(base)).defines)
+    assert df == db
