@@ -206,6 +206,14 @@ int klb_compare_fields(uint64_t a, uint64_t b, int elem_bytes, long long base_of
                        int jj, long long kk, double* max_abs_diff, double* max_abs_ref,
                        klb_stream stream);
 
+/* Periodic (MicroHH boundary_cyclic) x/y ghost fill of planes [k0, k1) of a
+ * ghost-padded field: every ghost cell (i < igc or i >= icells - igc, likewise
+ * j) receives the interior cell it wraps onto.  The step between two RK3
+ * substeps of a time loop (slab.SlabDriver.rk3_substep); no reference
+ * counterpart (the reference has no stencils). */
+int klb_cyclic_xy(uint64_t dptr, int elem_bytes, long long base_offset, int icells, int jcells, int jj,
+                  long long kk, int igc, int jgc, int k0, int k1, klb_stream stream);
+
 /* zlib-compatible CRC-32 of nbytes of device memory (capture payload
  * checksums computed where the data lives): per-chunk CRC
  * registers on the GPU, chained on the host with the zero-append operator.

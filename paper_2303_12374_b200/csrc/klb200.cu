@@ -222,6 +222,36 @@ __global__ void synth_kernel(T* __restrict__ base, long long total, int icells, 
   }
 }
 
+// x/y ghost cells of planes [k0, k1): one thread per ghost cell, copying the
+// interior cell it wraps onto (ghost cells are never a source, so one pass)
+template <typename T>
+__global__ void cyclic_xy_kernel(T* __restrict__ base, int icells, int jcells, int jj, long long kk, int igc,
+                                 int jgc, int k0, long long total) {
+  const int itot = icells - 2 * igc, jtot = jcells - 2 * jgc;
+  const long long per_plane = static_cast<long long>(icells) * jcells - static_cast<long long>(itot) * jtot;
+  for (long long t = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; t < total;
+       t += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int k = k0 + static_cast<int>(t / per_plane);
+    long long r = t % per_plane;
+    int i, j;
+    const long long band = static_cast<long long>(jgc) * icells;  // full ghost rows below / above
+    if (r < 2 * band) {
+      j = static_cast<int>(r / icells);
+      i = static_cast<int>(r % icells);
+      if (j >= jgc) j += jtot;  // the upper band
+    } else {
+      r -= 2 * band;  // rows jgc .. jcells-jgc-1: igc ghost columns on each side
+      j = jgc + static_cast<int>(r / (2 * igc));
+      const int c = static_cast<int>(r % (2 * igc));
+      i = c < igc ? c : itot + c;
+    }
+    const int is = igc + ((i - igc) % itot + itot) % itot;
+    const int js = jgc + ((j - jgc) % jtot + jtot) % jtot;
+    const long long plane = static_cast<long long>(k) * kk;
+    base[i + static_cast<long long>(j) * jj + plane] = base[is + static_cast<long long>(js) * jj + plane];
+  }
+}
+
 __device__ __forceinline__ void atomic_max_nonneg(double* addr, double v) {
   // IEEE ordering of non-negative doubles equals unsigned ordering of their bits.
   atomicMax(reinterpret_cast<unsigned long long*>(addr), static_cast<unsigned long long>(__double_as_longlong(v)));
@@ -845,6 +875,31 @@ int klb_compare_fields(uint64_t a, uint64_t b, int elem_bytes, long long base_of
   if (e != cudaSuccess) return fail(static_cast<int>(e), "compare_fields: %s", cudaGetErrorString(e));
   *max_abs_diff = host[0];
   *max_abs_ref = host[1];
+  return 0;
+}
+
+int klb_cyclic_xy(uint64_t dptr, int elem_bytes, long long base_offset, int icells, int jcells, int jj,
+                  long long kk, int igc, int jgc, int k0, int k1, klb_stream stream) {
+  if (elem_bytes != 4 && elem_bytes != 8) return fail(KLB_E_INVALID, "elem_bytes must be 4 or 8");
+  if (igc < 0 || jgc < 0 || icells <= 2 * igc || jcells <= 2 * jgc || jj < icells ||
+      kk < static_cast<long long>(jj) * jcells || k1 < k0)
+    return fail(KLB_E_INVALID, "klb_cyclic_xy: inconsistent field layout");
+  const long long per_plane = static_cast<long long>(icells) * jcells -
+                              static_cast<long long>(icells - 2 * igc) * (jcells - 2 * jgc);
+  const long long total = per_plane * (k1 - k0);
+  if (total == 0) return 0;
+  CTX_TRY();
+  const int threads = 256;
+  const int blocks = grid_for(total, threads);
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (elem_bytes == 4)
+    cyclic_xy_kernel<float><<<blocks, threads, 0, s>>>(reinterpret_cast<float*>(dptr) + base_offset, icells, jcells,
+                                                       jj, kk, igc, jgc, k0, total);
+  else
+    cyclic_xy_kernel<double><<<blocks, threads, 0, s>>>(reinterpret_cast<double*>(dptr) + base_offset, icells,
+                                                        jcells, jj, kk, igc, jgc, k0, total);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(static_cast<int>(e), "cyclic_xy_kernel launch: %s", cudaGetErrorString(e));
   return 0;
 }
 

@@ -118,6 +118,7 @@ EXPORTS: dict[str, list] = {
     "klb_tensor_map_encode_3d": [_vp, _i, _u64, C.POINTER(_u64), C.POINTER(_u64), C.POINTER(C.c_uint)],
     "klb_synth_field": [_u64, _i, _ll, _i, _i, _i, _i, _ll, _i, _i, _i, _i, _u64, _d, _d, _i, _vp],
     "klb_compare_fields": [_u64, _u64, _i, _ll, _i, _i, _i, _i, _i, _i, _i, _ll, C.POINTER(_d), C.POINTER(_d), _vp],
+    "klb_cyclic_xy": [_u64, _i, _ll, _i, _i, _i, _ll, _i, _i, _i, _i, _vp],
     "klb_crc32_device": [_u64, C.c_size_t, _vp, C.POINTER(C.c_uint32)],
     "klb_nccl_version": [C.POINTER(_i)],
     "klb_nccl_unique_id": [C.POINTER(C.c_ubyte)],

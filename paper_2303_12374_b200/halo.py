@@ -55,6 +55,7 @@ HALO_REACH = {
     "diff_uvw_rk3": {"evisc": (1, 1), "u": (1, 1), "v": (1, 1), "w": (1, 1)},
     "diff_uvw_peer": {"evisc": (1, 1), "u": (1, 1), "v": (1, 1), "w": (1, 1)},
     "advec_u_peer": {"u": (3, 3), "w": (1, 0)},
+    "diff_uvw_rk3_peer": {"evisc": (1, 1), "u": (1, 1), "v": (1, 1), "w": (1, 1)},
     "rk3_uvw": {},
 }
 
@@ -367,8 +368,12 @@ class LocalPeers:
     """Virtual ranks on ONE device for the fused-halo kernel: rank ``r``'s
     neighbours' fields are plain allocations of the same context, and every
     rank's launches go to one stream, so the fences are no-ops.  ``ranks[r]``
-    = (name -> pointer of element (0,0,0), kstart, kend); ``for_rank(r)`` is
-    the per-rank view ``SlabDriver(halo="fused")`` takes as its exchanger."""
+    = (field name -> pointer of element (0,0,0), kstart, kend) over all the
+    rank's fields; ``for_rank(r)`` is the per-rank view ``SlabDriver(halo=
+    "fused")`` takes as its exchanger.  As with ``IpcExchanger.peer_fields``
+    (which pairs the ranks' pointer lists position by position) a request
+    {key: my pointer} returns, per key, the neighbour's pointer of the SAME
+    field as mine — so {"u": my u_next} yields the neighbour's u_next."""
 
     def __init__(self, ranks: list[tuple[dict[str, int], int, int]]) -> None:
         self.ranks = ranks
@@ -381,11 +386,12 @@ class LocalPeers:
             self.owner, self.rank = owner, rank
 
         def peer_fields(self, fields: dict[str, int], kstart: int, kend: int) -> dict:
+            mine = {p: n for n, p in self.owner.ranks[self.rank][0].items()}
             out = {}
             for side, r in (("below", self.rank - 1), ("above", self.rank + 1)):
                 if 0 <= r < len(self.owner.ranks):
                     ptrs, ks, ke = self.owner.ranks[r]
-                    out[side] = ({n: ptrs[n] for n in fields}, ks, ke)
+                    out[side] = ({k: ptrs[mine[p]] for k, p in fields.items()}, ks, ke)
             return out
 
         def fence_ready(self, stream, below: int, above: int) -> None:

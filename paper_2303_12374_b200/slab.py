@@ -39,7 +39,7 @@ __all__ = ["SlabDriver", "FUSED_HALO"]
 
 #: kernels with a fused-halo variant (the planes outside the slab read from
 #: the neighbours' fields inside the TMA staging) -> that variant
-FUSED_HALO = {"diff_uvw": "diff_uvw_peer", "advec_u": "advec_u_peer"}
+FUSED_HALO = {"diff_uvw": "diff_uvw_peer", "advec_u": "advec_u_peer", "diff_uvw_rk3": "diff_uvw_rk3_peer"}
 
 
 class SlabDriver:
@@ -76,6 +76,8 @@ class SlabDriver:
                                    capture_policy=CapturePolicy(), wisdom_key=base_key)
         self.ranges = {"slab": (self.layout.kstart, self.layout.kend)} if self.fused else self.slab.subranges()
         self._peers_attached = not (self.fused and exchanger is not None and nranks > 1)
+        self._rk3_cache: dict = {}  # (parity, stage, dt) -> launch arguments (rk3_substep)
+        self._rk3_peers: dict = {}  # parity -> the neighbours' current fields
         self.args = {name: self.problem.args(rng) for name, rng in self.ranges.items()}
         self.below, self.above = self.decomposition.neighbours(rank)
         self._ev_start = Event()
@@ -189,6 +191,79 @@ class SlabDriver:
                 run(name)
                 launched += 1
         return launched
+
+    # -- RK3 time loop (diff_uvw_rk3) ----------------------------------------------------
+    #: MicroHH's low-storage RK3 (Williamson) coefficients
+    RK3_A = (0.0, -5.0 / 9.0, -153.0 / 128.0)
+    RK3_B = (1.0 / 3.0, 15.0 / 16.0, 8.0 / 15.0)
+
+    def rk3_substep(self, s: int, dt: float) -> int:
+        """Substep ``s`` (0, 1, 2, ... — three per time step) of a low-storage
+        RK3 time loop over the slab with diff_uvw_rk3: the tendencies T = t +
+        diffusion give t <- A[(s+1)%3] T and next <- cur + B[s%3] dt T, where
+        cur / next are (u, v, w) / (u_next, v_next, w_next) on even substeps
+        and swapped on odd ones (the buffers alternate); then the x/y ghost
+        cells of next are refilled periodically (``klb_cyclic_xy``).  With
+        ``halo="fused"`` the launch reads the neighbours' current fields
+        through their peer mappings — no exchange; the fences order it after
+        the neighbours' previous substep and before their next one.  Returns
+        the number of kernel launches (2: the stencil and the ghost fill)."""
+        from .cuda._abi import check, lib
+
+        if self.kernel != "diff_uvw_rk3" or (self.nranks > 1 and not self.fused):
+            raise ValueError("rk3_substep runs diff_uvw_rk3 (with halo='fused' when the grid is decomposed)")
+        parity = s % 2
+        args = self._rk3_args(parity, s % 3, dt)
+        if self.exchanger is not None and self.nranks > 1:
+            self.exchanger.fence_ready(self.compute, self.below, self.above)
+        self.wisdom.launch(self.ctx.ident, args, stream=self.compute)
+        lay = self.layout
+        for name in (("u_next", "v_next", "w_next") if parity == 0 else ("u", "v", "w")):
+            check(lib().klb_cyclic_xy(self.problem.field_ptr(name), lay.elem_bytes, 0, lay.icells, lay.jcells,
+                                      lay.jj, lay.kk, lay.igc, lay.jgc, lay.kstart, lay.kend, self.compute.handle))
+        if self.exchanger is not None and self.nranks > 1:
+            self.exchanger.fence_done(self.compute, self.below, self.above)
+        return 2
+
+    def _rk3_args(self, parity: int, sub: int, dt: float) -> list:
+        """Launch arguments of substep parity / RK stage (memoised): the
+        current/next buffers swapped on odd substeps, the neighbours' current
+        fields as the peer arguments, the stage's coefficients."""
+        key = (parity, sub, dt)
+        cache = self._rk3_cache
+        if key in cache:
+            return cache[key]
+        from .capture import ScalarArg
+        from .cuda.device import DeviceBuffer
+        from .stencils.definitions import ARG_LAYOUT
+
+        prob = self.problem
+        if self.fused and self.exchanger is not None and self.nranks > 1:
+            peers = self._rk3_peers
+            if not peers:  # collective, same order on every rank: both buffer sets of the neighbours
+                lay = self.layout
+                for par, names in ((0, ("u", "v", "w")), (1, ("u_next", "v_next", "w_next"))):
+                    ptrs = {"evisc": prob.field_ptr("evisc")}
+                    ptrs.update({f: prob.field_ptr(n) for f, n in zip(("u", "v", "w"), names)})
+                    got = self.exchanger.peer_fields(ptrs, lay.kstart, lay.kend)
+                    peers[par] = {side: (p, lay.span_elems + ((ke - ks) - (lay.kend - lay.kstart)) * lay.kk,
+                                         ke if side == "below" else ks) for side, (p, ks, ke) in got.items()}
+            prob.set_peers(below=peers[parity].get("below"), above=peers[parity].get("above"))
+        args = prob.args(self.ranges["slab"] if self.fused else None)
+        layout = ARG_LAYOUT[prob.kernel]
+        pos = {name: i for i, (name, _) in enumerate(layout["buffers"])}
+        if parity:
+            for a, b in (("u", "u_next"), ("v", "v_next"), ("w", "w_next")):
+                ia, ib = pos[a], pos[b]
+                da, db = args[ia], args[ib]
+                args[ia] = DeviceBuffer(ia, da.role, da.element_type, db.ptr, db.element_count, owner=db.owner)
+                args[ib] = DeviceBuffer(ib, db.role, db.element_type, da.ptr, da.element_count, owner=da.owner)
+        nb = len(layout["buffers"])
+        for name, value in (("rk_a", self.RK3_A[(sub + 1) % 3]), ("rk_bdt", self.RK3_B[sub] * dt)):
+            i = nb + layout["scalars"].index(name)
+            args[i] = ScalarArg(i, args[i].dtype, value)
+        cache[key] = args
+        return args
 
     def step_host(self, host: dict[str, int], chunks: int = 16, copy_streams: int = 1) -> int:
         """One step streamed from/to pinned host memory (``stream.py``).

@@ -64,7 +64,9 @@ FUSED_KERNELS = {"diff_uvw_rk3": ("diff_uvw", "KL_RK3"),
                  # slab are read from the neighbours' fields (diff_uvw.cu /
                  # advec_u.cu KL_PEER)
                  "diff_uvw_peer": ("diff_uvw", "KL_PEER"),
-                 "advec_u_peer": ("advec_u", "KL_PEER")}
+                 "advec_u_peer": ("advec_u", "KL_PEER"),
+                 # both: the RK3 substep of a multi-GPU time loop (slab.SlabDriver.rk3_substep)
+                 "diff_uvw_rk3_peer": ("diff_uvw", "KL_RK3 KL_PEER")}
 ALL_KERNELS = KERNELS + tuple(FUSED_KERNELS) + FAMILY_KERNELS
 
 
@@ -149,6 +151,15 @@ ARG_LAYOUT = {
         "scalars": ["dxi", "dyi", "peer_klo", "peer_khi", "peer_shift_lo", "peer_shift_hi", "jj", "kk", "istart",
                     "jstart", "kstart", "iend", "jend", "kend"],
     },
+    "diff_uvw_rk3_peer": {
+        "buffers": [("ut", "output"), ("vt", "output"), ("wt", "output"), ("evisc", "input"), ("u", "input"),
+                    ("v", "input"), ("w", "input"), ("dzi", "input"), ("dzhi", "input"), ("rhoref", "input"),
+                    ("rhorefh", "input"), ("u_next", "output"), ("v_next", "output"), ("w_next", "output"),
+                    ("evisc_lo", "input"), ("u_lo", "input"), ("v_lo", "input"), ("w_lo", "input"),
+                    ("evisc_hi", "input"), ("u_hi", "input"), ("v_hi", "input"), ("w_hi", "input")],
+        "scalars": ["dxi", "dyi", "rk_a", "rk_bdt", "peer_klo", "peer_khi", "peer_shift_lo", "peer_shift_hi", "jj",
+                    "kk", "istart", "jstart", "kstart", "iend", "jend", "kend"],
+    },
     "rk3_uvw": {
         "buffers": [("ut", "output"), ("vt", "output"), ("wt", "output"), ("u", "output"), ("v", "output"),
                     ("w", "output")],
@@ -230,7 +241,7 @@ def assemble_source(kernel: str, precision: str) -> str:
         "#define DIRECT 0\n#define ZMARCH 1\n#define TMA 2\n"
     )
     if kernel in FUSED_KERNELS:
-        prelude += f"#define {FUSED_KERNELS[kernel][1]} 1\n"
+        prelude += "".join(f"#define {name} 1\n" for name in FUSED_KERNELS[kernel][1].split())
     return prelude + _strip_comments(_inline(_HERE / f"{base_kernel(kernel)}.cu"))
 
 

@@ -38,6 +38,7 @@ KERNEL_FIELDS = {
     "diff_uvw_rk3": ("ut", "vt", "wt", "evisc", "u", "v", "w", "u_next", "v_next", "w_next"),
     "diff_uvw_peer": ("ut", "vt", "wt", "evisc", "u", "v", "w"),
     "advec_u_peer": ("ut", "u", "v", "w"),
+    "diff_uvw_rk3_peer": ("ut", "vt", "wt", "evisc", "u", "v", "w", "u_next", "v_next", "w_next"),
     "rk3_uvw": ("ut", "vt", "wt", "u", "v", "w"),
 }
 #: algorithmic HBM words per interior cell: advec_u reads u,v,w,ut
@@ -49,7 +50,7 @@ BYTES_PER_CELL_WORDS = {"advec_u": 5, "diff_uvw": 10, "advec_v": 5, "advec_w": 5
                         # diff_uvw + RK3 epilogue: reads evisc,u,v,w,ut,vt,wt, writes ut,vt,wt,u',v',w'
                         "diff_uvw_rk3": 13,
                         # diff_uvw with its z-halo read from the neighbours' fields: same words per cell
-                        "diff_uvw_peer": 10, "advec_u_peer": 5,
+                        "diff_uvw_peer": 10, "advec_u_peer": 5, "diff_uvw_rk3_peer": 13,
                         # the separate RK3 pass: read + write u,v,w,ut,vt,wt
                         "rk3_uvw": 12}
 #: MicroHH defaults of the model constants the family kernels take
@@ -63,7 +64,8 @@ _PROFILE_FIELDS = ("rhoref", "rhorefh", "dzi", "dzhi")
 #: the fused-halo kernels' neighbour-field arguments -> the local field they mirror
 _PEER_FIELDS = {f"{f}_{side}": f for side in ("lo", "hi") for f in ("evisc", "u", "v", "w")}
 #: fields each fused-halo kernel reads from its neighbours (its halo'd inputs)
-PEER_KERNELS = {"diff_uvw_peer": ("evisc", "u", "v", "w"), "advec_u_peer": ("u", "w")}
+PEER_KERNELS = {"diff_uvw_peer": ("evisc", "u", "v", "w"), "advec_u_peer": ("u", "w"),
+                "diff_uvw_rk3_peer": ("evisc", "u", "v", "w")}
 #: peer_klo / peer_khi of a side without a neighbour: a plane no launch reaches
 _NO_PEER = 1 << 30
 

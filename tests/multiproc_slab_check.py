@@ -70,6 +70,8 @@ def main() -> int:
     drv = SlabDriver(kernel, precision, grid, ctx, rank=rank, nranks=world, exchanger=ex,
                      compiler=NvrtcCompiler(ctx), wisdom_dir=str(ROOT / "wisdom"),
                      halo="fused" if transport == "fused" else "exchange")
+    if kernel == "diff_uvw_rk3":  # the RK3 time loop: 4 substeps, fused halo, vs the oracle's loop
+        return rk3_loop_check(drv, ctx, group, ex, rank, grid, precision)
     drv.resolve()
     if os.environ.get("KL_CHECK_SHARED"):
         # another driver on the same exchanger, stepped and closed: closing it
@@ -101,6 +103,36 @@ def main() -> int:
     tol = 1e-5 if precision == "fp32" else 1e-12
     ok = worst <= tol and (poisoned > 0 or world == 1)
     print(f"rank {rank} {'ok' if ok else 'FAIL'} {worst:.3e} poisoned_planes={poisoned}", flush=True)
+    return 0 if ok else 1
+
+
+def rk3_loop_check(drv, ctx, group, ex, rank, grid, precision) -> int:
+    import numpy as np
+
+    from stencil_helpers import oracle_rk3_loop
+
+    nsub, dt = 4, 0.05
+    poisoned = poison_halo(drv)
+    ctx.synchronize()
+    group.barrier()
+    for s in range(nsub):
+        drv.rk3_substep(s, dt)
+    ctx.synchronize()
+    want_t, want_u = oracle_rk3_loop(drv.global_layout, nsub, dt)
+    g = drv.layout.kgc
+    off, count = drv.slab.offset, drv.slab.count
+    worst = 0.0
+    for name, ref in list(want_t.items()) + list(want_u.items()):
+        got = drv.problem.download(name)[g:g + count, g:-g, g:g + grid[0]].astype(np.float64)
+        r = ref[g + off:g + off + count, g:-g, g:g + grid[0]]
+        err = float(np.max(np.abs(got - r)) / np.max(np.abs(ref[g:-g, g:-g, g:g + grid[0]])))
+        worst = max(worst, err if np.isfinite(err) else float("inf"))
+    drv.close()
+    ex.close()
+    group.close()
+    tol = 1e-5 if precision == "fp32" else 1e-12
+    ok = worst <= tol
+    print(f"rank {rank} {'ok' if ok else 'FAIL'} {worst:.3e} rk3 substeps={nsub} poisoned_planes={poisoned}", flush=True)
     return 0 if ok else 1
 
 

@@ -52,6 +52,40 @@ def oracle_window(kernel: str, layout: GridLayout, kb: int, ke: int, k_offset: i
     return {n: sub.interior(a) for n, a in res.items()}
 
 
+def cyclic_xy(a: np.ndarray, layout: GridLayout) -> np.ndarray:
+    """MicroHH boundary_cyclic on the interior planes of a (kcells, jcells,
+    icells) array: x/y ghost cells take the interior cell they wrap onto
+    (the oracle of ``klb_cyclic_xy``)."""
+    gi, gj, gk = layout.igc, layout.jgc, layout.kgc
+    ii = gi + (np.arange(a.shape[2]) - gi) % layout.itot
+    jj = gj + (np.arange(a.shape[1]) - gj) % layout.jtot
+    out = np.array(a, copy=True)
+    out[gk:a.shape[0] - gk] = a[gk:a.shape[0] - gk][:, jj][:, :, ii]
+    return out
+
+
+def oracle_rk3_loop(layout: GridLayout, nsub: int, dt: float, dxi=1.0, dyi=1.0):
+    """``nsub`` substeps of the low-storage RK3 time loop SlabDriver.rk3_substep
+    runs (diff_uvw_rk3 into the alternate buffers, then the periodic x/y ghost
+    fill), over the whole grid.  Returns (tendencies, current u/v/w) by name
+    ({"ut", "vt", "wt"}, {"u", "v", "w"}), float64."""
+    from paper_2303_12374_b200.slab import SlabDriver
+
+    f = {n: a.astype(np.float64) for n, a in host_fields(layout, KERNEL_FIELDS["diff_uvw_rk3"]).items()}
+    prof = make_profiles(layout.kcells, layout.kgc).as_dtype(layout.dtype)
+    g = (layout.igc, layout.jgc, layout.kgc)
+    cur = [f["u"], f["v"], f["w"]]
+    nxt = [f["u_next"], f["v_next"], f["w_next"]]
+    t = [f["ut"], f["vt"], f["wt"]]
+    for s in range(nsub):
+        rk_a, rk_bdt = SlabDriver.RK3_A[(s % 3 + 1) % 3], SlabDriver.RK3_B[s % 3] * dt
+        out = family_oracle.diff_uvw_rk3(*t, f["evisc"], *cur, *nxt, prof.dzi, prof.dzhi, prof.rhoref, prof.rhorefh,
+                                         dxi, dyi, rk_a, rk_bdt, ghost=g)
+        t = list(out[:3])
+        nxt, cur = cur, [cyclic_xy(a, layout) for a in out[3:]]
+    return dict(zip(("ut", "vt", "wt"), t)), dict(zip(("u", "v", "w"), cur))
+
+
 def download_planes(prob: StencilProblem, name: str, kb: int, ke: int) -> np.ndarray:
     """Interior i/j of local planes ``[kb, ke)`` of a device field, (ke-kb, jtot, itot)."""
     lay = prob.layout

@@ -77,7 +77,10 @@ def test_spawned_ranks_without_torch_match_oracle(kernel, precision, grid, nproc
                                                                 ("diff_uvw", "fp64", "40,24,36", 2, False),
                                                                 ("diff_uvw", "fp32", "48,32,20", 2, True),
                                                                 ("advec_u", "fp32", "64,48,40", 3, False),
-                                                                ("advec_u", "fp64", "48,32,30", 2, True)])
+                                                                ("advec_u", "fp64", "48,32,30", 2, True),
+                                                                # the RK3 time loop, 4 substeps (multiproc_slab_check)
+                                                                ("diff_uvw_rk3", "fp32", "48,40,31", 3, False),
+                                                                ("diff_uvw_rk3", "fp64", "40,32,24", 2, False)])
 def test_fused_peer_halo_ranks_match_oracle(kernel, precision, grid, nproc, shared):
     """diff_uvw / advec_u with the z-halo fused into the kernel: one launch per rank
     over its whole slab, the planes outside the slab read through CUDA-IPC

@@ -147,6 +147,66 @@ def test_fused_peer_halo_virtual_ranks_match_single_grid(gpu_ctx, tmp_path, kern
             drv.close()
 
 
+@pytest.mark.parametrize("precision", ["fp32", "fp64"])
+def test_rk3_time_loop_fused_halo_virtual_ranks_match_oracle(gpu_ctx, tmp_path, precision):
+    """Four substeps of the low-storage RK3 time loop (SlabDriver.rk3_substep:
+    diff_uvw_rk3 into the alternate buffers + periodic x/y ghost fill) on one
+    undecomposed grid and on 3 virtual ranks whose launches read the
+    neighbours' CURRENT buffers (diff_uvw_rk3_peer; u/v/w and u_next/v_next/
+    w_next alternate, so the peer arguments alternate too) — every rank's
+    tendencies and velocities equal the oracle's time loop."""
+    from paper_2303_12374_b200.cuda import NvrtcCompiler
+    from paper_2303_12374_b200.halo import LocalPeers
+    from paper_2303_12374_b200.slab import SlabDriver
+    from paper_2303_12374_b200.stencils.definitions import definition_for
+    from paper_2303_12374_b200.stencils.layout import GridLayout
+    from paper_2303_12374_b200.wisdom import WisdomFile, WisdomRecord
+    from stencil_helpers import oracle_rk3_loop
+
+    comp = NvrtcCompiler(gpu_ctx)
+    d = definition_for("diff_uvw_rk3", precision)
+    cfg = dict(d.space.default_config()[0], staging="TMA", zchunk=8, block_x=32, block_y=4, depth=2)
+    WisdomFile(d.kernel_key(), records=[WisdomRecord(gpu_ctx.ident, (1, 1, 1), cfg, 1.0)]).save(
+        tmp_path / f"{d.kernel_key()}.wisdom")
+    grid, nsub, dt = (48, 40, 31), 4, 0.05
+    lay = GridLayout(*grid, precision)
+    want_t, want_u = oracle_rk3_loop(lay, nsub, dt)
+    tol = 1e-5 if precision == "fp32" else 1e-12
+    g = lay.kgc
+    cur = ("u", "v", "w") if nsub % 2 == 0 else ("u_next", "v_next", "w_next")
+
+    def check(drv, off, count, what):
+        for name, ref in list(want_t.items()) + [(c, want_u[n]) for c, n in zip(cur, ("u", "v", "w"))]:
+            got = drv.problem.download(name)[g:g + count, g:-g, g:g + grid[0]].astype(np.float64)
+            r = ref[g + off:g + off + count, g:-g, g:g + grid[0]]
+            err = np.max(np.abs(got - r)) / np.max(np.abs(ref[g:-g, g:-g, g:g + grid[0]]))
+            assert err <= tol, (what, name, err)
+
+    whole = SlabDriver("diff_uvw_rk3", precision, grid, gpu_ctx, compiler=comp, wisdom_dir=tmp_path)
+    for s in range(nsub):
+        assert whole.rk3_substep(s, dt) == 2
+    gpu_ctx.synchronize()
+    check(whole, 0, grid[2], "whole grid")
+    whole.close()
+
+    nranks = 3
+    peers = LocalPeers([])
+    drivers = [SlabDriver("diff_uvw_rk3", precision, grid, gpu_ctx, rank=r, nranks=nranks, compiler=comp,
+                          wisdom_dir=tmp_path, halo="fused", exchanger=peers.for_rank(r)) for r in range(nranks)]
+    peers.ranks = [({n: drv.problem.field_ptr(n) for n in drv.problem.fields}, drv.layout.kstart, drv.layout.kend)
+                   for drv in drivers]
+    for drv in drivers:
+        _poison_ghosts(drv)
+    for s in range(nsub):  # one stream: rank r's substep s after every rank's substep s-1
+        for drv in drivers:
+            drv.rk3_substep(s, dt)
+    gpu_ctx.synchronize()
+    for drv in drivers:
+        check(drv, drv.slab.offset, drv.slab.count, f"rank {drv.rank}")
+        assert all(r.configuration == cfg for r in drv.wisdom.reports)
+        drv.close()
+
+
 def test_nccl_single_rank_exchange_is_a_noop(gpu_ctx):
     """The NCCL path end to end on one GPU: unique id, comm init, grouped
     send/recv call with no neighbours (the only topology one GPU allows)."""
