@@ -45,7 +45,14 @@
 #endif
 #ifndef KL_SKEL
 #define KL_SKEL 0  // diagnostic only (tools/skeleton_probe.py): 1 = keep the TMA rings, barriers and ut
-                   // stores but replace the stencil by ut += 1 — the data-movement floor of the tiling
+                   // stores but replace the stencil by ut += 1 — the data-movement floor of the tiling;
+                   // 2 = that with u boxes stripped of their x/y halo, 3 = v/w boxes too (what the
+                   // halos cost in bytes and time)
+#endif
+
+#ifndef KL_L2HINT
+#define KL_L2HINT 0  // experiment: L2 eviction priorities, bit 1 = ut loads evict_first, 2 = v/w loads
+                     // evict_first, 4 = u loads evict_last, 8 = ut stores evict_first
 #endif
 
 #include "kl_pack.cuh"
@@ -60,12 +67,21 @@ constexpr int kTYT = BLOCK_Y * kTY;         // rows per block
 constexpr int kVA = kTX < kE ? kTX : kE;    // vector width (elements) of aligned reads
 __host__ __device__ constexpr int rup(int a, int b) { return (a + b - 1) / b * b; }
 // box widths: start column i0-4 rounded down to 16 B (up to kE-1 slack)
+constexpr int kTW = rup(kXT + kE - 1, kE);      // ut: columns i0 .. i0+kXT-1
+#if KL_SKEL >= 2  // diagnostic floors: u boxes without the x/y halo (2), v/w boxes too (3)
+constexpr int kBW = kTW, kBH = kTYT;
+#else
 constexpr int kBW = rup(kXT + 8 + kE - 1, kE);  // u: columns i0-4 .. i0+kXT+3
 constexpr int kBH = kTYT + 6;
+#endif
+#if KL_SKEL >= 3
+constexpr int kVW = kTW, kVH = kTYT;
+#else
 constexpr int kVW = rup(kXT + 4 + kE - 1, kE);  // v, w: columns i0-4 .. i0+kXT-1
-constexpr int kTW = rup(kXT + kE - 1, kE);      // ut: columns i0 .. i0+kXT-1
+constexpr int kVH = kTYT + 1;                   // v: rows j0 .. j0+kTYT
+#endif
 constexpr int kUB = rup(kBW * kBH * kS, 128);
-constexpr int kVB = rup(kVW * (kTYT + 1) * kS, 128);
+constexpr int kVB = rup(kVW * kVH * kS, 128);
 constexpr int kWB = rup(kVW * kTYT * kS, 128);
 constexpr int kTB = rup(kTW * kTYT * kS, 128);
 // two rings: u planes (kNU slots: plane k feeds the x/y stencil of step k,
@@ -82,7 +98,7 @@ constexpr int kVO = 0, kWO = kVB / kS, kTO = (kVB + kWB) / kS;  // field offsets
 constexpr bool kPack = sizeof(real) == 4 && kTX >= 2;
 constexpr int kP = kTX / 2 > 0 ? kTX / 2 : 1;  // column pairs per thread
 constexpr unsigned kTxU = static_cast<unsigned>(kBW * kBH * kS);
-constexpr unsigned kTxV = static_cast<unsigned>((kVW * (kTYT + 1) + kVW * kTYT + kTW * kTYT) * kS);
+constexpr unsigned kTxV = static_cast<unsigned>((kVW * kVH + kVW * kTYT + kTW * kTYT) * kS);
 static_assert(kBW <= 256 && kBH <= 256, "TMA box extents are limited to 256");
 static_assert(kNU + kNV <= 16, "mbarriers must fit the 128-byte header");
 
@@ -105,14 +121,38 @@ __device__ __forceinline__ void ld_span(real (&d)[N], const real* s) {
   }
 }
 
+// one VA-element store with an L2 evict_first policy (KL_L2HINT & 8)
+template <int VA>
+__device__ __forceinline__ void st_hint(real* d, const Pack<VA>& p, unsigned long long pol) {
+  if constexpr (sizeof(real) == 4 && VA == 4) {
+    asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(d), "f"(p.v[0]), "f"(p.v[1]),
+                 "f"(p.v[2]), "f"(p.v[3]), "l"(pol) : "memory");
+  } else if constexpr (sizeof(real) == 4 && VA == 2) {
+    asm volatile("st.global.L2::cache_hint.v2.f32 [%0], {%1, %2}, %3;" ::"l"(d), "f"(p.v[0]), "f"(p.v[1]), "l"(pol)
+                 : "memory");
+  } else if constexpr (sizeof(real) == 8 && VA == 2) {
+    asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(d), "d"(p.v[0]), "d"(p.v[1]), "l"(pol)
+                 : "memory");
+  } else {
+    *reinterpret_cast<Pack<VA>*>(d) = p;
+  }
+}
+
 template <int VA>
 __device__ __forceinline__ void st_span(real* d, const real (&s)[kTX]) {
+#if KL_L2HINT & 8
+  const unsigned long long pol = kl::l2_evict_first();
+#endif
 #pragma unroll
   for (int e = 0; e < kTX; e += VA) {
     Pack<VA> p;
 #pragma unroll
     for (int q = 0; q < VA; ++q) p.v[q] = s[e + q];
+#if KL_L2HINT & 8
+    st_hint<VA>(d + e, p, pol);
+#else
     *reinterpret_cast<Pack<VA>*>(d + e) = p;
+#endif
   }
 }
 
@@ -147,20 +187,36 @@ struct AdvecTma {
       return;
     }
 #endif
+#if KL_L2HINT & 4
+    kl::tma_load_3d_hint(ring_u + slot * kUS, maps + 0, bar_u + slot, xu, j0 - 3, p, kl::l2_evict_last());
+#else
     kl::tma_load_3d(ring_u + slot * kUS, maps + 0, bar_u + slot, xu, j0 - 3, p);
+#endif
   }
   __device__ __forceinline__ void issue_v(int slot, int p) const {
     unsigned long long* bar = bar_v + slot;
     real* dst = ring_v + slot * kVS;
     kl::mbar_expect_tx(bar, kTxV);
+#if KL_L2HINT & 2
+    kl::tma_load_3d_hint(dst + kVO, maps + 1, bar, xv, j0, p, kl::l2_evict_first());
+#else
     kl::tma_load_3d(dst + kVO, maps + 1, bar, xv, j0, p);
+#endif
 #if KL_PEER
     if (p >= peer_khi)  // above the slab: the neighbour's w (map 5); v / ut of that plane are never read
       kl::tma_load_3d(dst + kWO, maps + 5, bar, xw, j0, p + peer_shift_hi);
     else
 #endif
+#if KL_L2HINT & 2
+      kl::tma_load_3d_hint(dst + kWO, maps + 2, bar, xw, j0, p, kl::l2_evict_first());
+#else
       kl::tma_load_3d(dst + kWO, maps + 2, bar, xw, j0, p);
+#endif
+#if KL_L2HINT & 1
+    kl::tma_load_3d_hint(dst + kTO, maps + 3, bar, xt, j0, p, kl::l2_evict_first());
+#else
     kl::tma_load_3d(dst + kTO, maps + 3, bar, xt, j0, p);
+#endif
   }
   // u of plane k0 + d at element offset b of plane k0 (the chunk prologue's
   // unstaged loads, planes k0-3 .. k0+2: below the slab for the first chunk,
@@ -542,7 +598,7 @@ struct Marcher<true> {
 #define KL_K KL_POS_KK
 #define KL_NMAPS (4 + 2 * KL_PEER)
 extern "C" __device__ const int kl_tma_spec[1 + 5 * KL_NMAPS] = {
-    KL_NMAPS, 1, KL_J, KL_K, kBW, kBH, 2, KL_J, KL_K, kVW, kTYT + 1, 3, KL_J, KL_K, kVW, kTYT, 0, KL_J, KL_K, kTW, kTYT
+    KL_NMAPS, 1, KL_J, KL_K, kBW, kBH, 2, KL_J, KL_K, kVW, kVH, 3, KL_J, KL_K, kVW, kTYT, 0, KL_J, KL_K, kTW, kTYT
 #if KL_PEER
     , 9, KL_J, KL_K, kBW, kBH, 10, KL_J, KL_K, kVW, kTYT
 #endif

@@ -87,9 +87,17 @@ def test_rk3_pass_matches_oracle(gpu_ctx, compiler):
     for precision in ("fp32", "fp64"):
         lay = GridLayout(45, 23, 19, precision)
         ref, _ = oracle_outputs("rk3_uvw", lay)
-        got = run_config(gpu_ctx, compiler, "rk3_uvw", lay, _space("rk3_uvw", precision).default_config()[0])
-        for name in ref:
-            assert rel_error(got[name], ref[name], lay) <= TOL[precision], name
+        base = _space("rk3_uvw", precision).default_config()[0]
+        # default (scalar), then the vector path: consecutive column tiles of
+        # 2 / 4 cells, the last chunk of every row crossing iend (45 columns)
+        cfgs = [base,
+                dict(base, contiguous_x=True, tile_x=2, block_x=16, block_y=2, tile_y=2, tile_z=2),
+                dict(base, contiguous_x=True, tile_x=4, block_x=16, block_y=4, block_z=2, unroll_x=True),
+                dict(base, contiguous_x=True, tile_x=4, block_x=32, contiguous_z=True, tile_z=4, unravel="ZYX")]
+        for cfg in cfgs:
+            got = run_config(gpu_ctx, compiler, "rk3_uvw", lay, cfg)
+            for name in ref:
+                assert rel_error(got[name], ref[name], lay) <= TOL[precision], (cfg, name)
 
 
 @pytest.mark.parametrize("kernel", ["advec_v", "advec_w", "advec_s"])

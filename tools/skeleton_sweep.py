@@ -25,7 +25,10 @@ def main(argv=None) -> int:
     ap.add_argument("--top", type=int, default=30)
     ap.add_argument("--reps", type=int, default=15)
     ap.add_argument("--json-out")
+    ap.add_argument("--levels", default="1", help="KL_SKEL levels to time (advec_u: 2 = u boxes without halo, "
+                                                  "3 = v/w boxes too)")
     a = ap.parse_args(argv)
+    levels = [int(x) for x in a.levels.split(",")]
 
     from paper_2303_12374_b200.cuda import open_device
     from paper_2303_12374_b200.cuda.compiler import CudaExecutable
@@ -61,7 +64,9 @@ def main(argv=None) -> int:
         cfg = dict(default, **e.config)  # sessions of an older space lack the later knobs (their defaults)
         rec = {"kernel": kernel, "precision": precision, "grid": list(grid), "config": cfg,
                "session_us": round(e.measurement.objective * 1e6, 2)}
-        for tag, extra in (("full", ()), ("skeleton", ("-D KL_SKEL=1",))):
+        variants = [("full", ())] + [("skeleton" if lv == 1 else f"skeleton{lv}", (f"-D KL_SKEL={lv}",))
+                                     for lv in levels]
+        for tag, extra in variants:
             req = d.render_compile_request(cfg, ex.problem, ex.scalar_env)
             req = CompileRequest(req.source, req.entry, req.defines + extra, req.flags)
             geom = d.derive_geometry(cfg, ex.problem, ex.scalar_env)
