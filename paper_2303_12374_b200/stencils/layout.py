@@ -44,8 +44,8 @@ class GridLayout:
             raise ValueError(f"precision must be fp32 or fp64, got {self.precision!r}")
         if min(self.itot, self.jtot, self.ktot) < 1:
             raise ValueError("interior extents must be >= 1")
-        if self.igc > self.align:
-            raise ValueError("igc larger than the alignment quantum")
+        if self.align_bytes < 16 or self.align_bytes % 16:
+            raise ValueError("align_bytes must be a multiple of 16 (TMA strides, 16-byte vector rows)")
 
     # -- element geometry --------------------------------------------------------
     @property
@@ -84,7 +84,9 @@ class GridLayout:
 
     @property
     def lead(self) -> int:
-        return self.align - self.igc
+        # smallest offset putting the first interior cell (i = igc) on an
+        # alignment boundary
+        return -(-self.igc // self.align) * self.align - self.igc
 
     @property
     def kk(self) -> int:

@@ -32,7 +32,7 @@ extern "C" __global__ void empty_k(int dummy) {
 extern "C" __global__ void flush_k(unsigned* buf, unsigned long long n, unsigned seed) {
   extern __shared__ unsigned char smem[];
   if (seed == 0xFFFFFFFFu) smem[threadIdx.x] = 0;
-  for (unsigned long long t = blockIdx.x * 256ull + threadIdx.x; t < n / 4; t += gridDim.x * 256ull)
+  for (unsigned long long t = blockIdx.x * 256ull + threadIdx.x; t < n / 16; t += gridDim.x * 256ull)
     reinterpret_cast<uint4*>(buf)[t] = make_uint4(seed, seed + 1, seed + 2, t);
 }
 extern "C" __global__ void __launch_bounds__(256) stream4(float* __restrict__ ut, const float* __restrict__ u,
