@@ -107,6 +107,69 @@ def window_error(prob: StencilProblem, kernel: str, kb: int, ke: int) -> dict:
     return out
 
 
+def cref_chunks(kernel: str, layout: GridLayout, k_offset: int = 0, kcells_global: int | None = None,
+                dxi: float = 1.0, dyi: float = 1.0, chunk: int = 32, threads: int | None = None,
+                rk_a: float = RK_A, rk_bdt: float = RK_BDT):
+    """Yield ``(kb, ke, {output: (ke-kb, jtot, itot) float64})`` over every
+    interior plane of ``layout`` (local plane 0 = global plane ``k_offset``):
+    the C restatement (oracle/cref, float64 arithmetic on inputs of the
+    layout's precision) on z-chunks of ``chunk`` planes, each chunk's inputs
+    (+ ghost reach) generated by the C synth twin — host memory stays bounded
+    at any grid size.  advec_u / diff_uvw (the kernels cref restates) and
+    diff_uvw_rk3 (cref's diff_uvw + the RK3 epilogue of
+    family_oracle.diff_uvw_rk3, elementwise in float64)."""
+    import os
+
+    from oracle import cref
+
+    g = layout.kgc
+    threads = threads or os.cpu_count() or 1
+    base = make_profiles(kcells_global if kcells_global is not None else layout.kcells, g)
+    for kb in range(layout.kstart, layout.kend, chunk):
+        ke = min(kb + chunk, layout.kend)
+        sub = GridLayout(layout.itot, layout.jtot, ke - kb, layout.precision, layout.igc, layout.jgc, g)
+        k0 = k_offset + kb - g
+        f = {}
+        for n in KERNEL_FIELDS[kernel]:
+            off, lo, hi = FIELD_SPECS[n]
+            a = cref.synth_field(FIELD_SEED_BASE + off, lo, hi, sub.icells, sub.jcells, sub.kcells, sub.igc, sub.jgc,
+                                 k_offset=k0, dtype=layout.dtype, threads=threads)
+            f[n] = a.astype(np.float64)
+        prof = base.window(k0, sub.kcells).as_dtype(layout.dtype)
+        pf = {k: np.ascontiguousarray(getattr(prof, k), dtype=np.float64) for k in ("rhoref", "rhorefh", "dzi", "dzhi")}
+        gh = (sub.igc, sub.jgc, g)
+        if kernel == "advec_u":
+            cref.advec_u(f["ut"], f["u"], f["v"], f["w"], pf["rhoref"], pf["rhorefh"], pf["dzi"], dxi, dyi, ghost=gh,
+                         threads=threads)
+            outs = ("ut",)
+        elif kernel in ("diff_uvw", "diff_uvw_rk3"):
+            cref.diff_uvw(f["ut"], f["vt"], f["wt"], f["evisc"], f["u"], f["v"], f["w"], pf["dzi"], pf["dzhi"],
+                          pf["rhoref"], pf["rhorefh"], dxi, dyi, ghost=gh, threads=threads)
+            outs = ("ut", "vt", "wt")
+            if kernel == "diff_uvw_rk3":
+                for c, t in (("u", "ut"), ("v", "vt"), ("w", "wt")):
+                    f[c + "_next"] = f[c] + rk_bdt * f[t]  # interior cells only are compared
+                    f[t] = rk_a * f[t]
+                outs += ("u_next", "v_next", "w_next")
+        else:
+            raise ValueError(f"no C restatement of {kernel}")
+        yield kb, ke, {n: sub.interior(f[n]) for n in outs}
+
+
+def full_volume_error(prob: StencilProblem, kernel: str, chunk: int = 32) -> dict:
+    """max|gpu - ref| / max|ref| per output over EVERY interior cell of the
+    device problem (all its local planes), reference = ``cref_chunks``."""
+    diff, scale = {}, {}
+    for kb, ke, ref in cref_chunks(kernel, prob.layout, prob.k_offset, prob.kcells_global, prob.dxi, prob.dyi,
+                                   chunk, rk_a=prob.rk_a, rk_bdt=prob.rk_bdt):
+        for n, r in ref.items():
+            got = download_planes(prob, n, kb, ke).astype(np.float64)
+            d = float(np.max(np.abs(got - r)))
+            diff[n] = max(diff.get(n, 0.0), d if np.isfinite(d) else float("inf"))
+            scale[n] = max(scale.get(n, 0.0), float(np.max(np.abs(r))))
+    return {n: diff[n] / scale[n] for n in diff}
+
+
 def _oracle_compute(kernel, f, prof, layout, dxi, dyi):
     g = (layout.igc, layout.jgc, layout.kgc)
     if kernel == "advec_u":

@@ -150,3 +150,36 @@ def test_oracle_window_equals_whole_grid(kernel):
     win = oracle_window(kernel, slab, 3, 11, k_offset=4, kcells_global=lay.kcells)
     for name, arr in win.items():
         assert np.array_equal(arr, lay.interior(full[name])[4:12])
+
+
+@pytest.mark.parametrize("kernel,precision", [("advec_u", "fp32"), ("diff_uvw", "fp64"), ("diff_uvw", "fp32"),
+                                              ("diff_uvw_rk3", "fp64")])
+def test_cref_chunks_cover_the_grid_like_the_numpy_oracle(kernel, precision):
+    """The full-volume GPU parity check (stencil_helpers.full_volume_error)
+    streams the C restatement over z-chunks with their inputs regenerated per
+    chunk; stitched together they must equal the NumPy oracle of the whole
+    grid, and a z-slab (k_offset) must equal the same planes of the grid."""
+    from oracle import cref
+
+    if not cref.available():
+        pytest.skip("oracle/_build not built")
+    from stencil_helpers import cref_chunks, oracle_outputs
+
+    from paper_2303_12374_b200.stencils.layout import GridLayout
+
+    lay = GridLayout(20, 14, 11, precision)
+    ref, _ = oracle_outputs(kernel, lay)
+    covered = 0
+    for kb, ke, out in cref_chunks(kernel, lay, chunk=4, threads=2):
+        covered += ke - kb
+        for n, r in out.items():
+            want = lay.interior(ref[n])[kb - lay.kstart:ke - lay.kstart]
+            assert np.allclose(r, want, rtol=0, atol=1e-12 * np.max(np.abs(want))), (n, kb)
+    assert covered == lay.ktot
+    # a slab of planes 4..8 of the same grid (its own 3 ghost planes read the neighbours' planes)
+    slab = GridLayout(20, 14, 4, precision)
+    for kb, ke, out in cref_chunks(kernel, slab, k_offset=4, kcells_global=lay.kcells, chunk=3, threads=1):
+        for n, r in out.items():
+            lo = kb - slab.kstart + 4
+            want = lay.interior(ref[n])[lo:lo + ke - kb]
+            assert np.allclose(r, want, rtol=0, atol=1e-12 * np.max(np.abs(want))), (n, kb)

@@ -28,7 +28,8 @@ def main(argv=None) -> int:
     ap.add_argument("--precision", default="fp32")
     ap.add_argument("--grid", default="256,256,256")
     ap.add_argument("--variant", action="append", default=[])
-    ap.add_argument("--config", default=None, help="JSON config merged over the wisdom record")
+    ap.add_argument("--config", action="append", default=[],
+                    help="JSON config merged over the wisdom record (repeatable: each is a variant)")
     ap.add_argument("--rounds", type=int, default=5)
     ap.add_argument("--reps", type=int, default=15)
     ap.add_argument("--no-check", action="store_true")
@@ -54,23 +55,23 @@ def main(argv=None) -> int:
     problem = d.derive_problem_size(env)
     comp = NvrtcCompiler(ctx)
     wk = WisdomKernel(d, comp, wisdom_dir=ROOT / "wisdom", capture_policy=CapturePolicy())
-    _, config, kind = wk.resolve(ctx.ident, problem, env)
-    if a.config:
-        config = dict(config, **json.loads(a.config))
-    geom = d.derive_geometry(config, problem, env)
-    base = d.render_compile_request(config, problem, env)
-    variants = a.variant or [""]
-    exes = []
-    for v in variants:
-        extra = tuple(f"-D {x.strip()}" for x in v.split(",") if x.strip())
-        req = CompileRequest(base.source, base.entry, base.defines + extra, base.flags)
-        exe = CudaExecutable(req, comp.compile_image(req, ctx.ident), ctx)
-        exe.load()
-        exes.append(exe)
+    _, record, kind = wk.resolve(ctx.ident, problem, env)
+    configs = [dict(record, **json.loads(c)) for c in a.config] or [record]
+    variants, exes, geoms = [], [], []
+    for config in configs:
+        base = d.render_compile_request(config, problem, env)
+        for v in a.variant or [""]:
+            extra = tuple(f"-D {x.strip()}" for x in v.split(",") if x.strip())
+            req = CompileRequest(base.source, base.entry, base.defines + extra, base.flags)
+            exe = CudaExecutable(req, comp.compile_image(req, ctx.ident), ctx)
+            exe.load()
+            exes.append(exe)
+            geoms.append(d.derive_geometry(config, problem, env))
+            variants.append((v, config))
     args = prob.args()
     outs = []
     if not a.no_check:
-        for exe in exes:
+        for exe, geom in zip(exes, geoms):
             prob.regenerate()
             exe.launch(geom, args, timed=True)
             outs.append({n: prob.download(n).copy() for n in prob.outputs()})
@@ -79,14 +80,14 @@ def main(argv=None) -> int:
     times = [[] for _ in exes]
     for _ in range(a.rounds):
         for i, exe in enumerate(exes):
-            times[i].append(statistics.median(exe.time_launches(geom, args, 3, a.reps, flush=flush)))
+            times[i].append(statistics.median(exe.time_launches(geoms[i], args, 3, a.reps, flush=flush)))
     nbytes = BYTES_PER_CELL_WORDS[a.kernel] * lay.elem_bytes * lay.cells
     peak = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["hbm_gbs"]
     out = open(a.json_out, "a") if a.json_out else None
-    for i, v in enumerate(variants):
+    for i, (v, config) in enumerate(variants):
         t = statistics.median(times[i])
         rec = {"kernel": a.kernel, "precision": a.precision, "grid": list(grid), "variant": v, "config": config,
-               "match_kind": kind, "us": round(t * 1e6, 2), "us_rounds": [round(x * 1e6, 2) for x in times[i]],
+               "blocks": geoms[i].grid[0], "match_kind": kind, "us": round(t * 1e6, 2), "us_rounds": [round(x * 1e6, 2) for x in times[i]],
                "frac": round(nbytes / t / 1e9 / peak, 4)}
         if outs:
             rec["bit_identical_to_first"] = all(np.array_equal(outs[i][n], outs[0][n]) for n in outs[0])
