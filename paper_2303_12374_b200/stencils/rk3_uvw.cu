@@ -11,8 +11,9 @@
 // a thread's cells of one row are TILE_X adjacent elements starting at a
 // multiple of TILE_X from istart, so when the six fields' row starts are
 // aligned to the vector width (always, for the GridLayout pitches; checked
-// at run time, uniformly) each row of the tile is read and written with
-// VA-element vector accesses (VA = min(TILE_X, 16 B)) — 12 / VA memory
+// uniformly: pointers at run time, pitches at compile time) each row of the
+// tile is read and written with VA-element vector accesses (VA =
+// min(TILE_X, 16 B)) — 12 / VA memory
 // instructions per cell instead of 12, which is what keeps an fp32
 // elementwise pass on the HBM roofline.  Any other alignment takes the
 // scalar loop of direct_tiles.
@@ -33,8 +34,11 @@ struct __align__(N * sizeof(real)) Vec {
   real v[N];
 };
 
+// every row start (i = istart) of the field is VA-element aligned: the
+// pointer at istart, and the row / plane pitches (compile-time) in VA steps
 __device__ __forceinline__ bool aligned_rows(const void* p, int istart) {
-  return ((reinterpret_cast<unsigned long long>(p) + static_cast<unsigned long long>(istart) * sizeof(real)) %
+  return KL_JJ % kVA == 0 && KL_KK % kVA == 0 &&
+         ((reinterpret_cast<unsigned long long>(p) + static_cast<unsigned long long>(istart) * sizeof(real)) %
           (kVA * sizeof(real))) == 0;
 }
 

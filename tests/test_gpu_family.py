@@ -171,6 +171,51 @@ def test_family_tma_misaligned_fields_use_scalar_path(gpu_ctx, compiler, kernel)
         prob.close()
 
 
+def test_rk3_vector_config_on_misaligned_fields_takes_the_scalar_path(gpu_ctx, compiler):
+    """rk3_uvw's vector path needs every row start vector-aligned; with the
+    fields shifted one element off the 16-byte grid the same column-tile
+    configuration must take the scalar loop and still match the oracle."""
+    from paper_2303_12374_b200.capture import scalar_env_from_args
+    from paper_2303_12374_b200.cuda import DeviceArray, DeviceBuffer
+    from paper_2303_12374_b200.cuda._abi import check, lib
+    from paper_2303_12374_b200.stencils.layout import GridLayout
+    from paper_2303_12374_b200.stencils.problem import StencilProblem
+
+    precision = "fp32"
+    lay = GridLayout(45, 23, 19, precision)
+    ref, _ = oracle_outputs("rk3_uvw", lay)
+    cfg = dict(_space("rk3_uvw", precision).default_config()[0], contiguous_x=True, tile_x=4, block_x=16, block_y=4)
+    prob = StencilProblem("rk3_uvw", lay, gpu_ctx)
+    shifted, names = {}, {}
+    try:
+        args = []
+        for a in prob.args():
+            if isinstance(a, DeviceBuffer) and a.element_count == lay.span_elems:
+                arr = DeviceArray(lay.alloc_bytes + 64)
+                dst = arr.ptr + lay.elem_bytes
+                check(lib().klb_memcpy_dtod(dst, a.ptr - lay.lead * lay.elem_bytes, lay.alloc_bytes, None))
+                shifted[a.position] = arr
+                a = DeviceBuffer(a.position, a.role, a.element_type, dst + lay.lead * lay.elem_bytes,
+                                 a.element_count, owner=arr)
+            args.append(a)
+        gpu_ctx.synchronize()
+        d = prob.definition
+        env = scalar_env_from_args(args)
+        problem = d.derive_problem_size(env)
+        exe = compiler.compile(d.render_compile_request(cfg, problem, env), gpu_ctx.ident)
+        exe.load()
+        exe.launch(d.derive_geometry(cfg, problem, env), args, timed=True)
+        order = ("ut", "vt", "wt", "u", "v", "w")  # ARG_LAYOUT["rk3_uvw"] buffer order
+        assert sorted(shifted) == list(range(6))
+        for pos, name in enumerate(order):
+            flat = np.frombuffer(shifted[pos].download(lay.alloc_bytes, offset_bytes=lay.elem_bytes), dtype=lay.dtype)
+            assert rel_error(lay.host_view(flat), ref[name], lay) <= TOL[precision], name
+    finally:
+        for arr in shifted.values():
+            arr.free()
+        prob.close()
+
+
 @pytest.mark.parametrize("kernel", ["diff_c", "evisc_smag"])
 @pytest.mark.parametrize("precision", ["fp32", "fp64"])
 def test_family_tma_plane_march_matches_oracle(gpu_ctx, compiler, kernel, precision):
