@@ -50,6 +50,9 @@
                    // halos cost in bytes and time)
 #endif
 
+#ifndef KL_L2PF
+#define KL_L2PF 0  // > 0: also prefetch plane p + KL_L2PF into L2 when plane p is loaded into a ring
+#endif
 #ifndef KL_L2HINT
 #define KL_L2HINT 0  // experiment: L2 eviction priorities, bit 1 = ut loads evict_first, 2 = v/w loads
                      // evict_first, 4 = u loads evict_last, 8 = ut stores evict_first
@@ -218,6 +221,14 @@ struct AdvecTma {
     kl::tma_load_3d(dst + kTO, maps + 3, bar, xt, j0, p);
 #endif
   }
+  // L2 prefetches (KL_L2PF): DRAM reads of planes beyond the rings start
+  // early without costing shared memory
+  __device__ __forceinline__ void prefetch_u(int p) const { kl::tma_prefetch_3d(maps + 0, xu, j0 - 3, p); }
+  __device__ __forceinline__ void prefetch_v(int p) const {
+    kl::tma_prefetch_3d(maps + 1, xv, j0, p);
+    kl::tma_prefetch_3d(maps + 2, xw, j0, p);
+    kl::tma_prefetch_3d(maps + 3, xt, j0, p);
+  }
   // u of plane k0 + d at element offset b of plane k0 (the chunk prologue's
   // unstaged loads, planes k0-3 .. k0+2: below the slab for the first chunk,
   // above it for a last chunk shorter than 3 planes — from the neighbours)
@@ -233,6 +244,10 @@ struct AdvecTma {
   __device__ __forceinline__ void prime() const {
     for (int p = k0; p <= min(k0 + kNU - 1, k1 + 2); ++p) issue_u(p - k0, p);
     for (int p = k0; p <= min(k0 + kNV - 1, k1); ++p) issue_v(p - k0, p);
+#if KL_L2PF > 0 && !KL_PEER
+    for (int p = k0 + kNU; p < min(k0 + kNU + KL_L2PF, k1 + 3); ++p) prefetch_u(p);
+    for (int p = k0 + kNV; p < min(k0 + kNV + KL_L2PF, k1 + 1); ++p) prefetch_v(p);
+#endif
   }
 
   // Ring positions at step k: slots of u planes k, k+3, k-1 and of v/w/ut
@@ -267,6 +282,10 @@ struct AdvecTma {
       kl::fence_proxy_async_smem();
       if (pu <= k1 + 2) issue_u(c.uprev, pu);
       if (pv <= k1) issue_v(c.vprev, pv);
+#if KL_L2PF > 0 && !KL_PEER
+      if (pu + KL_L2PF <= k1 + 2) prefetch_u(pu + KL_L2PF);
+      if (pv + KL_L2PF <= k1) prefetch_v(pv + KL_L2PF);
+#endif
     }
     kl::mbar_wait(bar_u + c.u3, c.ph_u3);
     kl::mbar_wait(bar_v + c.v1, c.ph_v1);

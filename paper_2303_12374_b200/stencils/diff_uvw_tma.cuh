@@ -35,6 +35,9 @@
 #ifndef DEPTH
 #define DEPTH 2
 #endif
+#ifndef KL_L2PF
+#define KL_L2PF 0  // > 0: also prefetch plane p + KL_L2PF into L2 when plane p is loaded into the ring
+#endif
 
 #include "kl_pack.cuh"
 #include "kl_tma.cuh"
@@ -465,6 +468,14 @@ struct DiffTma {
 #pragma unroll
     for (int f = 0; f < 3; ++f) kl::tma_load_3d(dst + 4 * kFS + f * kTS, maps + 4 + f, bar, xt, j0, p);
   }
+  // L2 prefetch of plane p (KL_L2PF): DRAM reads of the planes beyond the
+  // ring start early without costing shared memory
+  __device__ __forceinline__ void prefetch(int p) const {
+#pragma unroll
+    for (int f = 0; f < 4; ++f) kl::tma_prefetch_3d(maps + f, xh[f], j0 - 1, p);
+#pragma unroll
+    for (int f = 0; f < 3; ++f) kl::tma_prefetch_3d(maps + 4 + f, xt, j0, p);
+  }
 
   template <int VA, bool PK = false>
   __device__ __forceinline__ void march() const {
@@ -486,6 +497,9 @@ struct DiffTma {
           kl::fence_proxy_async_smem();
           issue(sprev, p);
         }
+#if KL_L2PF > 0 && !KL_PEER
+        if (p + KL_L2PF <= k1) prefetch(p + KL_L2PF);
+#endif
       }
       kl::mbar_wait(full + sk1, ph1);
       const real* zp = zprof + 5 * (k - k0);
@@ -700,6 +714,9 @@ KL_ENTRY(real* __restrict__ ut, real* __restrict__ vt, real* __restrict__ wt, co
   __syncthreads();
   if (tid == 0) {
     for (int p = kfirst; p <= min(kfirst + kNS - 1, m.k1); ++p) m.issue(p - kfirst, p);
+#if KL_L2PF > 0 && !KL_PEER
+    for (int p = kfirst + kNS; p < min(kfirst + kNS + KL_L2PF, m.k1 + 1); ++p) m.prefetch(p);
+#endif
   }
   // per-plane factors of the chunk (one division per plane and block instead
   // of two per thread and plane; published by the march's first __syncthreads)

@@ -94,6 +94,15 @@ __device__ __forceinline__ void tma_load_3d_hint(void* dst, const TmaDesc* map, 
       : "memory");
 }
 
+// L2 prefetch of a 3-D box (no shared memory, no barrier): the box's DRAM
+// reads start now, and a later tma_load_3d of it hits L2
+__device__ __forceinline__ void tma_prefetch_3d(const TmaDesc* map, int x, int y, int z) {
+  asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global [%0, {%1, %2, %3}];" ::"l"(
+                   reinterpret_cast<unsigned long long>(map)),
+               "r"(x), "r"(y), "r"(z)
+               : "memory");
+}
+
 }  // namespace kl
 
 #endif  // KL_TMA_CUH
