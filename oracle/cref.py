@@ -2,7 +2,9 @@
 
 Runs the C restatement over numpy (kcells, jcells, icells) arrays (contiguous,
 pitch = icells) on a thread pool of z-chunks; used as the timed CPU baseline
-(bench.py) and cross-checked against the NumPy oracle (tests/test_oracle.py).
+(bench.py) and cross-checked against the NumPy oracle (tests/test_oracle.py,
+tests/test_family_oracle.py).  advec_u / diff_uvw: stencil_ref.c (fp32 and
+fp64 arithmetic); the §8f family: family_ref.c (float64 arithmetic).
 """
 
 from __future__ import annotations
@@ -66,6 +68,42 @@ def diff_uvw(ut, vt, wt, e, u, v, w, dzi, dzhi, rhoref, rhorefh, dxi, dyi, ghost
            kr[1])
 
     _map(run, _chunks(gk, kc - gk, threads), threads, pool)
+
+
+def _family(name, arrays, scalars, ghost, threads, pool):
+    """oracle/family_ref.c kernel ``name`` (float64 arrays, in place on the
+    first) over the interior, z-chunks on ``threads``."""
+    if any(a.dtype != np.float64 for a in arrays):
+        raise TypeError("family_ref.c computes in float64")
+    fn = getattr(_lib(), f"{name}_f64")
+    kc, jc, ic = arrays[0].shape
+    gi, gj, gk = ghost
+
+    def run(kr):
+        fn(*(_ptr(a) for a in arrays), *(C.c_double(x) for x in scalars), C.c_int(ic), C.c_ssize_t(ic * jc), gi,
+           ic - gi, gj, jc - gj, kr[0], kr[1])
+
+    _map(run, _chunks(gk, kc - gk, threads), threads, pool)
+
+
+def advec_v(vt, u, v, w, rhoref, rhorefh, dzi, dxi, dyi, ghost=(3, 3, 3), threads=1, pool=None):
+    _family("advec_v", (vt, u, v, w, rhoref, rhorefh, dzi), (dxi, dyi), ghost, threads, pool)
+
+
+def advec_w(wt, u, v, w, rhoref, rhorefh, dzhi, dxi, dyi, ghost=(3, 3, 3), threads=1, pool=None):
+    _family("advec_w", (wt, u, v, w, rhoref, rhorefh, dzhi), (dxi, dyi), ghost, threads, pool)
+
+
+def advec_s(st, s, u, v, w, rhoref, rhorefh, dzi, dxi, dyi, ghost=(3, 3, 3), threads=1, pool=None):
+    _family("advec_s", (st, s, u, v, w, rhoref, rhorefh, dzi), (dxi, dyi), ghost, threads, pool)
+
+
+def diff_c(st, s, evisc, dzi, dzhi, rhoref, rhorefh, dxi, dyi, tpri, ghost=(3, 3, 3), threads=1, pool=None):
+    _family("diff_c", (st, s, evisc, dzi, dzhi, rhoref, rhorefh), (dxi, dyi, tpri), ghost, threads, pool)
+
+
+def evisc_smag(evisc, u, v, w, dzi, dzhi, dxi, dyi, cs, ghost=(3, 3, 3), threads=1, pool=None):
+    _family("evisc_smag", (evisc, u, v, w, dzi, dzhi), (dxi, dyi, cs), ghost, threads, pool)
 
 
 def _map(fn, items, threads, pool):

@@ -109,15 +109,16 @@ def window_error(prob: StencilProblem, kernel: str, kb: int, ke: int) -> dict:
 
 def cref_chunks(kernel: str, layout: GridLayout, k_offset: int = 0, kcells_global: int | None = None,
                 dxi: float = 1.0, dyi: float = 1.0, chunk: int = 32, threads: int | None = None,
-                rk_a: float = RK_A, rk_bdt: float = RK_BDT):
+                rk_a: float = RK_A, rk_bdt: float = RK_BDT, tpri: float = TPRI, cs: float = CS):
     """Yield ``(kb, ke, {output: (ke-kb, jtot, itot) float64})`` over every
     interior plane of ``layout`` (local plane 0 = global plane ``k_offset``):
     the C restatement (oracle/cref, float64 arithmetic on inputs of the
     layout's precision) on z-chunks of ``chunk`` planes, each chunk's inputs
     (+ ghost reach) generated by the C synth twin — host memory stays bounded
-    at any grid size.  advec_u / diff_uvw (the kernels cref restates) and
-    diff_uvw_rk3 (cref's diff_uvw + the RK3 epilogue of
-    family_oracle.diff_uvw_rk3, elementwise in float64)."""
+    at any grid size.  advec_u / diff_uvw (stencil_ref.c), the §8f family
+    advec_v/w/s, diff_c, evisc_smag (family_ref.c), and diff_uvw_rk3 /
+    rk3_uvw (cref's diff_uvw + the RK3 epilogue of family_oracle, elementwise
+    in float64)."""
     import os
 
     from oracle import cref
@@ -151,6 +152,31 @@ def cref_chunks(kernel: str, layout: GridLayout, k_offset: int = 0, kcells_globa
                     f[c + "_next"] = f[c] + rk_bdt * f[t]  # interior cells only are compared
                     f[t] = rk_a * f[t]
                 outs += ("u_next", "v_next", "w_next")
+        elif kernel == "advec_v":
+            cref.advec_v(f["vt"], f["u"], f["v"], f["w"], pf["rhoref"], pf["rhorefh"], pf["dzi"], dxi, dyi, ghost=gh,
+                         threads=threads)
+            outs = ("vt",)
+        elif kernel == "advec_w":
+            cref.advec_w(f["wt"], f["u"], f["v"], f["w"], pf["rhoref"], pf["rhorefh"], pf["dzhi"], dxi, dyi,
+                         ghost=gh, threads=threads)
+            outs = ("wt",)
+        elif kernel == "advec_s":
+            cref.advec_s(f["st"], f["s"], f["u"], f["v"], f["w"], pf["rhoref"], pf["rhorefh"], pf["dzi"], dxi, dyi,
+                         ghost=gh, threads=threads)
+            outs = ("st",)
+        elif kernel == "diff_c":
+            cref.diff_c(f["st"], f["s"], f["evisc"], pf["dzi"], pf["dzhi"], pf["rhoref"], pf["rhorefh"], dxi, dyi,
+                        tpri, ghost=gh, threads=threads)
+            outs = ("st",)
+        elif kernel == "evisc_smag":
+            cref.evisc_smag(f["evisc"], f["u"], f["v"], f["w"], pf["dzi"], pf["dzhi"], dxi, dyi, cs, ghost=gh,
+                            threads=threads)
+            outs = ("evisc",)
+        elif kernel == "rk3_uvw":
+            for c, t in (("u", "ut"), ("v", "vt"), ("w", "wt")):
+                f[c] = f[c] + rk_bdt * f[t]
+                f[t] = rk_a * f[t]
+            outs = ("ut", "vt", "wt", "u", "v", "w")
         else:
             raise ValueError(f"no C restatement of {kernel}")
         yield kb, ke, {n: sub.interior(f[n]) for n in outs}
@@ -161,7 +187,7 @@ def full_volume_error(prob: StencilProblem, kernel: str, chunk: int = 32) -> dic
     device problem (all its local planes), reference = ``cref_chunks``."""
     diff, scale = {}, {}
     for kb, ke, ref in cref_chunks(kernel, prob.layout, prob.k_offset, prob.kcells_global, prob.dxi, prob.dyi,
-                                   chunk, rk_a=prob.rk_a, rk_bdt=prob.rk_bdt):
+                                   chunk, rk_a=prob.rk_a, rk_bdt=prob.rk_bdt, tpri=prob.tpri, cs=prob.cs):
         for n, r in ref.items():
             got = download_planes(prob, n, kb, ke).astype(np.float64)
             d = float(np.max(np.abs(got - r)))

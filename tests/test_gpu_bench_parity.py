@@ -13,8 +13,10 @@ epilogue).
 Bar (BASELINE.json north_star): max|gpu - ref| / max|ref| <= 1e-5 (fp32),
 <= 1e-12 (fp64) per output array.
 
-Cases = BASELINE configs 1-4 (+ the north-star 512^3 fp32 pair and the fused
-RK3 kernel), and config 4's N = 2/4/8 z-slab ranks: the 1024^2 x {511, 254,
+Cases = BASELINE configs 1-4 (+ the north-star 512^3 fp32 pair, the fused
+RK3 kernel and its unfused rk3_uvw baseline, and the §8f family kernels at
+the 512^3 shape the bench's ``family`` rows time), and config 4's N = 2/4/8
+z-slab ranks: the 1024^2 x {511, 254,
 126}-plane interior sub-ranges and single-plane boundary sub-ranges, each
 selected from wisdom for its own shape, exactly as ``bench.py --gpus N``
 launches them on every rank.
@@ -47,10 +49,15 @@ CASES = [
     ("north_star", "diff_uvw", "fp32", (512, 512, 512), "exact"),
     ("§8f fusion", "diff_uvw_rk3", "fp32", (512, 512, 512), "exact"),
     ("§8f fusion", "diff_uvw_rk3", "fp64", (512, 512, 512), "exact"),
-]
+    ("§8f fusion", "rk3_uvw", "fp32", (512, 512, 512), "exact"),
+    ("§8f fusion", "rk3_uvw", "fp64", (512, 512, 512), "exact"),
+] + [("§8f family", k, p, (512, 512, 512), "exact")
+     for k in ("advec_v", "advec_w", "advec_s", "diff_c", "evisc_smag") for p in ("fp32", "fp64")]
 
 
-FULL_VOLUME = ("advec_u", "diff_uvw", "diff_uvw_rk3")  # restated by oracle/cref (+ the RK3 epilogue)
+#: restated in C by oracle/cref (stencil_ref.c, family_ref.c; + the RK3 epilogue)
+FULL_VOLUME = ("advec_u", "diff_uvw", "diff_uvw_rk3", "rk3_uvw", "advec_v", "advec_w", "advec_s", "diff_c",
+               "evisc_smag")
 
 
 def _windows(lay, n=8):

@@ -153,7 +153,9 @@ def test_oracle_window_equals_whole_grid(kernel):
 
 
 @pytest.mark.parametrize("kernel,precision", [("advec_u", "fp32"), ("diff_uvw", "fp64"), ("diff_uvw", "fp32"),
-                                              ("diff_uvw_rk3", "fp64")])
+                                              ("diff_uvw_rk3", "fp64"), ("advec_v", "fp32"), ("advec_w", "fp64"),
+                                              ("advec_s", "fp32"), ("diff_c", "fp64"), ("evisc_smag", "fp32"),
+                                              ("evisc_smag", "fp64"), ("rk3_uvw", "fp32")])
 def test_cref_chunks_cover_the_grid_like_the_numpy_oracle(kernel, precision):
     """The full-volume GPU parity check (stencil_helpers.full_volume_error)
     streams the C restatement over z-chunks with their inputs regenerated per
