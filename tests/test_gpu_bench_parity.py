@@ -15,7 +15,8 @@ Bar (BASELINE.json north_star): max|gpu - ref| / max|ref| <= 1e-5 (fp32),
 
 Cases = BASELINE configs 1-4 (+ the north-star 512^3 fp32 pair, the fused
 RK3 kernel and its unfused rk3_uvw baseline, and the §8f family kernels at
-the 512^3 shape the bench's ``family`` rows time), and config 4's N = 2/4/8
+the 512^3 shape the bench's ``family`` rows time; config 5's runtime
+selection at shapes without a record of their own), and config 4's N = 2/4/8
 z-slab ranks: the 1024^2 x {511, 254,
 126}-plane interior sub-ranges and single-plane boundary sub-ranges, each
 selected from wisdom for its own shape, exactly as ``bench.py --gpus N``
@@ -52,7 +53,14 @@ CASES = [
     ("§8f fusion", "rk3_uvw", "fp32", (512, 512, 512), "exact"),
     ("§8f fusion", "rk3_uvw", "fp64", (512, 512, 512), "exact"),
 ] + [("§8f family", k, p, (512, 512, 512), "exact")
-     for k in ("advec_v", "advec_w", "advec_s", "diff_c", "evisc_smag") for p in ("fp32", "fp64")]
+     for k in ("advec_v", "advec_w", "advec_s", "diff_c", "evisc_smag") for p in ("fp32", "fp64")] + [
+    # config 5: shapes with no record of their own, where runtime selection
+    # picks the nearest tuned problem's configuration (portability.QUERIES)
+    ("config 5", "advec_u", "fp32", (192, 192, 192), "same_device_nearest"),
+    ("config 5", "diff_uvw", "fp64", (384, 384, 384), "same_device_nearest"),
+    ("config 5", "diff_uvw", "fp32", (768, 768, 768), "same_device_nearest"),
+    ("config 5", "advec_u", "fp64", (320, 200, 150), "same_device_nearest"),
+]
 
 
 #: restated in C by oracle/cref (stencil_ref.c, family_ref.c; + the RK3 epilogue)
