@@ -753,15 +753,19 @@ def run_ours(args, dist):
         "e2e": e2e,
     }
     if dist.rank == 0 and dist.world == 1 and not args.no_cpu_baseline:
+        # a bounded sample of the workload sized to ~10 s of CPU work: 32
+        # z-planes per host thread of the same grid, steps repeated
         threads = host_threads()
-        cpu = CpuOracle(kernel, precision, grid, threads)
+        cpu = CpuOracle(kernel, precision, grid, threads, planes_per_thread=32)
+        t0 = time.perf_counter()
         cpu.step()
-        rate, secs = cpu.rate(reps=3)
+        reps = min(30, max(3, round(10.0 / max(time.perf_counter() - t0, 1e-3))))
+        rate, secs = cpu.rate(reps=reps)
         cpu.close()
         line["cpu_baseline"] = {
             "value": round(rate, 5), "unit": "Gcells/s", "cores": threads, "kind": "port",
             "sample": f"{cpu.nk} z-planes ({cpu.cells} cells) of the same grid; {cpu.kind}; {threads} host "
-                      f"threads; median of 3 ({secs:.3f} s each)"}
+                      f"threads; median of {reps} steps ({secs:.3f} s each, {reps * secs:.1f} s of CPU work)"}
     if dist.rank == 0 and dist.world == 1 and args.suite:
         try:
             line["suite"] = suite_measure(ctx, compiler, wisdom_dir, peak, cpu=not args.no_cpu_baseline)
