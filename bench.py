@@ -413,6 +413,33 @@ def timed_steps(driver, dist, steps, time_kernel=True):
     return dist.max(step_s), (dist.max(kern_s) if kern_s is not None else None), launches
 
 
+def same_box_copy_gbs(ctx, nbytes=1 << 31, reps=10):
+    """This box's device-to-device copy bandwidth right now (read + write
+    bytes / time, best of ``reps`` event-timed copies of ``nbytes``) — the
+    MEASURED_PEAKS.json method repeated in the same run, so the kernel's
+    fraction can also be read against the box it ran on (HBM bandwidth
+    differs a few per cent between boxes and clocks)."""
+    from paper_2303_12374_b200.cuda import DeviceArray, Event
+    from paper_2303_12374_b200.cuda._abi import check, lib
+
+    src, dst = DeviceArray(nbytes), DeviceArray(nbytes)
+    s = ctx.stream
+    try:
+        best = float("inf")
+        for i in range(reps + 3):
+            e0, e1 = Event(), Event()
+            e0.record(s)
+            check(lib().klb_memcpy_dtod(dst.ptr, src.ptr, nbytes, s.handle))
+            e1.record(s)
+            e1.synchronize()
+            if i >= 3:
+                best = min(best, e0.elapsed_ms(e1) * 1e-3)
+        return 2 * nbytes / best / 1e9
+    finally:
+        src.free()
+        dst.free()
+
+
 def run_e2e(driver, dist, steps, chunks, copy_streams=1):
     """End to end through the public API: every step streams all fields from
     pinned host memory and the tendencies back (``SlabDriver.step_host``:
@@ -736,6 +763,12 @@ def run_ours(args, dist):
                 "peak_source": peak_src, "frac_of_8tbs": round(achieved / 8000.0, 4)}
     if traffic_src:
         roofline["traffic_source"] = f"profiles/{traffic_src}"
+    try:
+        box = same_box_copy_gbs(ctx)
+        roofline["same_box_copy_gbs"] = round(box, 1)
+        roofline["frac_of_same_box_copy"] = round(achieved / box, 4)
+    except Exception as err:  # diagnostic only
+        roofline["same_box_copy_gbs"] = repr(err)[:120]
 
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": "Gcells/s", "n_gpus": dist.world, "steps": args.steps,
