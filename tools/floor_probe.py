@@ -35,6 +35,30 @@ extern "C" __global__ void flush_k(unsigned* buf, unsigned long long n, unsigned
   for (unsigned long long t = blockIdx.x * 256ull + threadIdx.x; t < n / 16; t += gridDim.x * 256ull)
     reinterpret_cast<uint4*>(buf)[t] = make_uint4(seed, seed + 1, seed + 2, t);
 }
+// the stencil's traversal without its ring: a block of 64 threads owns a
+// 64 x 8 column tile (thread tile 4 x 2) and marches ZC planes, each thread
+// reading its cells of u, v, w, ut with float4 loads and writing ut
+extern "C" __global__ void __launch_bounds__(64) march4(float* __restrict__ ut, const float* __restrict__ u,
+    const float* __restrict__ v, const float* __restrict__ w, int jj, int kk, int istart, int jstart, int kstart,
+    int itot, int jtot, int ktot, int zc) {
+  const int nbx = itot / 64, nby = jtot / 8;
+  const int b = blockIdx.x, bx = b % nbx, by = (b / nbx) % nby, bz = b / (nbx * nby);
+  const int i = istart + bx * 64 + (threadIdx.x % 16) * 4, j = jstart + by * 8 + (threadIdx.x / 16) * 2;
+  const int k0 = kstart + bz * zc;
+#pragma unroll 2
+  for (int k = k0; k < k0 + zc; ++k) {
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+      const long long o = i + static_cast<long long>(j + t) * jj + static_cast<long long>(k) * kk;
+      const float4 a = __ldcs(reinterpret_cast<const float4*>(u + o));
+      const float4 bb = __ldcs(reinterpret_cast<const float4*>(v + o));
+      const float4 c = __ldcs(reinterpret_cast<const float4*>(w + o));
+      float4 d = *reinterpret_cast<const float4*>(ut + o);
+      d.x += a.x + bb.x + c.x; d.y += a.y + bb.y + c.y; d.z += a.z + bb.z + c.z; d.w += a.w + bb.w + c.w;
+      __stcs(reinterpret_cast<float4*>(ut + o), d);
+    }
+  }
+}
 extern "C" __global__ void __launch_bounds__(256) stream4(float* __restrict__ ut, const float* __restrict__ u,
     const float* __restrict__ v, const float* __restrict__ w, int jj, int kk, int istart, int jstart, int kstart,
     int itot, int jtot, int ktot) {
@@ -112,6 +136,14 @@ def main(argv=None) -> int:
                           ("gridstride_148x4", 148 * 4), ("gridstride_148x16", 148 * 16)):
         g = LaunchGeometry((256, 1, 1), (blocks, 1, 1), 0)
         res[f"stream4r1w_{label}"] = row(st.time_launches(g, sargs, 3, a.reps, flush=flush))
+
+    mk = comp.compile(CompileRequest(SRC, "march4", (), ("-std=c++17",)), ctx.ident)
+    mk.load()
+    for zc in (256, 64, 32, 16, 8, 4):
+        margs = sargs + [ScalarArg(12, "i32", zc)]
+        nblk = (grid[0] // 64) * (grid[1] // 8) * (grid[2] // zc)
+        res[f"march4_64x8_zchunk{zc}_{nblk}blocks"] = row(
+            mk.time_launches(LaunchGeometry((64, 1, 1), (nblk, 1, 1), 0), margs, 3, a.reps, flush=flush))
 
     # shared-memory carveout: the empty kernel with no dynamic shared memory,
     # and the empty kernel / the record after a flush done by a kernel that
