@@ -119,9 +119,14 @@ def main(argv=None) -> int:
     comp = NvrtcCompiler(ctx)
     wk = WisdomKernel(d, comp, wisdom_dir=ROOT / "wisdom", capture_policy=CapturePolicy())
     _, record, _ = wk.resolve(ctx.ident, problem, env)
+    from paper_2303_12374_b200.backend import CompileError
+
     runs = []
     for label, cfg in variants(d.space, record):
-        exe = comp.compile(d.render_compile_request(cfg, problem, env), ctx.ident)
+        try:  # (a space point a kernel does not implement — e.g. ZMARCH of the family — fails to compile)
+            exe = comp.compile(d.render_compile_request(cfg, problem, env), ctx.ident)
+        except CompileError:
+            continue
         exe.load()
         runs.append((label, cfg, exe, d.derive_geometry(cfg, problem, env)))
     args = prob.args()
