@@ -146,3 +146,54 @@ def test_slab_rank_subranges_match_oracle(gpu_ctx, compiler, nranks):
     interior = {2: 511, 4: 254, 8: 126}[nranks]
     assert shapes["interior"] == interior and shapes.get("lower", shapes.get("upper")) == 1
     assert worst <= TOL["fp32"], errors
+
+
+@pytest.mark.parametrize("nranks", [2, 8])
+def test_fused_halo_slab_matches_oracle(gpu_ctx, compiler, nranks):
+    """Config 4 at N ranks with the fused halo (``--halo fused``): rank 1's
+    ONE slab launch of diff_uvw_peer, selected from the committed diff_uvw
+    wisdom for the slab's shape, reads the planes outside its slab from its
+    neighbours' fields (virtual ranks on this device: separate allocations
+    generated at their own global planes), its own ghost planes poisoned —
+    checked over every cell of the slab."""
+    from paper_2303_12374_b200.halo import LocalPeers
+    from paper_2303_12374_b200.slab import SlabDriver
+    from paper_2303_12374_b200.stencils.problem import PEER_KERNELS
+
+    grid = (1024, 1024, 1024)
+    ranks = [r for r in (0, 1, 2) if r < nranks]
+    peers = LocalPeers([])
+    drivers = {}
+    try:
+        for r in ranks:
+            fused = r == 1
+            drivers[r] = SlabDriver("diff_uvw", "fp32", grid, gpu_ctx, rank=r, nranks=nranks, compiler=compiler,
+                                    wisdom_dir=WISDOM, halo="fused" if fused else "exchange",
+                                    exchanger=peers.for_rank(r) if fused else None)
+        fields = PEER_KERNELS["diff_uvw_peer"]
+        peers.ranks = [({n: drivers[r].problem.field_ptr(n) for n in fields}, drivers[r].layout.kstart,
+                        drivers[r].layout.kend) if r in drivers else ({}, 0, 0) for r in range(max(ranks) + 1)]
+        drv = drivers[1]
+        lay = drv.layout
+        plane = lay.kk * lay.elem_bytes
+        from paper_2303_12374_b200.cuda._abi import check, lib
+
+        for n in fields:  # the fused launch must never read its own ghost planes
+            base = drv.problem.field_ptr(n)
+            check(lib().klb_memset_d8(base + (lay.kstart - lay.kgc) * plane, 0xFF, lay.kgc * plane, None))
+            if drv.above >= 0:
+                check(lib().klb_memset_d8(base + lay.kend * plane, 0xFF, lay.kgc * plane, None))
+        gpu_ctx.synchronize()
+        chosen = drv.resolve()
+        assert drv.step() == 1
+        gpu_ctx.synchronize()
+        errors = {"all planes": full_volume_error(drv.problem, "diff_uvw")}
+    finally:
+        for d in drivers.values():
+            d.close()
+    worst = max(errors["all planes"].values())
+    _record({"case": f"config 4 fused-halo slab rank 1 of {nranks}", "selection":
+             {n: {"match_kind": k, "config": c} for n, (c, k) in chosen.items()}, "worst_rel_err": worst,
+             "checked": f"every interior cell of the slab ({lay.cells})", "errors": errors})
+    assert chosen["slab"][1] == "exact"
+    assert worst <= TOL["fp32"], errors
