@@ -380,11 +380,12 @@ def workload_config(args, kernel, precision, grid, label, world):
     from paper_2303_12374_b200.stencils.problem import KERNEL_FIELDS
 
     wisdom_dir = Path(args.wisdom)
-    nf, field = len(KERNEL_FIELDS[kernel]), GridLayout(*grid, precision).alloc_bytes
+    nf, field = len(KERNEL_FIELDS[kernel]), GridLayout(*grid, precision, align_bytes=args.row_align).alloc_bytes
     l2 = (f"inputs larger than L2 ({nf} fields x {field / 1e9:.2f} GB), no flush" if nf * field > 2 * 126e6
           else f"working set {nf * field / 1e6:.0f} MB (under 2x L2), no flush")
     return {"workload": label, "kernel": kernel, "precision": precision, "grid": list(grid),
-            "decomposition": f"z-slab x{world}", "parallelism": f"slab{world}", "ghost_cells": 3, "l2": l2,
+            "decomposition": f"z-slab x{world}", "parallelism": f"slab{world}", "ghost_cells": 3,
+            "row_align_bytes": args.row_align, "l2": l2,
             "wisdom": str(wisdom_dir.relative_to(ROOT)) if wisdom_dir.is_relative_to(ROOT) else str(wisdom_dir)}
 
 
@@ -612,7 +613,7 @@ def other_halo_variant(args, dist, driver, kernel, precision, grid, ctx, exchang
 
     mode = "exchange" if driver.fused else "fused"
     other = SlabDriver(kernel, precision, grid, ctx, rank=dist.rank, nranks=dist.world, exchanger=exchanger,
-                       compiler=compiler, wisdom_dir=wisdom_dir, halo=mode)
+                       compiler=compiler, wisdom_dir=wisdom_dir, halo=mode, align_bytes=args.row_align)
     try:
         other.resolve()
         for _ in range(args.warmup):
@@ -692,7 +693,8 @@ def run_ours(args, dist):
     for variant, wdir in (("tuned", wisdom_dir), ("default", empty)):
         # (the Table-2 default is a DIRECT configuration: it has no TMA staging to fuse the halo into)
         driver = SlabDriver(kernel, precision, grid, ctx, rank=dist.rank, nranks=dist.world, exchanger=exchanger,
-                            compiler=compiler, wisdom_dir=wdir, halo=halo if variant == "tuned" else "exchange")
+                            compiler=compiler, wisdom_dir=wdir, halo=halo if variant == "tuned" else "exchange",
+                            align_bytes=args.row_align)
         chosen = driver.resolve()
         for _ in range(args.warmup):
             driver.step()
@@ -737,7 +739,8 @@ def run_ours(args, dist):
         try:
             if driver.fused:  # the host-streamed step runs the exchange variant
                 host_driver = SlabDriver(kernel, precision, grid, ctx, rank=dist.rank, nranks=dist.world,
-                                         exchanger=exchanger, compiler=compiler, wisdom_dir=wisdom_dir)
+                                         exchanger=exchanger, compiler=compiler, wisdom_dir=wisdom_dir,
+                                         align_bytes=args.row_align)
             e2e_s, h2d, d2h, launches = run_e2e(host_driver, dist, args.e2e_steps, args.e2e_chunks,
                                                 args.e2e_streams)
             e2e = {"value": round(cells_total / e2e_s / 1e9, 4), "unit": "Gcells/s", "h2d_bytes_per_step": h2d,
@@ -836,6 +839,8 @@ def main(argv=None):
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--e2e-chunks", type=int, default=16)
     ap.add_argument("--e2e-streams", type=int, default=1, help="copy streams per direction in the e2e step")
+    ap.add_argument("--row-align", type=int, default=int(os.environ.get("KL_ROW_ALIGN", "16")),
+                    help="row-pitch quantum of the fields in bytes (GridLayout.align_bytes; 16 = densest rows)")
     ap.add_argument("--halo", choices=("exchange", "fused"), default=os.environ.get("KL_HALO", "exchange"),
                     help="N > 1, IPC transport: 'exchange' = interior launch overlapped with the halo pulls, then "
                          "the boundary launches; 'fused' = one diff_uvw_peer launch per slab reading the planes "

@@ -45,7 +45,8 @@ FUSED_HALO = {"diff_uvw": "diff_uvw_peer", "advec_u": "advec_u_peer", "diff_uvw_
 class SlabDriver:
     def __init__(self, kernel: str, precision: str, grid: tuple[int, int, int], ctx: DeviceContext, *,
                  rank: int = 0, nranks: int = 1, exchanger=None, compiler=None,
-                 wisdom_dir: str | Path | None = None, ghost: int = 3, halo: str = "exchange") -> None:
+                 wisdom_dir: str | Path | None = None, ghost: int = 3, halo: str = "exchange",
+                 align_bytes: int = 128) -> None:
         from .cuda.compiler import NvrtcCompiler
 
         if halo not in ("exchange", "fused"):
@@ -59,10 +60,12 @@ class SlabDriver:
         self.ctx = ctx
         self.rank, self.nranks = rank, nranks
         self.exchanger = exchanger
-        self.global_layout = GridLayout(*grid, precision, ghost, ghost, ghost)
+        # ``align_bytes``: the row-pitch quantum of the fields (stencils/layout.py);
+        # 16 packs rows densely (less padding to stream in step_host)
+        self.global_layout = GridLayout(*grid, precision, ghost, ghost, ghost, align_bytes)
         self.decomposition = SlabDecomposition(grid[2], nranks)
         self.slab = SlabRank(self.decomposition, rank, ghost, kernel)
-        self.layout = GridLayout(grid[0], grid[1], self.slab.count, precision, ghost, ghost, ghost)
+        self.layout = GridLayout(grid[0], grid[1], self.slab.count, precision, ghost, ghost, ghost, align_bytes)
         profiles = make_profiles(self.global_layout.kcells, ghost)
         self.compute = ctx.stream
         self.comm = Stream.create() if exchanger is not None and not self.fused else None

@@ -119,6 +119,32 @@ def test_wisdom_selected_kernel_matches_oracle(gpu_ctx, compiler, tag, kernel, p
     assert worst <= TOL[precision], errors
 
 
+@pytest.mark.parametrize("align", [16])
+def test_bench_row_pitch_matches_oracle(gpu_ctx, compiler, align):
+    """Config 4 on the layout the bench runs it on (``bench.py --row-align``,
+    default 16: rows packed at 16-byte pitch, so the host-streamed step moves
+    no padding): the whole 1024^3 grid through the committed wisdom, every
+    interior cell against the oracle."""
+    from paper_2303_12374_b200.slab import SlabDriver
+
+    drv = SlabDriver("diff_uvw", "fp32", (1024, 1024, 1024), gpu_ctx, compiler=compiler, wisdom_dir=WISDOM,
+                     align_bytes=align)
+    try:
+        assert drv.layout.jj == 1032 and drv.layout.align_bytes == align
+        chosen = drv.resolve()
+        drv.step()
+        gpu_ctx.synchronize()
+        errors = {"all planes": full_volume_error(drv.problem, "diff_uvw")}
+    finally:
+        drv.close()
+    worst = max(errors["all planes"].values())
+    _record({"case": f"config 4, {align}-byte row pitch", "selection":
+             {n: {"match_kind": k, "config": c} for n, (c, k) in chosen.items()}, "worst_rel_err": worst,
+             "checked": "every interior cell (1073741824)", "errors": errors})
+    assert all(k == "exact" for _, k in chosen.values())
+    assert worst <= TOL["fp32"], errors
+
+
 @pytest.mark.parametrize("nranks", [2, 4, 8])
 def test_slab_rank_subranges_match_oracle(gpu_ctx, compiler, nranks):
     """Config 4 at N ranks: rank 1's slab (interior sub-range + its boundary

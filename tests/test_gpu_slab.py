@@ -228,8 +228,9 @@ def test_nccl_single_rank_exchange_is_a_noop(gpu_ctx):
     assert ver.value >= 22700
 
 
-@pytest.mark.parametrize("kernel,copy_streams", [("advec_u", 1), ("diff_uvw", 1), ("diff_uvw", 2), ("advec_u", 3)])
-def test_host_streamed_step_matches_device_step(gpu_ctx, tmp_path, kernel, copy_streams):
+@pytest.mark.parametrize("kernel,copy_streams,align", [("advec_u", 1, 128), ("diff_uvw", 1, 128), ("diff_uvw", 2, 128),
+                                                      ("advec_u", 3, 128), ("diff_uvw", 1, 16), ("advec_u", 2, 16)])
+def test_host_streamed_step_matches_device_step(gpu_ctx, tmp_path, kernel, copy_streams, align):
     """SlabDriver.step_host (fields in pinned host memory, chunked H2D |
     launch | D2H on overlapped streams, one or several copy streams per
     direction) returns the same tendencies as step() on device-resident
@@ -246,8 +247,10 @@ def test_host_streamed_step_matches_device_step(gpu_ctx, tmp_path, kernel, copy_
     cfg.update(staging="TMA", zchunk=8, block_x=32, block_y=4, depth=2)
     WisdomFile(d.kernel_key(), records=[WisdomRecord(gpu_ctx.ident, (1, 1, 1), cfg, 1.0)]).save(
         tmp_path / f"{d.kernel_key()}.wisdom")
-    drv = SlabDriver(kernel, precision, grid, gpu_ctx, compiler=NvrtcCompiler(gpu_ctx), wisdom_dir=tmp_path)
+    drv = SlabDriver(kernel, precision, grid, gpu_ctx, compiler=NvrtcCompiler(gpu_ctx), wisdom_dir=tmp_path,
+                     align_bytes=align)
     prob, lay = drv.problem, drv.layout
+    assert lay.align_bytes == align
     nbytes = lay.alloc_bytes
     host = {}
     for n in prob.fields:
