@@ -1,3 +1,5 @@
+# headline record vs two runners-up under the bench loop on the 16-byte pitch; w_a / w_b were temporary
+# copies of wisdom/ with the 1024^3 diff_uvw fp32 record replaced (64x2/2x4/zchunk 128, 32x4/4x2/zchunk 128)
 OUT=gpurun_out/r05q; mkdir -p $OUT
 for i in 1 2 3; do
   for w in wisdom w_a w_b; do
